@@ -1,0 +1,365 @@
+#!/usr/bin/env python
+"""Benchmark: A^T A effective GFLOP/s (m*n^2/time), fp64, on 1..8 B200s.
+
+Default workload (BASELINE.json): config c4 -- A 65536 x 32768 fp64,
+U[-1,1] from seed 3 (numpy default_rng, host-generated, then H2D), lower
+triangle of C = A^T A, threshold "auto" (GPU plan).  At N>1 the rows of A are
+sharded over the ranks (each rank draws only its rows of the same seeded
+stream) and the packed lower-triangle partials are summed with NCCL
+(paper_2110_13042_b200.dist).  ``--config c2|c3|c5`` selects another config.
+
+One JSON line on rank 0 (the driver contract):
+  value      = m*n^2 / t / 1e9 for the whole job, t = max over ranks of the
+               CUDA-event time of the K timed steps / K (inputs resident in HBM)
+  e2e        = same metric through the public ``ata()`` call with pinned HOST
+               buffers (H2D of A and C, D2H of C inside the timed region; N=1)
+  roofline   = dominant kernel (the fused product kernel) against the measured
+               FP64 DMMA peak (profiles/fp64_peak.txt) or the TF32 peak
+  cpu_baseline = the CPU oracle port of the reference (oracle/atamul_oracle.py,
+               threaded like the reference's AtA-S) on a bounded sample
+``--impl reference`` instead times that CPU port alone (rank 0), same metric.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+# Measured on this pool's B200 (profiles/fp64_peak.txt, tools/microbench/fp64_peak.cu):
+# DMMA m8n8k4 issue-rate peak; cuBLAS DGEMM 8192^3 reached 35.5-36.3 TF/s on the same box.
+FP64_PEAK_TFLOPS = 37.17
+# TF32: cuBLAS TF32 GEMM measured 766-839 TF/s (profiles/fp64_peak.txt); nominal dense 1100.
+TF32_PEAK_TFLOPS = 839.0
+CPU_SAMPLE = {"c4": (16384, 4096), "c3": (16384, 4096), "c2": (6001, 4097), "c5": (65536, 2048),
+              "c1": (1024, 1024)}
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--config", default="c4", choices=["c1", "c2", "c3", "c4", "c5"])
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu", action="store_true")
+    p.add_argument("--leaf-cols", type=int, default=None)
+    p.add_argument("--strassen-min", type=int, default=None)
+    return p.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.summary = {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        if self.proc is None:
+            return False
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        self.summary = {"sm_mhz": statistics.median(sm) if sm else None,
+                        "sm_max_mhz": max(smax) if smax else None,
+                        "reasons": sorted(reasons), "samples": len(sm)}
+        return False
+
+
+def launch_units(plan):
+    """Split a plan into the launches the native executor issues (consecutive
+    same-group products form one launch), with algorithmic flops per unit."""
+    from paper_2110_13042_b200 import _native as nat
+    ops = plan.ops
+    units = []
+    i = 0
+    while i < len(ops):
+        t = int(ops[i]["type"])
+        j = i + 1
+        if t in (nat.OP_GEMM, nat.OP_SYRK) and int(ops[i]["group"]) >= 0:
+            g = int(ops[i]["group"])
+            while j < len(ops) and int(ops[j]["type"]) in (nat.OP_GEMM, nat.OP_SYRK) \
+                    and int(ops[j]["group"]) == g:
+                j += 1
+        flops = 0
+        for op in ops[i:j]:
+            ot = int(op["type"])
+            m, n, k = int(op["m"]), int(op["n"]), int(op["k"])
+            if ot == nat.OP_GEMM:
+                flops += 2 * m * n * k
+            elif ot == nat.OP_SYRK:
+                flops += m * n * (n + 1)
+        units.append((i, j, t in (nat.OP_GEMM, nat.OP_SYRK), flops))
+        i = j
+    # the executor splits groups beyond 32 products into several launches
+    launches = 0
+    for (i, j, is_prod, _) in units:
+        launches += -(-(j - i) // 32) if is_prod else 1
+    return units, launches
+
+
+def cpu_sample_rate(cfg_name, cores):
+    """Oracle port (threaded AtA-S restatement) on a bounded sample of the
+    config's own seeded stream; returns (eff GFLOP/s, seconds, sample text)."""
+    from oracle import atamul_oracle as O
+    from paper_2110_13042_b200.measure import CONFIGS, config_matrix
+    r, c = CPU_SAMPLE[cfg_name]
+    a = config_matrix(cfg_name, rows=r)[:, :c]
+    a = np.ascontiguousarray(a)
+    t = 1 << 19
+    t0 = time.perf_counter()
+    O.ata_shared(a, procs=cores, t=t)
+    dt = time.perf_counter() - t0
+    sample = (f"first {r} rows x {c} cols of {cfg_name}'s seeded A, oracle port of the reference "
+              f"AtA-S (threads={cores}, threshold={t})")
+    return r * c * c / dt / 1e9, dt, sample
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    cores = os.cpu_count() or 1
+    from paper_2110_13042_b200.measure import CONFIGS
+    cfg = CONFIGS[args.config]
+    rates = []
+    for i in range(args.warmup + args.steps):
+        rate, dt, sample = cpu_sample_rate(args.config, cores)
+        if i >= args.warmup:
+            rates.append((rate, dt))
+    value = statistics.median(r for r, _ in rates)
+    ms = statistics.median(d for _, d in rates) * 1e3
+    line = {"metric": "AtA effective GFLOP/s (m*n^2/time)", "value": value, "unit": "GFLOP/s",
+            "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64" if cfg["dtype"] == "f64" else "f32", "data": "synthetic",
+            "config": {"workload": f"{args.config}: A {cfg['m']}x{cfg['n']} {cfg['dtype']}",
+                       "sample": sample},
+            "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": cores, "kind": "port",
+                             "sample": sample},
+            "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    world, rank, local = dist_env()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+    import torch
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+    import paper_2110_13042_b200 as P
+    from paper_2110_13042_b200 import _native as nat, dist as pdist, engine, planner
+    from paper_2110_13042_b200.measure import CONFIGS
+
+    cfg = CONFIGS[args.config]
+    m, n = cfg["m"], cfg["n"]
+    f64 = cfg["dtype"] == "f64"
+    np_dt = np.float64 if f64 else np.float32
+    precision = "fp32" if f64 else "tf32"
+    threshold = cfg["threshold"]
+    r0, r1 = pdist.shard_rows(m, world, rank)
+    # ---- inputs: seeded host draw of this rank's rows, then H2D ----
+    t_gen = time.perf_counter()
+    if cfg["dist"] == "uniform":
+        host = pdist.uniform_rows(m, n, cfg["seed"], r0, r1, np_dt)
+    else:
+        host = np.random.default_rng(cfg["seed"]).standard_normal((m, n))[r0:r1].astype(np_dt)
+    t_gen = time.perf_counter() - t_gen
+    A = torch.from_numpy(host).to(dev)
+    C = torch.zeros((n, n), dtype=A.dtype, device=dev)
+    packed = torch.empty(n * (n + 1) // 2, dtype=A.dtype, device=dev) if world > 1 else None
+    params = planner.AutoParams(**{k: v for k, v in (("leaf_cols", args.leaf_cols),
+                                                      ("strassen_min", args.strassen_min)) if v})
+    mloc = r1 - r0
+    if threshold == "auto":
+        plan = planner.plan_ata_auto(mloc, n, n, n, params)
+        wsbuf = None
+    else:
+        ws = P.workspace_for_ata(mloc, n, threshold, dtype=np_dt)
+        plan = planner.plan_ata_reference(mloc, n, n, n, threshold, ws.level_offsets())
+        wsbuf = ws.ensure(dev)
+    units, n_launch = launch_units(plan)
+    code = nat.dtype_code(A.dtype, precision)
+    a_elems, c_elems = A.numel(), C.numel()
+    wptr = int(wsbuf.data_ptr()) if wsbuf is not None else 0
+    wel = int(wsbuf.numel()) if wsbuf is not None else 0
+    stream = torch.cuda.current_stream()
+    sptr = int(stream.cuda_stream)
+
+    class SubPlan:
+        def __init__(self, ops):
+            self.ops = ops
+
+    sub = [SubPlan(np.ascontiguousarray(plan.ops[i:j])) for (i, j, _, _) in units]
+
+    def step(events=None):
+        C.zero_()
+        for u, sp in enumerate(sub):
+            if events is not None:
+                events[u][0].record(stream)
+            engine.run_plan(sp, code, int(A.data_ptr()), a_elems, int(C.data_ptr()), c_elems, 1.0,
+                            ws=wptr, ws_elems=wel, stream=sptr)
+            if events is not None:
+                events[u][1].record(stream)
+        if world > 1:
+            P.pack_lower(C, out=packed)
+            pdist.reduce_packed(packed, 0)
+            if rank == 0:
+                P.unpack_lower(P.PackedLowerTriangular(n, packed), C)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    ev = [[(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in units] for _ in range(args.steps)]
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        barrier()
+        e0.record(stream)
+        for s in range(args.steps):
+            step(ev[s])
+        e1.record(stream)
+        barrier()
+    total_ms = e0.elapsed_time(e1)
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([total_ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms = float(t.item())
+    ms_step = total_ms / args.steps
+    value = m * n * n / (ms_step * 1e-3) / 1e9
+    # ---- roofline of the dominant kernel (fused product kernel) ----
+    prod_ms, prod_flops, ew_ms = 0.0, 0, 0.0
+    for s in range(args.steps):
+        for u, (i, j, is_prod, fl) in enumerate(units):
+            d = ev[s][u][0].elapsed_time(ev[s][u][1])
+            if is_prod:
+                prod_ms += d
+                prod_flops += fl
+            else:
+                ew_ms += d
+    prod_launches = sum(-(-(j - i) // 32) for (i, j, p, _) in units if p) * args.steps
+    achieved = prod_flops / (prod_ms * 1e-3) / 1e12 if prod_ms > 0 else 0.0
+    peak = FP64_PEAK_TFLOPS if f64 else TF32_PEAK_TFLOPS
+    roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
+                "frac": achieved / peak, "traffic": None,
+                "kernel": "prod_f64_kernel" if f64 else "prod_f32_kernel",
+                "peak_source": ("measured DMMA m8n8k4 issue-rate peak on this pool's B200 "
+                                "(profiles/fp64_peak.txt); MEASURED_PEAKS.json has no FP64 figure")
+                if f64 else "measured cuBLAS TF32 GEMM on this pool's B200 (profiles/fp64_peak.txt)",
+                "share_of_step": prod_ms / total_ms if total_ms else None,
+                "executed_flops_per_step": prod_flops // args.steps,
+                "algorithmic_flops_per_step": m * n * n,
+                "avg_launch_ms": prod_ms / max(1, prod_launches)}
+    line = {"metric": "AtA effective GFLOP/s (m*n^2/time)", "value": value, "unit": "GFLOP/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "f64" if f64 else "f32 (tf32 products)", "data": "synthetic",
+            "config": {"workload": f"{args.config}: A {m}x{n} {cfg['dtype']} "
+                                   f"{cfg['dist']} seed {cfg['seed']}, lower(A^T A), "
+                                   f"threshold {threshold}",
+                       "parallelism": f"row-shard x{world}" if world > 1 else "single GPU",
+                       "l2": "inputs larger than L2 (A is %.1f GB)" % (A.numel() * A.element_size() / 1e9),
+                       "plan": {"kind": plan.kind, "ops": len(plan.ops), "launches": n_launch,
+                                "executed_mults": plan.mults,
+                                "mults_over_classical": plan.mults / (mloc * n * (n + 1) / 2)},
+                       "effective_pct_of_peak": value / 1e3 / peak},
+            "roofline": roofline,
+            "clocks": clk.summary,
+            "gpu_launches": n_launch * args.steps + (3 * args.steps if world > 1 else 0) + args.steps,
+            "input_gen_s": t_gen}
+    # ---- e2e through the public API with pinned host buffers (N = 1) ----
+    if world == 1 and not args.no_e2e:
+        del C
+        torch.cuda.empty_cache()
+        hA = torch.from_numpy(host).pin_memory()
+        hC = torch.zeros((n, n), dtype=A.dtype).pin_memory()
+        del A
+        torch.cuda.empty_cache()
+        kw = dict(threshold=threshold, precision=precision)
+        if threshold == "auto":
+            kw["auto_params"] = params
+        P.ata(hA, hC, 1.0, **kw)     # warm (plan cache, allocator)
+        times = []
+        for _ in range(max(1, min(args.steps, 3))):
+            hC.zero_()
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            P.ata(hA, hC, 1.0, **kw)
+            torch.cuda.synchronize()
+            times.append(time.perf_counter() - t0)
+        te = statistics.median(times)
+        line["e2e"] = {"value": m * n * n / te / 1e9, "unit": "GFLOP/s",
+                       "h2d_bytes_per_step": hA.numel() * hA.element_size() + hC.numel() * hC.element_size(),
+                       "d2h_bytes_per_step": hC.numel() * hC.element_size(),
+                       "ms_per_step": te * 1e3, "api": "paper_2110_13042_b200.ata(host pinned A, C)"}
+    if rank == 0 and world == 1 and not args.no_cpu:
+        cores = os.cpu_count() or 1
+        rate, dt, sample = cpu_sample_rate(args.config, cores)
+        line["cpu_baseline"] = {"value": rate, "unit": "GFLOP/s", "cores": cores, "kind": "port",
+                                "sample": sample, "seconds": dt}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,35 @@
+"""paper_2110_13042_b200 — B200-native AtA (C = alpha*A^T A + C, lower triangle,
+Strassen sub-kernel) behind the reference ``atamul`` entry points.
+
+Drop-in surface (reference pkg/src/atamul/__init__.py:9-27, hot path only):
+``ata``, ``ata_full``, ``ata_mult_count``, ``workspace_for_ata``,
+``fast_strassen``, ``workspace_for``, ``strassen_mult_count``,
+``DEFAULT_THRESHOLD``, ``StrassenWorkspace``, ``naive_gemm_atb``,
+``naive_syrk_lower``, ``add_truncated``, ``mirror_lower_to_upper``,
+``pack_lower``/``unpack_lower``/``PackedLowerTriangular``, ``split4``,
+``DenseMatrix``/``MatrixView``, ``MultCounter``, ``effective_gflops``,
+``gen_matrix``, the exception classes, and the multi-GPU entry ``ata_dist``.
+"""
+from .ata import AUTO, ata, ata_full, ata_mult_count, workspace_for_ata
+from .errors import (AtamulError, InvalidMeasurementError, NativeError, ProtocolError,
+                     ShapeMismatchError, TooManyWorkersError, UnknownProcessError,
+                     UnsplittableError, UnsupportedSizeError, WorkspaceUndersizedError)
+from .matrix import (DenseMatrix, MatrixView, MultCounter, PackedLowerTriangular, add_truncated,
+                     count_allocations, mirror_lower_to_upper, naive_gemm_atb, naive_syrk_lower,
+                     pack_lower, split4, unpack_lower)
+from .measure import check_tolerance, effective_gflops, gen_matrix
+from .strassen import fast_strassen, strassen_mult_count, workspace_for
+from .workspace import DEFAULT_THRESHOLD, StrassenWorkspace
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "AUTO", "AtamulError", "DEFAULT_THRESHOLD", "DenseMatrix", "InvalidMeasurementError",
+    "MatrixView", "MultCounter", "NativeError", "PackedLowerTriangular", "ProtocolError",
+    "ShapeMismatchError", "StrassenWorkspace", "TooManyWorkersError", "UnknownProcessError",
+    "UnsplittableError", "UnsupportedSizeError", "WorkspaceUndersizedError", "add_truncated",
+    "ata", "ata_full", "ata_mult_count", "check_tolerance", "count_allocations",
+    "effective_gflops", "fast_strassen", "gen_matrix", "mirror_lower_to_upper",
+    "naive_gemm_atb", "naive_syrk_lower", "pack_lower", "split4", "strassen_mult_count",
+    "unpack_lower", "workspace_for", "workspace_for_ata",
+]

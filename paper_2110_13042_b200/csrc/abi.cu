@@ -1,0 +1,389 @@
+// C ABI + native plan executor (see include/atamul_b200.h).
+//
+// The executor walks a flat op list produced by the host planner, validates
+// every window against its base buffer (a workspace overrun is the
+// reference's WorkspaceUndersizedError, strassen.py:82-85), resolves windows
+// into device pointers, coalesces consecutive same-group products into one
+// grouped launch, and issues everything on one stream.  It never allocates and
+// never synchronises, so a whole plan can be captured in a CUDA graph.
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/atamul_b200.h"
+#include "ata_common.cuh"
+
+namespace {
+
+thread_local std::string g_last_error;
+
+int fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  return code;
+}
+
+int cuda_fail(cudaError_t e, const char* where) {
+  g_last_error = std::string(where) + ": " + cudaGetErrorString(e);
+  return ATA_E_CUDA;
+}
+
+struct Bases {
+  const char* ptr[4];
+  long long elems[4];
+  size_t esize;
+};
+
+// Validate a window against its base. rows==0 or cols==0 means "empty/absent".
+int check_ref(const ata_ref& r, const Bases& b, const char* what, int opi, bool write) {
+  if (r.base < 0 || r.base > 3) return fail(ATA_E_ARG, std::string(what) + ": bad base");
+  if (r.rows < 0 || r.cols < 0 || r.off < 0)
+    return fail(ATA_E_SHAPE, "shape mismatch: negative window in op " + std::to_string(opi));
+  if (r.rows == 0 || r.cols == 0) return ATA_OK;
+  if (b.ptr[r.base] == nullptr)
+    return fail(ATA_E_ARG, std::string(what) + ": null base pointer in op " + std::to_string(opi));
+  if (r.rows > 1 && r.ld < r.cols)
+    return fail(ATA_E_SHAPE, "shape mismatch: ld < cols in op " + std::to_string(opi));
+  if (write && r.base == ATA_BASE_A)
+    return fail(ATA_E_ARG, "op " + std::to_string(opi) + " writes into A");
+  const long long last = r.off + (long long)(r.rows - 1) * r.ld + r.cols;
+  if (last > b.elems[r.base]) {
+    if (r.base == ATA_BASE_WS)
+      return fail(ATA_E_WORKSPACE, "workspace undersized: op " + std::to_string(opi) + " needs " +
+                                       std::to_string(last) + " scalars, have " +
+                                       std::to_string(b.elems[r.base]));
+    return fail(ATA_E_SHAPE, "shape mismatch: window exceeds its base buffer in op " +
+                                 std::to_string(opi));
+  }
+  return ATA_OK;
+}
+
+template <typename T>
+ata::DTerm<T> term_of(const ata_ref& r, const Bases& b) {
+  ata::DTerm<T> t;
+  t.p = reinterpret_cast<const T*>(b.ptr[r.base] ? b.ptr[r.base] + r.off * (long long)sizeof(T) : nullptr);
+  t.ld = r.ld;
+  t.rows = r.rows;
+  t.cols = r.cols;
+  t.sign = r.sign;
+  if (t.p == nullptr) t.rows = t.cols = 0;
+  return t;
+}
+
+template <typename T>
+ata::DDest<T> dest_of(const ata_ref& r, const Bases& b) {
+  ata::DDest<T> d;
+  d.p = reinterpret_cast<T*>(const_cast<char*>(b.ptr[r.base]) + r.off * (long long)sizeof(T));
+  d.ld = r.ld;
+  d.rows = r.rows;
+  d.cols = r.cols;
+  d.sign = r.sign;
+  return d;
+}
+
+template <typename T>
+cudaError_t launch_batch(const ata::BatchArgs<T>& a, cudaStream_t s, int dtype);
+template <>
+cudaError_t launch_batch<double>(const ata::BatchArgs<double>& a, cudaStream_t s, int) {
+  return ata::launch_batch_f64(a, s);
+}
+template <>
+cudaError_t launch_batch<float>(const ata::BatchArgs<float>& a, cudaStream_t s, int dtype) {
+  return ata::launch_batch_f32(a, s, dtype != ATA_TF32);
+}
+template <typename T>
+int tile_rows();
+template <>
+int tile_rows<double>() { return ata::tile_rows_f64(); }
+template <>
+int tile_rows<float>() { return ata::tile_rows_f32(); }
+
+int validate_op(const ata_op& op, const Bases& b, int i) {
+  int rc;
+  if (op.ns < 0 || op.ns > ATA_MAX_TERMS || op.nt < 0 || op.nt > ATA_MAX_TERMS || op.nd < 0 ||
+      op.nd > ATA_MAX_DESTS)
+    return fail(ATA_E_ARG, "bad term/dest count in op " + std::to_string(i));
+  for (int j = 0; j < op.ns; ++j)
+    if ((rc = check_ref(op.s[j], b, "s", i, false))) return rc;
+  for (int j = 0; j < op.nt; ++j)
+    if ((rc = check_ref(op.t[j], b, "t", i, false))) return rc;
+  for (int j = 0; j < op.nd; ++j)
+    if ((rc = check_ref(op.d[j], b, "d", i, true))) return rc;
+  switch (op.type) {
+    case ATA_OP_GEMM:
+    case ATA_OP_SYRK:
+      if (op.m < 1 || op.n < 1 || op.k < 1 || op.ns < 1 || op.nd < 1 ||
+          (op.type == ATA_OP_GEMM && op.nt < 1))
+        return fail(ATA_E_SHAPE, "shape mismatch: empty product in op " + std::to_string(i));
+      if (op.s[0].sign != 1.0 || (op.type == ATA_OP_GEMM && op.t[0].sign != 1.0))
+        return fail(ATA_E_ARG, "leading operand term must have sign +1 (op " + std::to_string(i) + ")");
+      for (int j = 0; j < op.ns; ++j)
+        if (op.s[j].rows > op.m || op.s[j].cols > op.n)
+          return fail(ATA_E_SHAPE, "shape mismatch: S term exceeds product in op " + std::to_string(i));
+      for (int j = 0; j < op.nt; ++j)
+        if (op.t[j].rows > op.m || op.t[j].cols > op.k)
+          return fail(ATA_E_SHAPE, "shape mismatch: T term exceeds product in op " + std::to_string(i));
+      for (int j = 0; j < op.nd; ++j)
+        if (op.d[j].rows > op.n || op.d[j].cols > op.k)
+          return fail(ATA_E_SHAPE, "shape mismatch: destination exceeds product in op " + std::to_string(i));
+      if (op.type == ATA_OP_SYRK && op.n != op.k)
+        return fail(ATA_E_SHAPE, "shape mismatch: SYRK output must be square");
+      return ATA_OK;
+    case ATA_OP_COMBO:
+      if (op.nd != 1 || op.ns < 1) return fail(ATA_E_ARG, "combo needs 1 dest and >=1 term");
+      for (int j = 0; j < op.ns; ++j)
+        if (op.s[j].rows > op.d[0].rows + 1 || op.s[j].cols > op.d[0].cols + 1 ||
+            op.s[j].rows < op.d[0].rows - 1 || op.s[j].cols < op.d[0].cols - 1)
+          return fail(ATA_E_SHAPE, "shape mismatch: combo term differs by more than one row/col");
+      return ATA_OK;
+    case ATA_OP_UPDATE:
+      if (op.ns != 1 || op.nd < 1) return fail(ATA_E_ARG, "update needs 1 source and >=1 dest");
+      for (int j = 0; j < op.nd; ++j)
+        if (op.d[j].rows > op.s[0].rows || op.d[j].cols > op.s[0].cols)
+          return fail(ATA_E_SHAPE, "shape mismatch: update destination window exceeds source");
+      return ATA_OK;
+    case ATA_OP_FILL:
+      if (op.nd != 1) return fail(ATA_E_ARG, "fill needs 1 dest");
+      return ATA_OK;
+    default:
+      return fail(ATA_E_ARG, "unknown op type " + std::to_string(op.type));
+  }
+}
+
+template <typename T>
+int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, double alpha, cudaStream_t s,
+               int dtype) {
+  for (int i = 0; i < n_ops; ++i) {
+    int rc = validate_op(ops[i], b, i);
+    if (rc) return rc;
+  }
+  const int TR = tile_rows<T>();
+  ata::BatchArgs<T> batch;
+  std::memset(&batch, 0, sizeof(batch));
+  batch.alpha = alpha;
+  int batch_group = -1;
+  auto flush = [&]() -> int {
+    if (batch.count == 0) return ATA_OK;
+    cudaError_t e = launch_batch<T>(batch, s, dtype);
+    batch.count = 0;
+    batch.total_tiles = 0;
+    if (e != cudaSuccess) return cuda_fail(e, "product launch");
+    return ATA_OK;
+  };
+  for (int i = 0; i < n_ops; ++i) {
+    const ata_op& op = ops[i];
+    int rc;
+    if (op.type == ATA_OP_GEMM || op.type == ATA_OP_SYRK) {
+      const bool join = batch.count > 0 && op.group >= 0 && op.group == batch_group &&
+                        batch.count < ata::kMaxBatch;
+      if (!join && (rc = flush())) return rc;
+      ata::DProd<T>& p = batch.p[batch.count];
+      std::memset(&p, 0, sizeof(p));
+      p.kind = op.type == ATA_OP_SYRK ? ata::kSyrk : ata::kGemm;
+      p.m = op.m;
+      p.n = op.n;
+      p.k = op.k;
+      p.ns = op.ns;
+      p.nt = op.type == ATA_OP_SYRK ? 0 : op.nt;
+      p.nd = op.nd;
+      p.accumulate = op.accumulate;
+      for (int j = 0; j < op.ns; ++j) p.s[j] = term_of<T>(op.s[j], b);
+      for (int j = 0; j < p.nt; ++j) p.t[j] = term_of<T>(op.t[j], b);
+      for (int j = 0; j < op.nd; ++j) p.d[j] = dest_of<T>(op.d[j], b);
+      p.tn = (op.n + TR - 1) / TR;
+      p.tk = (op.k + TR - 1) / TR;
+      const long long tiles = p.kind == ata::kSyrk ? (long long)p.tn * (p.tn + 1) / 2
+                                                   : (long long)p.tn * p.tk;
+      if (batch.total_tiles + tiles > 0x7fffffffLL) return fail(ATA_E_UNSUPPORTED, "too many tiles");
+      p.tile_begin = batch.total_tiles;
+      batch.total_tiles += (int)tiles;
+      batch.count++;
+      batch_group = op.group;
+      if (op.group < 0 && (rc = flush())) return rc;
+      continue;
+    }
+    if ((rc = flush())) return rc;
+    cudaError_t e = cudaSuccess;
+    if (op.type == ATA_OP_COMBO || op.type == ATA_OP_UPDATE) {
+      ata::EwArgs<T> a;
+      std::memset(&a, 0, sizeof(a));
+      a.nsrc = op.ns;
+      a.ndst = op.nd;
+      for (int j = 0; j < op.ns; ++j) a.src[j] = term_of<T>(op.s[j], b);
+      for (int j = 0; j < op.nd; ++j) a.dst[j] = dest_of<T>(op.d[j], b);
+      if (op.type == ATA_OP_COMBO) {
+        a.rows = op.d[0].rows;
+        a.cols = op.d[0].cols;
+        e = ata::launch_combo<T>(a, s);
+      } else {
+        // iterate over the union of the destination windows (each <= source)
+        for (int j = 0; j < op.nd; ++j) {
+          a.rows = a.rows > op.d[j].rows ? a.rows : op.d[j].rows;
+          a.cols = a.cols > op.d[j].cols ? a.cols : op.d[j].cols;
+        }
+        e = ata::launch_update<T>(a, s);
+      }
+    } else if (op.type == ATA_OP_FILL) {
+      ata::DDest<T> d = dest_of<T>(op.d[0], b);
+      e = ata::launch_fill<T>(d.p, d.ld, d.rows, d.cols, s);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "elementwise launch");
+  }
+  return flush();
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ata_last_error(void) { return g_last_error.c_str(); }
+
+const char* ata_strerror(int code) {
+  switch (code) {
+    case ATA_OK: return "ok";
+    case ATA_E_SHAPE: return "shape mismatch";
+    case ATA_E_UNSPLITTABLE: return "unsplittable";
+    case ATA_E_WORKSPACE: return "workspace undersized";
+    case ATA_E_UNSUPPORTED: return "unsupported size";
+    case ATA_E_PROTOCOL: return "protocol error";
+    case ATA_E_CUDA: return "cuda error";
+    case ATA_E_ARG: return "invalid argument";
+    default: return "unknown error";
+  }
+}
+
+int ata_version(void) { return 100; }
+int ata_abi_op_size(void) { return (int)sizeof(ata_op); }
+
+int ata_run_plan(int dtype, const ata_op* ops, int32_t n_ops, const void* A, int64_t a_elems,
+                 const void* B, int64_t b_elems, void* C, int64_t c_elems, void* WS,
+                 int64_t ws_elems, double alpha, void* stream) {
+  if (n_ops < 0 || (n_ops > 0 && ops == nullptr)) return fail(ATA_E_ARG, "null op list");
+  Bases b;
+  b.ptr[ATA_BASE_A] = static_cast<const char*>(A);
+  b.ptr[ATA_BASE_C] = static_cast<const char*>(C);
+  b.ptr[ATA_BASE_WS] = static_cast<const char*>(WS);
+  b.ptr[ATA_BASE_B] = static_cast<const char*>(B);
+  b.elems[ATA_BASE_A] = a_elems;
+  b.elems[ATA_BASE_C] = c_elems;
+  b.elems[ATA_BASE_WS] = ws_elems;
+  b.elems[ATA_BASE_B] = b_elems;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  if (dtype == ATA_F64) {
+    b.esize = 8;
+    return run_plan_t<double>(ops, n_ops, b, alpha, s, dtype);
+  }
+  if (dtype == ATA_F32 || dtype == ATA_TF32) {
+    b.esize = 4;
+    return run_plan_t<float>(ops, n_ops, b, alpha, s, dtype);
+  }
+  return fail(ATA_E_ARG, "unknown dtype");
+}
+
+static ata_ref mkref(int base, long long ld, int rows, int cols) {
+  ata_ref r;
+  std::memset(&r, 0, sizeof(r));
+  r.base = base;
+  r.off = 0;
+  r.ld = ld;
+  r.rows = rows;
+  r.cols = cols;
+  r.sign = 1.0;
+  return r;
+}
+
+int ata_syrk_lower(int dtype, const void* A, int64_t lda, int32_t m, int32_t n, void* C,
+                   int64_t ldc, double alpha, void* stream) {
+  if (m < 1 || n < 1) return fail(ATA_E_SHAPE, "shape mismatch: empty operand");
+  ata_op op;
+  std::memset(&op, 0, sizeof(op));
+  op.type = ATA_OP_SYRK;
+  op.m = m;
+  op.n = n;
+  op.k = n;
+  op.ns = 1;
+  op.nd = 1;
+  op.accumulate = 1;
+  op.group = -1;
+  op.s[0] = mkref(ATA_BASE_A, lda, m, n);
+  op.d[0] = mkref(ATA_BASE_C, ldc, n, n);
+  const long long ae = (long long)(m - 1) * lda + n, ce = (long long)(n - 1) * ldc + n;
+  return ata_run_plan(dtype, &op, 1, A, ae, nullptr, 0, C, ce, nullptr, 0, alpha, stream);
+}
+
+int ata_gemm_atb(int dtype, const void* A, int64_t lda, const void* B, int64_t ldb, int32_t m,
+                 int32_t n, int32_t k, void* C, int64_t ldc, double alpha, void* stream) {
+  if (m < 1 || n < 1 || k < 1) return fail(ATA_E_SHAPE, "shape mismatch: empty operand");
+  ata_op op;
+  std::memset(&op, 0, sizeof(op));
+  op.type = ATA_OP_GEMM;
+  op.m = m;
+  op.n = n;
+  op.k = k;
+  op.ns = 1;
+  op.nt = 1;
+  op.nd = 1;
+  op.accumulate = 1;
+  op.group = -1;
+  op.s[0] = mkref(ATA_BASE_A, lda, m, n);
+  op.t[0] = mkref(ATA_BASE_B, ldb, m, k);
+  op.d[0] = mkref(ATA_BASE_C, ldc, n, k);
+  const long long ae = (long long)(m - 1) * lda + n, be = (long long)(m - 1) * ldb + k,
+                  ce = (long long)(n - 1) * ldc + k;
+  return ata_run_plan(dtype, &op, 1, A, ae, B, be, C, ce, nullptr, 0, alpha, stream);
+}
+
+int ata_add_truncated(int dtype, void* dst, int64_t ldd, int32_t dr, int32_t dc, const void* src,
+                      int64_t lds, int32_t sr, int32_t sc, double scale, void* stream) {
+  if (dr < 1 || dc < 1 || sr < 1 || sc < 1) return fail(ATA_E_SHAPE, "shape mismatch: empty block");
+  if (dr - sr > 1 || sr - dr > 1 || dc - sc > 1 || sc - dc > 1)
+    return fail(ATA_E_SHAPE, "shape mismatch: add_truncated (" + std::to_string(dr) + "," +
+                                 std::to_string(dc) + ") vs (" + std::to_string(sr) + "," +
+                                 std::to_string(sc) + ")");
+  const int r = dr < sr ? dr : sr, c = dc < sc ? dc : sc;
+  ata_op op;
+  std::memset(&op, 0, sizeof(op));
+  op.type = ATA_OP_UPDATE;
+  op.ns = 1;
+  op.nd = 1;
+  op.group = -1;
+  op.s[0] = mkref(ATA_BASE_A, lds, sr, sc);
+  op.d[0] = mkref(ATA_BASE_C, ldd, r, c);
+  op.d[0].sign = scale;
+  const long long se = (long long)(sr - 1) * lds + sc, de = (long long)(dr - 1) * ldd + dc;
+  return ata_run_plan(dtype, &op, 1, src, se, nullptr, 0, dst, de, nullptr, 0, 1.0, stream);
+}
+
+int ata_mirror_lower(int dtype, void* C, int64_t ldc, int32_t n, void* stream) {
+  if (n < 1 || C == nullptr) return fail(ATA_E_SHAPE, "shape mismatch: mirror needs a square block");
+  cudaError_t e = dtype == ATA_F64
+                      ? ata::launch_mirror<double>(static_cast<double*>(C), ldc, n, (cudaStream_t)stream)
+                      : ata::launch_mirror<float>(static_cast<float*>(C), ldc, n, (cudaStream_t)stream);
+  return e == cudaSuccess ? ATA_OK : cuda_fail(e, "mirror");
+}
+
+int ata_pack_lower(int dtype, const void* C, int64_t ldc, int32_t n, void* packed, void* stream) {
+  if (n < 1 || C == nullptr || packed == nullptr) return fail(ATA_E_SHAPE, "shape mismatch: pack_lower");
+  cudaError_t e =
+      dtype == ATA_F64
+          ? ata::launch_pack<double>(static_cast<const double*>(C), ldc, n, static_cast<double*>(packed),
+                                     (cudaStream_t)stream)
+          : ata::launch_pack<float>(static_cast<const float*>(C), ldc, n, static_cast<float*>(packed),
+                                    (cudaStream_t)stream);
+  return e == cudaSuccess ? ATA_OK : cuda_fail(e, "pack");
+}
+
+int ata_unpack_lower(int dtype, const void* packed, int32_t n, void* C, int64_t ldc,
+                     int32_t accumulate, void* stream) {
+  if (n < 1 || C == nullptr || packed == nullptr) return fail(ATA_E_SHAPE, "shape mismatch: unpack_lower target");
+  cudaError_t e = dtype == ATA_F64
+                      ? ata::launch_unpack<double>(static_cast<const double*>(packed), n,
+                                                   static_cast<double*>(C), ldc, accumulate,
+                                                   (cudaStream_t)stream)
+                      : ata::launch_unpack<float>(static_cast<const float*>(packed), n,
+                                                  static_cast<float*>(C), ldc, accumulate,
+                                                  (cudaStream_t)stream);
+  return e == cudaSuccess ? ATA_OK : cuda_fail(e, "unpack");
+}
+
+}  // extern "C"

@@ -1,0 +1,88 @@
+// Shared device-side descriptors and helpers for the AtA kernels (sm_100a).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ata {
+
+constexpr int kMaxBatch = 32;  // products per grouped launch (kernel-param by value)
+
+template <typename T>
+struct DTerm {  // zero-extended read window
+  const T* p;
+  long long ld;
+  int rows, cols;
+  double sign;
+};
+
+template <typename T>
+struct DDest {  // truncated write window
+  T* p;
+  long long ld;
+  int rows, cols;
+  double sign;
+};
+
+enum : int { kGemm = 0, kSyrk = 1 };
+
+template <typename T>
+struct DProd {
+  int kind;        // kGemm / kSyrk
+  int m, n, k;     // contraction, output rows, output cols
+  int ns, nt, nd;  // term / dest counts
+  int accumulate;  // 1: D += v ; 0: D = v
+  int tn, tk;      // tile grid (rows x cols); SYRK uses the lower triangle of tn x tn
+  int tile_begin;  // prefix offset of this product in the launch's tile space
+  int _pad;
+  DTerm<T> s[2], t[2];
+  DDest<T> d[4];
+};
+
+template <typename T>
+struct BatchArgs {
+  int count;
+  int total_tiles;
+  double alpha;
+  DProd<T> p[kMaxBatch];
+};
+
+template <typename T>
+struct EwArgs {  // elementwise op: rows x cols iteration space
+  int rows, cols, nsrc, ndst;
+  DTerm<T> src[2];
+  DDest<T> dst[4];
+};
+
+// ---- host launchers (defined in gemm_*.cu / elementwise.cu) ----
+cudaError_t launch_batch_f64(const BatchArgs<double>& a, cudaStream_t s);
+cudaError_t launch_batch_f32(const BatchArgs<float>& a, cudaStream_t s, bool split);
+int tile_rows_f64();
+int tile_rows_f32();
+template <typename T> cudaError_t launch_combo(const EwArgs<T>& a, cudaStream_t s);
+template <typename T> cudaError_t launch_update(const EwArgs<T>& a, cudaStream_t s);
+template <typename T> cudaError_t launch_fill(T* p, long long ld, int rows, int cols, cudaStream_t s);
+template <typename T> cudaError_t launch_mirror(T* C, long long ldc, int n, cudaStream_t s);
+template <typename T> cudaError_t launch_pack(const T* C, long long ldc, int n, T* packed, cudaStream_t s);
+template <typename T>
+cudaError_t launch_unpack(const T* packed, int n, T* C, long long ldc, int acc, cudaStream_t s);
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+// cp.async with zero-fill: copies src_bytes (0 or full) and zero-fills the rest.
+__device__ __forceinline__ void cp_async_8(void* smem, const void* gmem, int src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),
+               "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_16(void* smem, const void* gmem, int src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(smem_u32(smem)), "l"(gmem),
+               "r"(src_bytes));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
+}
+
+}  // namespace ata

@@ -1,0 +1,199 @@
+// HBM-bound elementwise kernels of the AtA path (sm_100a).
+//
+//   combo      dst = s0*X0 + s1*X1, zero-extended      (_load_combo, strassen.py:195-203:
+//              one pass instead of fill + 2 add_truncated = 7 memory passes)
+//   update     D_d[:r,:c] += s_d * P[:r,:c], d < 4      (add_truncated, matrix.py:218-239;
+//              one read of P feeds every destination, strassen.py:238-275)
+//   fill       D = 0                                     (p.fill(0), strassen.py:224)
+//   mirror     C[i,j] = C[j,i], i<j, 32x32 smem tiles    (mirror_lower_to_upper, matrix.py:373-380)
+//   pack       packed[i(i+1)/2+j] = C[i,j], j<=i          (pack_lower, matrix.py:353-360)
+//   unpack     C[i,j] (+)= packed[...]                    (unpack_lower :363-370, distsim.py:208-216)
+//
+// All are grid-stride, coalesced along rows, and sized in multiples of the
+// 148 SMs.  They are judged against measured HBM copy bandwidth.
+#include "ata_common.cuh"
+
+namespace ata {
+
+constexpr int kEwThreadsX = 128, kEwThreadsY = 2;
+
+static int ew_grid_y(long long rows, int gx) {
+  // ~8 resident blocks per SM x 148 SMs worth of blocks in total
+  long long want = (148LL * 8 * 4 + gx - 1) / gx;
+  long long gy = (rows + kEwThreadsY - 1) / kEwThreadsY;
+  if (gy > want) gy = want;
+  if (gy > 65535) gy = 65535;
+  if (gy < 1) gy = 1;
+  return (int)gy;
+}
+
+// combo: dst[0] (rows x cols) = sum_i src[i].sign * zero-extended src[i]
+template <typename T>
+__global__ void combo_kernel(const __grid_constant__ EwArgs<T> a) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= a.cols) return;
+  const DDest<T>& D = a.dst[0];
+  for (int r = blockIdx.y * blockDim.y + threadIdx.y; r < a.rows; r += gridDim.y * blockDim.y) {
+    T v = T(0);
+#pragma unroll
+    for (int i = 0; i < 2; ++i) {
+      if (i < a.nsrc) {
+        const DTerm<T>& S = a.src[i];
+        if (r < S.rows && c < S.cols) v += T(S.sign) * S.p[(long long)r * S.ld + c];
+      }
+    }
+    D.p[(long long)r * D.ld + c] = v;
+  }
+}
+
+// update: for each dest d, D_d[r,c] += sign_d * P[r,c] (r < D_d.rows, c < D_d.cols)
+template <typename T>
+__global__ void update_kernel(const __grid_constant__ EwArgs<T> a) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= a.cols) return;
+  const DTerm<T>& S = a.src[0];
+  for (int r = blockIdx.y * blockDim.y + threadIdx.y; r < a.rows; r += gridDim.y * blockDim.y) {
+    const T v = S.p[(long long)r * S.ld + c];
+#pragma unroll
+    for (int d = 0; d < 4; ++d) {
+      if (d < a.ndst) {
+        const DDest<T>& D = a.dst[d];
+        if (r < D.rows && c < D.cols) {
+          T* p = D.p + (long long)r * D.ld + c;
+          *p = *p + T(D.sign) * v;
+        }
+      }
+    }
+  }
+}
+
+template <typename T>
+__global__ void fill_kernel(T* p, long long ld, int rows, int cols) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  for (int r = blockIdx.y * blockDim.y + threadIdx.y; r < rows; r += gridDim.y * blockDim.y)
+    p[(long long)r * ld + c] = T(0);
+}
+
+// mirror: one 32x32 tile pair per block, tiles enumerated over the lower triangle.
+template <typename T>
+__global__ void mirror_kernel(T* C, long long ldc, int n, long long ntiles_tri) {
+  __shared__ T tile[32][33];
+  const int nt = (n + 31) / 32;
+  for (long long t = blockIdx.x; t < ntiles_tri; t += gridDim.x) {
+    long long bi = (long long)((sqrt(8.0 * (double)t + 1.0) - 1.0) * 0.5);
+    while ((bi + 1) * (bi + 2) / 2 <= t) ++bi;
+    while (bi * (bi + 1) / 2 > t) --bi;
+    const long long bj = t - bi * (bi + 1) / 2;  // bj <= bi
+    (void)nt;
+    // read lower tile rows bi*32.., cols bj*32..
+    for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+      const long long r = bi * 32 + y, c = bj * 32 + threadIdx.x;
+      if (r < n && c < n) tile[y][threadIdx.x] = C[r * ldc + c];
+    }
+    __syncthreads();
+    // write upper tile rows bj*32.., cols bi*32.. : C[c][r] = C[r][c] for r > c
+    for (int y = threadIdx.y; y < 32; y += blockDim.y) {
+      const long long r = bj * 32 + y, c = bi * 32 + threadIdx.x;
+      if (r < n && c < n && c > r) C[r * ldc + c] = tile[threadIdx.x][y];
+    }
+    __syncthreads();
+  }
+}
+
+__device__ __forceinline__ long long tri_row(long long p) {
+  long long i = (long long)((sqrt(8.0 * (double)p + 1.0) - 1.0) * 0.5);
+  while ((i + 1) * (i + 2) / 2 <= p) ++i;
+  while (i * (i + 1) / 2 > p) --i;
+  return i;
+}
+
+template <typename T>
+__global__ void pack_kernel(const T* C, long long ldc, long long total, T* packed) {
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < total;
+       p += (long long)gridDim.x * blockDim.x) {
+    const long long i = tri_row(p);
+    const long long j = p - i * (i + 1) / 2;
+    packed[p] = C[i * ldc + j];
+  }
+}
+
+template <typename T>
+__global__ void unpack_kernel(const T* packed, long long total, T* C, long long ldc, int acc) {
+  for (long long p = blockIdx.x * (long long)blockDim.x + threadIdx.x; p < total;
+       p += (long long)gridDim.x * blockDim.x) {
+    const long long i = tri_row(p);
+    const long long j = p - i * (i + 1) / 2;
+    T* dst = C + i * ldc + j;
+    *dst = acc ? *dst + packed[p] : packed[p];
+  }
+}
+
+// ---------------- host launchers ----------------
+template <typename T>
+cudaError_t launch_combo(const EwArgs<T>& a, cudaStream_t s) {
+  if (a.rows <= 0 || a.cols <= 0) return cudaSuccess;
+  dim3 blk(kEwThreadsX, kEwThreadsY);
+  const int gx = (a.cols + kEwThreadsX - 1) / kEwThreadsX;
+  dim3 grd(gx, ew_grid_y(a.rows, gx));
+  combo_kernel<T><<<grd, blk, 0, s>>>(a);
+  return cudaGetLastError();
+}
+template <typename T>
+cudaError_t launch_update(const EwArgs<T>& a, cudaStream_t s) {
+  if (a.rows <= 0 || a.cols <= 0) return cudaSuccess;
+  dim3 blk(kEwThreadsX, kEwThreadsY);
+  const int gx = (a.cols + kEwThreadsX - 1) / kEwThreadsX;
+  dim3 grd(gx, ew_grid_y(a.rows, gx));
+  update_kernel<T><<<grd, blk, 0, s>>>(a);
+  return cudaGetLastError();
+}
+template <typename T>
+cudaError_t launch_fill(T* p, long long ld, int rows, int cols, cudaStream_t s) {
+  if (rows <= 0 || cols <= 0) return cudaSuccess;
+  dim3 blk(kEwThreadsX, kEwThreadsY);
+  const int gx = (cols + kEwThreadsX - 1) / kEwThreadsX;
+  dim3 grd(gx, ew_grid_y(rows, gx));
+  fill_kernel<T><<<grd, blk, 0, s>>>(p, ld, rows, cols);
+  return cudaGetLastError();
+}
+template <typename T>
+cudaError_t launch_mirror(T* C, long long ldc, int n, cudaStream_t s) {
+  if (n <= 1) return cudaSuccess;
+  const long long nt = (n + 31) / 32;
+  const long long tri = nt * (nt + 1) / 2;
+  const int grid = (int)(tri < 148LL * 16 ? tri : 148LL * 16);
+  mirror_kernel<T><<<grid, dim3(32, 8), 0, s>>>(C, ldc, n, tri);
+  return cudaGetLastError();
+}
+template <typename T>
+cudaError_t launch_pack(const T* C, long long ldc, int n, T* packed, cudaStream_t s) {
+  const long long total = (long long)n * (n + 1) / 2;
+  if (total <= 0) return cudaSuccess;
+  long long blocks = (total + 255) / 256;
+  if (blocks > 148LL * 32) blocks = 148LL * 32;
+  pack_kernel<T><<<(int)blocks, 256, 0, s>>>(C, ldc, total, packed);
+  return cudaGetLastError();
+}
+template <typename T>
+cudaError_t launch_unpack(const T* packed, int n, T* C, long long ldc, int acc, cudaStream_t s) {
+  const long long total = (long long)n * (n + 1) / 2;
+  if (total <= 0) return cudaSuccess;
+  long long blocks = (total + 255) / 256;
+  if (blocks > 148LL * 32) blocks = 148LL * 32;
+  unpack_kernel<T><<<(int)blocks, 256, 0, s>>>(packed, total, C, ldc, acc);
+  return cudaGetLastError();
+}
+
+#define ATA_INST(T)                                                                       \
+  template cudaError_t launch_combo<T>(const EwArgs<T>&, cudaStream_t);                   \
+  template cudaError_t launch_update<T>(const EwArgs<T>&, cudaStream_t);                  \
+  template cudaError_t launch_fill<T>(T*, long long, int, int, cudaStream_t);             \
+  template cudaError_t launch_mirror<T>(T*, long long, int, cudaStream_t);                \
+  template cudaError_t launch_pack<T>(const T*, long long, int, T*, cudaStream_t);        \
+  template cudaError_t launch_unpack<T>(const T*, int, T*, long long, int, cudaStream_t);
+ATA_INST(double)
+ATA_INST(float)
+#undef ATA_INST
+
+}  // namespace ata

@@ -1,0 +1,288 @@
+"""Recursion planners: turn an AtA / Strassen call into a flat list of
+native plan ops (include/atamul_b200.h, ``ata_op``).
+
+Two planners share one op vocabulary:
+
+* ``plan_ata_reference`` / ``plan_strassen_reference`` — the reference
+  recursion with an integer element-count ``threshold``: same leaf
+  predicates (ata.py:23-26, strassen.py:38-41), same floor/ceil quadrants
+  (ata.py:104-109, strassen.py:216-220), same seven products and
+  destinations (strassen.py:234-275), same per-depth workspace use
+  (strassen.py:74-85) — hence the same leaves and the same exact
+  multiplication count as the reference's MultCounter.  One GPU-first
+  change, numerically equivalent: a Strassen product whose recursive call is
+  a leaf is emitted as ONE fused product op (pre-additions in the operand
+  load, post-additions in the epilogue) instead of combo + fill + leaf +
+  update (same operand sums, same single rounding of each C update).
+
+* ``plan_ata_auto`` — ``threshold="auto"``: the GPU plan.  The contraction
+  (rows of A) is never split -- a long contraction belongs in one kernel's K
+  loop -- the column recursion of the AtA scheme (ata.py:110-115, with the
+  two C21 addends merged into one product over all m rows) runs to a leaf
+  width chosen from the B200 tile grid, every below-diagonal block uses one
+  fused Strassen level (7 products, strassen.py:234-275), products of the
+  same index across all blocks of one level share a launch (their C windows
+  are disjoint), and every SYRK leaf shares one launch.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+from typing import NamedTuple
+
+import numpy as np
+
+from . import _native as nat
+from .errors import ShapeMismatchError
+from .workspace import is_ata_base_case, is_base_case
+
+_EMPTY = (0, 0, 0, 0, 0, 0, 0.0)
+
+
+class Win(NamedTuple):
+    """Window (base, element offset, ld, rows, cols) into a base buffer."""
+    base: int
+    off: int
+    ld: int
+    rows: int
+    cols: int
+
+    def sub(self, r0: int, c0: int, rows: int, cols: int) -> "Win":
+        return Win(self.base, self.off + r0 * self.ld + c0, self.ld, rows, cols)
+
+    def top(self, rows: int) -> "Win":
+        return Win(self.base, self.off, self.ld, min(rows, self.rows), self.cols)
+
+    def clip(self, rows: int, cols: int) -> "Win":
+        return Win(self.base, self.off, self.ld, min(rows, self.rows), min(cols, self.cols))
+
+
+def _ref(w: Win, sign: float = 1.0):
+    return (w.base, w.rows, w.off, w.ld, w.cols, 0, float(sign))
+
+
+@dataclass
+class Plan:
+    ops: np.ndarray          # OP_DTYPE records
+    mults: int               # exact scalar multiplications (MultCounter semantics)
+    ws_scalars: int          # workspace scalars the plan touches (extent of WS refs)
+    launches: int            # kernel launches the executor will issue
+    kind: str
+
+    def __len__(self):
+        return len(self.ops)
+
+
+class PlanBuilder:
+    def __init__(self, kind: str):
+        self.kind = kind
+        self.rows = []
+        self.mults = 0
+        self.ws_hi = 0
+        self._last_group = None
+        self.launches = 0
+
+    def _touch(self, w: Win):
+        if w.base == nat.BASE_WS and w.rows > 0 and w.cols > 0:
+            self.ws_hi = max(self.ws_hi, w.off + (w.rows - 1) * w.ld + w.cols)
+
+    def product(self, kind, m, n, k, S, T, D, accumulate=1, group=-1, count=True):
+        """S, T: [(Win, sign)] operand terms; D: [(Win, sign)] destinations."""
+        if len(S) > nat.MAX_TERMS or len(T) > nat.MAX_TERMS or len(D) > nat.MAX_DESTS:
+            raise ValueError("too many product terms")
+        for w, _ in list(S) + list(T) + list(D):
+            self._touch(w)
+        s = [_ref(w.clip(m, n), sg) for w, sg in S] + [_EMPTY] * (nat.MAX_TERMS - len(S))
+        t = [_ref(w.clip(m, k), sg) for w, sg in T] + [_EMPTY] * (nat.MAX_TERMS - len(T))
+        d = [_ref(w.clip(n, k), sg) for w, sg in D] + [_EMPTY] * (nat.MAX_DESTS - len(D))
+        op = nat.OP_SYRK if kind == "syrk" else nat.OP_GEMM
+        self.rows.append((op, m, n, k, len(S), len(T), len(D), accumulate, group, 0, s, t, d))
+        if group < 0 or group != self._last_group:
+            self.launches += 1
+        self._last_group = group if group >= 0 else None
+        if count:
+            self.mults += m * n * (n + 1) // 2 if kind == "syrk" else m * n * k
+
+    def _ew(self, op, S, D):
+        for w, _ in list(S) + list(D):
+            self._touch(w)
+        s = [_ref(w, sg) for w, sg in S] + [_EMPTY] * (nat.MAX_TERMS - len(S))
+        d = [_ref(w, sg) for w, sg in D] + [_EMPTY] * (nat.MAX_DESTS - len(D))
+        self.rows.append((op, 0, 0, 0, len(S), 0, len(D), 0, -1, 0, s, [_EMPTY] * nat.MAX_TERMS, d))
+        self.launches += 1
+        self._last_group = None
+
+    def combo(self, dst: Win, terms):
+        self._ew(nat.OP_COMBO, [(w.clip(dst.rows, dst.cols), sg) for w, sg in terms], [(dst, 1.0)])
+
+    def update(self, src: Win, dests):
+        self._ew(nat.OP_UPDATE, [(src, 1.0)],
+                 [(w.clip(src.rows, src.cols), sg) for w, sg in dests])
+
+    def fill(self, dst: Win):
+        self._ew(nat.OP_FILL, [], [(dst, 1.0)])
+
+    def finish(self) -> Plan:
+        ops = np.array(self.rows, dtype=nat.OP_DTYPE) if self.rows else np.zeros(0, nat.OP_DTYPE)
+        return Plan(ops, self.mults, self.ws_hi, self.launches, self.kind)
+
+
+# ------------------------------------------------------------------ Strassen
+
+def _strassen_products(a: Win, b: Win, c: Win):
+    """The seven products of one node (strassen.py:234-275) as
+    (S-shape, S-terms, T-shape, T-terms, dests); shape None = plain view."""
+    m, n = a.rows, a.cols
+    k = b.cols
+    m1, n1, k1 = m // 2, n // 2, k // 2
+    m2, n2, k2 = m - m1, n - n1, k - k1
+    A11, A12 = a.sub(0, 0, m1, n1), a.sub(0, n1, m1, n2)
+    A21, A22 = a.sub(m1, 0, m2, n1), a.sub(m1, n1, m2, n2)
+    B11, B12 = b.sub(0, 0, m1, k1), b.sub(0, k1, m1, k2)
+    B21, B22 = b.sub(m1, 0, m2, k1), b.sub(m1, k1, m2, k2)
+    C11, C12 = c.sub(0, 0, n1, k1), c.sub(0, k1, n1, k2)
+    C21, C22 = c.sub(n1, 0, n2, k1), c.sub(n1, k1, n2, k2)
+    return [
+        ((m2, n2), [(A22, 1.0), (A11, 1.0)], (m2, k2), [(B22, 1.0), (B11, 1.0)],
+         [(C11, 1.0), (C22, 1.0)]),
+        ((m1, n2), [(A12, 1.0), (A22.top(m1), 1.0)], None, [(B11, 1.0)],
+         [(C21, 1.0), (C22, -1.0)]),
+        (None, [(A11, 1.0)], (m1, k2), [(B12, 1.0), (B22.top(m1), -1.0)],
+         [(C12, 1.0), (C22, 1.0)]),
+        (None, [(A22, 1.0)], (m2, k1), [(B21, 1.0), (B11, -1.0)],
+         [(C11, 1.0), (C21, 1.0)]),
+        ((m2, n1), [(A21, 1.0), (A11, 1.0)], None, [(B22, 1.0)],
+         [(C11, -1.0), (C12, 1.0)]),
+        ((m1, n2), [(A12, 1.0), (A11, -1.0)], (m1, k2), [(B12, 1.0), (B11, 1.0)],
+         [(C22, 1.0)]),
+        ((m2, n2), [(A21, 1.0), (A22, -1.0)], (m2, k2), [(B22, 1.0), (B21, 1.0)],
+         [(C11, 1.0)]),
+    ]
+
+
+class _ReferencePlanner:
+    def __init__(self, threshold: int, level_offsets, fuse: bool = True):
+        self.t = threshold
+        self.lv = level_offsets
+        self.fuse = fuse
+        self.pb = PlanBuilder("reference")
+
+    def strassen(self, a: Win, b: Win, c: Win, depth: int):
+        m, n, k = a.rows, a.cols, b.cols
+        if is_base_case(m, n, k, self.t):
+            self.pb.product("gemm", m, n, k, [(a, 1.0)], [(b, 1.0)], [(c, 1.0)])
+            return
+        if depth >= len(self.lv):
+            from .errors import WorkspaceUndersizedError
+            raise WorkspaceUndersizedError(f"workspace undersized: no level {depth} for ({m},{n},{k})")
+        prod_off, lhs_off, rhs_off = self.lv[depth]
+        for s_shape, s_terms, t_shape, t_terms, dests in _strassen_products(a, b, c):
+            ms, ns = s_shape if s_shape else (s_terms[0][0].rows, s_terms[0][0].cols)
+            mt, kt = t_shape if t_shape else (t_terms[0][0].rows, t_terms[0][0].cols)
+            assert ms == mt
+            if self.fuse and is_base_case(ms, ns, kt, self.t):
+                self.pb.product("gemm", ms, ns, kt, s_terms, t_terms, dests)
+                continue
+            if s_shape:
+                S = Win(nat.BASE_WS, lhs_off, ns, ms, ns)
+                self.pb.combo(S, s_terms)
+            else:
+                S = s_terms[0][0]
+            if t_shape:
+                T = Win(nat.BASE_WS, rhs_off, kt, mt, kt)
+                self.pb.combo(T, t_terms)
+            else:
+                T = t_terms[0][0]
+            P = Win(nat.BASE_WS, prod_off, kt, ns, kt)
+            self.pb.fill(P)
+            self.strassen(S, T, P, depth + 1)
+            self.pb.update(P, dests)
+
+    def ata(self, a: Win, c: Win):
+        m, n = a.rows, a.cols
+        if is_ata_base_case(m, n, self.t):
+            self.pb.product("syrk", m, n, n, [(a, 1.0)], [], [(c, 1.0)])
+            return
+        m1, n1 = m // 2, n // 2
+        m2, n2 = m - m1, n - n1
+        a11, a12 = a.sub(0, 0, m1, n1), a.sub(0, n1, m1, n2)
+        a21, a22 = a.sub(m1, 0, m2, n1), a.sub(m1, n1, m2, n2)
+        c11, c21, c22 = c.sub(0, 0, n1, n1), c.sub(n1, 0, n2, n1), c.sub(n1, n1, n2, n2)
+        self.ata(a11, c11)
+        self.ata(a21, c11)
+        self.ata(a12, c22)
+        self.ata(a22, c22)
+        self.strassen(a12, a11, c21, 0)
+        self.strassen(a22, a21, c21, 0)
+
+
+def plan_ata_reference(m, n, lda, ldc, threshold, level_offsets, fuse=True) -> Plan:
+    p = _ReferencePlanner(threshold, level_offsets, fuse)
+    p.ata(Win(nat.BASE_A, 0, lda, m, n), Win(nat.BASE_C, 0, ldc, n, n))
+    return p.pb.finish()
+
+
+def plan_strassen_reference(m, n, k, lda, ldb, ldc, threshold, level_offsets, fuse=True) -> Plan:
+    p = _ReferencePlanner(threshold, level_offsets, fuse)
+    p.strassen(Win(nat.BASE_A, 0, lda, m, n), Win(nat.BASE_B, 0, ldb, m, k),
+               Win(nat.BASE_C, 0, ldc, n, k), 0)
+    return p.pb.finish()
+
+
+# ---------------------------------------------------------------------- auto
+
+TILE = 128
+
+
+@dataclass(frozen=True)
+class AutoParams:
+    leaf_cols: int = 1024        # stop the column recursion at this width
+    strassen_min: int = 1024     # use a fused Strassen level when both C21 sides >= this
+
+
+def plan_ata_auto(m, n, lda, ldc, params: AutoParams = AutoParams()) -> Plan:
+    """GPU plan for lower(C) += alpha A^T A (see module docstring)."""
+    if m < 1 or n < 1:
+        raise ShapeMismatchError("shape mismatch: empty operand")
+    pb = PlanBuilder("auto")
+    A = Win(nat.BASE_A, 0, lda, m, n)
+    C = Win(nat.BASE_C, 0, ldc, n, n)
+    nodes = [(0, n)]
+    group = 0
+    while True:
+        split = [(c0, w) for (c0, w) in nodes if w > params.leaf_cols and w >= 2]
+        if not split:
+            break
+        keep = [(c0, w) for (c0, w) in nodes if not (w > params.leaf_cols and w >= 2)]
+        nxt = list(keep)
+        fused = []     # (a, b, c) blocks taking the Strassen path
+        plain = []
+        for (c0, w) in split:
+            n1 = w // 2
+            n2 = w - n1
+            nxt += [(c0, n1), (c0 + n1, n2)]
+            a = A.sub(0, c0 + n1, m, n2)      # A_right
+            b = A.sub(0, c0, m, n1)           # A_left
+            c = C.sub(c0 + n1, c0, n2, n1)    # C21
+            if min(n1, n2) >= params.strassen_min and m >= 2:
+                fused.append((a, b, c))
+            else:
+                plain.append((a, b, c))
+        if plain:
+            for (a, b, c) in plain:
+                pb.product("gemm", m, a.cols, b.cols, [(a, 1.0)], [(b, 1.0)],
+                           [(c, 1.0)], group=group)
+            group += 1
+        if fused:
+            per_node = [_strassen_products(a, b, c) for (a, b, c) in fused]
+            for pi in range(7):
+                for prods in per_node:
+                    s_shape, s_terms, t_shape, t_terms, dests = prods[pi]
+                    ms, ns = s_shape if s_shape else (s_terms[0][0].rows, s_terms[0][0].cols)
+                    _, kt = t_shape if t_shape else (t_terms[0][0].rows, t_terms[0][0].cols)
+                    pb.product("gemm", ms, ns, kt, s_terms, t_terms, dests, group=group)
+                group += 1
+        nodes = nxt
+    for (c0, w) in sorted(nodes):
+        pb.product("syrk", m, w, w, [(A.sub(0, c0, m, w), 1.0)], [], [(C.sub(c0, c0, w, w), 1.0)],
+                   group=group)
+    return pb.finish()

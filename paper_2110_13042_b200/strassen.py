@@ -1,0 +1,66 @@
+"""Drop-in Strassen entry points (reference pkg/src/atamul/strassen.py:187-307).
+
+``fast_strassen(A, B, C, alpha, ws, threshold, counter)`` computes
+C += alpha * A^T B through the reference's Strassen recursion on the GPU
+(planner.plan_strassen_reference): same products, same odd-size semantics,
+same per-depth workspace, alpha applied only where leaf products accumulate
+(so scaling is exactly linear, strassen.py:284-285).
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import _native as nat
+from . import engine, planner
+from .errors import ShapeMismatchError, UnsupportedSizeError, WorkspaceUndersizedError
+from .matrix import DeviceOperand, MultCounter, as_array
+from .workspace import (DEFAULT_THRESHOLD, StrassenWorkspace, is_base_case,  # noqa: F401
+                        workspace_for_calls)
+
+
+def workspace_for(m: int, n: int, k: int, threshold: int = DEFAULT_THRESHOLD,
+                  dtype=np.float64) -> StrassenWorkspace:
+    """Workspace for one fast_strassen call on A (m x n), B (m x k) (strassen.py:187-192)."""
+    if min(m, n, k) < 1 or threshold < 1:
+        raise ShapeMismatchError("shape mismatch: dimensions must be >= 1")
+    return workspace_for_calls([(m, n, k)], threshold, dtype=dtype)
+
+
+def fast_strassen(A, B, C, alpha=1.0, ws: StrassenWorkspace | None = None,
+                  threshold: int = DEFAULT_THRESHOLD, counter: MultCounter | None = None) -> None:
+    """C += alpha * A^T B with A (m x n), B (m x k), C (n x k)."""
+    a, b, c = as_array(A), as_array(B), as_array(C)
+    m, n = int(a.shape[0]), int(a.shape[1])
+    if b.shape[0] != m:
+        raise ShapeMismatchError(f"shape mismatch: A {tuple(a.shape)} vs B {tuple(b.shape)}")
+    k = int(b.shape[1])
+    if tuple(c.shape) != (n, k):
+        raise ShapeMismatchError(f"shape mismatch: C {tuple(c.shape)} != {(n, k)}")
+    threshold = int(threshold)
+    C_ = DeviceOperand(c, writable=True)
+    A_ = DeviceOperand(a, dtype=C_.t.dtype, device=C_.t.device)
+    B_ = DeviceOperand(b, dtype=C_.t.dtype, device=C_.t.device)
+    if ws is None:
+        ws = workspace_for(m, n, k, threshold, dtype=C_.t.dtype)
+    elif not ws.covers(m, n, k, threshold):
+        raise WorkspaceUndersizedError(
+            f"workspace undersized for ({m},{n},{k}) at threshold {threshold}")
+    offs = tuple(ws.level_offsets())
+    key = ("strassen-ref", m, n, k, A_.ld, B_.ld, C_.ld, threshold, offs)
+    plan = engine.cached_plan(key, lambda: planner.plan_strassen_reference(
+        m, n, k, A_.ld, B_.ld, C_.ld, threshold, list(offs)))
+    wbuf = ws.ensure(C_.t.device) if plan.ws_scalars > 0 else None
+    engine.run_plan(plan, nat.dtype_code(C_.t.dtype), A_.ptr, A_.elems, C_.ptr, C_.elems, alpha,
+                    ws=int(wbuf.data_ptr()) if wbuf is not None else 0,
+                    ws_elems=int(wbuf.numel()) if wbuf is not None else 0,
+                    B=B_.ptr, b_elems=B_.elems)
+    C_.commit()
+    if counter is not None:
+        counter.add(plan.mults)
+
+
+def strassen_mult_count(n: int) -> int:
+    """7**log2(n) (strassen.py:302-307)."""
+    if n < 1 or n & (n - 1):
+        raise UnsupportedSizeError(f"unsupported size: {n} is not a power of two")
+    return 7 ** (n.bit_length() - 1)

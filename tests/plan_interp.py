@@ -1,0 +1,72 @@
+"""Test-only NumPy interpreter of native plan ops (include/atamul_b200.h).
+
+Executes a planner's op list on host arrays with the documented semantics,
+so planner logic (windows, signs, truncation, grouping) is checked on the CPU
+without a GPU.  Never used by the product path.
+"""
+import numpy as np
+
+OP_GEMM, OP_SYRK, OP_COMBO, OP_UPDATE, OP_FILL = 0, 1, 2, 3, 4
+
+
+def _win(bases, r, write=False):
+    base = bases[int(r["base"])]
+    rows, cols, off, ld = int(r["rows"]), int(r["cols"]), int(r["off"]), int(r["ld"])
+    if rows == 0 or cols == 0:
+        return None
+    flat = base.reshape(-1)
+    assert off >= 0 and off + (rows - 1) * ld + cols <= flat.size, "window out of bounds"
+    return np.lib.stride_tricks.as_strided(flat[off:], shape=(rows, cols),
+                                           strides=(ld * flat.itemsize, flat.itemsize),
+                                           writeable=write)
+
+
+def _operand(bases, refs, count, m, width, dtype):
+    out = np.zeros((m, width), dtype=dtype)
+    for j in range(count):
+        w = _win(bases, refs[j])
+        if w is None:
+            continue
+        r, c = min(w.shape[0], m), min(w.shape[1], width)
+        out[:r, :c] += float(refs[j]["sign"]) * w[:r, :c]
+    return out
+
+
+def run(ops, A, C, alpha=1.0, WS=None, B=None):
+    dtype = C.dtype
+    bases = {0: A, 1: C, 2: WS if WS is not None else np.zeros(1, dtype), 3: B if B is not None else A}
+    for op in ops:
+        t = int(op["type"])
+        if t in (OP_GEMM, OP_SYRK):
+            m, n, k = int(op["m"]), int(op["n"]), int(op["k"])
+            S = _operand(bases, op["s"], int(op["ns"]), m, n, dtype)
+            T = S if t == OP_SYRK else _operand(bases, op["t"], int(op["nt"]), m, k, dtype)
+            P = S.T @ T
+            for j in range(int(op["nd"])):
+                d = op["d"][j]
+                w = _win(bases, d, write=True)
+                v = alpha * float(d["sign"]) * P[:w.shape[0], :w.shape[1]]
+                if t == OP_SYRK:
+                    mask = np.tril(np.ones(w.shape, dtype=bool))
+                    if int(op["accumulate"]):
+                        w[mask] += v[mask]
+                    else:
+                        w[mask] = v[mask]
+                else:
+                    if int(op["accumulate"]):
+                        w += v
+                    else:
+                        w[...] = v
+        elif t == OP_COMBO:
+            d = _win(bases, op["d"][0], write=True)
+            d[...] = _operand(bases, op["s"], int(op["ns"]), d.shape[0], d.shape[1], dtype)
+        elif t == OP_UPDATE:
+            src = _win(bases, op["s"][0])
+            for j in range(int(op["nd"])):
+                w = _win(bases, op["d"][j], write=True)
+                w += float(op["d"][j]["sign"]) * src[:w.shape[0], :w.shape[1]]
+        elif t == OP_FILL:
+            _win(bases, op["d"][0], write=True)[...] = 0
+        else:
+            raise ValueError(t)
+    return C

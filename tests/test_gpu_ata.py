@@ -1,0 +1,136 @@
+"""GPU parity of the AtA / Strassen drop-ins against the reference's golden
+outputs and the oracle: reference-faithful plans (exact counts), auto plans,
+odd and degenerate shapes, workspace semantics, determinism, configs c1/c2."""
+import numpy as np
+import pytest
+
+from oracle import atamul_oracle as O
+
+pytestmark = pytest.mark.gpu
+
+
+def test_golden_cases(golden):
+    import paper_2110_13042_b200 as P
+    meta, arrays = golden
+    for case in meta["cases"]:
+        key = case["key"]
+        if case["kind"] == "ata":
+            a = arrays[key + "_A"]
+            n = a.shape[1]
+            c = np.zeros((n, n), dtype=a.dtype)
+            sentinel = 1.2345e67 if a.dtype == np.float64 else 3.0e30
+            c[np.triu_indices(n, 1)] = sentinel
+            cnt = P.MultCounter()
+            P.ata(a, c, case["alpha"], threshold=case["threshold"], counter=cnt)
+            assert cnt.scalar_mults == case["mults"], key
+            assert np.all(c[np.triu_indices(n, 1)] == sentinel), key
+            tol = 1e-10 if a.dtype == np.float64 else 1e-4
+            assert O.rel_frobenius_lower(c, arrays[key + "_C"]) <= tol, key
+        else:
+            a, b, c0 = arrays[key + "_A"], arrays[key + "_B"], arrays[key + "_C0"]
+            c = c0.copy()
+            cnt = P.MultCounter()
+            P.fast_strassen(a, b, c, 1.0, None, case["threshold"], cnt)
+            assert cnt.scalar_mults == case["mults"], key
+            ref = arrays[key + "_C"]
+            assert np.linalg.norm(c - ref) <= 1e-10 * max(np.linalg.norm(ref), 1.0), key
+
+
+def test_exact_counts_power_of_two(rng):
+    import paper_2110_13042_b200 as P
+    for n in [1, 2, 4, 8, 16, 32]:
+        cnt = P.MultCounter()
+        P.ata(rng.uniform(-1, 1, (n, n)), np.zeros((n, n)), 1.0, threshold=1, counter=cnt)
+        assert cnt.scalar_mults == P.ata_mult_count(n)
+        cnt = P.MultCounter()
+        P.fast_strassen(rng.normal(size=(n, n)), rng.normal(size=(n, n)), np.zeros((n, n)), 1.0,
+                        P.workspace_for(n, n, n, 1), 1, cnt)
+        assert cnt.scalar_mults == P.strassen_mult_count(n)
+
+
+@pytest.mark.parametrize("shape,t", [((1, 8), 4), ((8, 1), 4), ((63, 65), 16), ((512, 32), 512),
+                                     ((300, 17), 512), ((129, 65), 1), ((1000, 999), 4096)])
+def test_reference_plan_vs_oracle(shape, t, rng):
+    import paper_2110_13042_b200 as P
+    a = rng.uniform(-1, 1, shape)
+    got = P.ata_full(a, threshold=t).a
+    ref = O.gram(a)
+    assert np.abs(got - ref).max() <= 1e-9 * shape[0]
+    assert np.array_equal(got, got.T)
+
+
+@pytest.mark.parametrize("shape", [(1, 1), (3, 300), (1000, 1), (2000, 2500), (4097, 1537),
+                                   (5000, 3001)])
+def test_auto_plan_vs_oracle(shape, rng):
+    torch = pytest.importorskip("torch")
+    import paper_2110_13042_b200 as P
+    from paper_2110_13042_b200.planner import AutoParams
+    a = rng.standard_normal(shape)
+    n = shape[1]
+    for params in (AutoParams(), AutoParams(leaf_cols=256, strassen_min=256)):
+        A = torch.from_numpy(a).cuda()
+        C = torch.triu(torch.full((n, n), 7.0, dtype=torch.float64, device="cuda"), 1)
+        P.ata(A, C, 1.0, threshold="auto", auto_params=params)
+        got = C.cpu().numpy()
+        assert np.all(got[np.triu_indices(n, 1)] == 7.0)
+        assert O.rel_frobenius_lower(got, O.gram_blas(a)) <= 1e-13
+
+
+def test_workspace_reuse_zero_alloc_and_determinism(rng):
+    import paper_2110_13042_b200 as P
+    a, b = rng.uniform(-1, 1, (96, 80)), rng.uniform(-1, 1, (96, 70))
+    ws = P.workspace_for(96, 80, 70, 64)
+    c1 = np.zeros((80, 70))
+    P.fast_strassen(a, b, c1, 1.0, ws, threshold=64)
+    c2 = np.zeros((80, 70))
+    with P.count_allocations() as tr:
+        P.fast_strassen(a, b, c2, 1.0, ws, threshold=64)
+    assert tr["count"] == 0
+    assert np.array_equal(c1, c2)
+    c3 = np.zeros((80, 70))
+    P.fast_strassen(a, b, c3, 2.0, ws, threshold=64)
+    assert np.array_equal(c3, 2.0 * c1)
+
+
+def test_workspace_undersized_and_shape_errors():
+    import paper_2110_13042_b200 as P
+    ws = P.workspace_for_ata(8, 8, threshold=64)
+    with pytest.raises(P.WorkspaceUndersizedError):
+        P.ata(np.zeros((64, 64)), np.zeros((64, 64)), 1.0, threshold=64, ws=ws)
+    with pytest.raises(P.ShapeMismatchError):
+        P.ata(np.zeros((4, 3)), np.zeros((4, 4)))
+    ws = P.workspace_for(8, 8, 8, threshold=32)
+    with pytest.raises(P.WorkspaceUndersizedError):
+        P.fast_strassen(np.zeros((8, 8)), np.zeros((8, 8)), np.zeros((8, 8)), 1.0, ws, threshold=1)
+
+
+def test_config_c1_golden(golden):
+    """c1 (1024^2 U[-1,1], seed 0) at the parity cutoff t = 64^2: exact count,
+    sampled entries and checksums against the reference's own run."""
+    import paper_2110_13042_b200 as P
+    meta, arrays = golden
+    info = meta["c1"]
+    a = P.gen_matrix(1024, 1024, 0).a
+    c = np.zeros((1024, 1024))
+    cnt = P.MultCounter()
+    P.ata(a, c, 1.0, threshold=info["threshold"], counter=cnt)
+    assert cnt.scalar_mults == info["mults"]
+    il, jl = np.tril_indices(1024)
+    vals = c[il, jl]
+    samp = arrays["c1_sample_val"]
+    got = vals[arrays["c1_sample_idx"]]
+    assert np.linalg.norm(got - samp) / np.linalg.norm(samp) <= 1e-12
+    assert abs(np.linalg.norm(vals) - info["lower_fro"]) <= 1e-12 * info["lower_fro"]
+    rows = np.array([c[i, :i + 1].sum() for i in range(1024)])
+    assert np.linalg.norm(rows - arrays["c1_row_sums"]) <= 1e-11 * np.linalg.norm(arrays["c1_row_sums"])
+
+
+def test_config_c2_full_parity():
+    """c2 (6001x4097 N(0,1), seed 1, cutoff 256 -> t = 256^2): odd sizes on
+    every level, checked on the stored triangle against the oracle."""
+    import paper_2110_13042_b200 as P
+    from paper_2110_13042_b200.measure import config_matrix
+    a = config_matrix("c2")
+    c = np.zeros((4097, 4097))
+    P.ata(a, c, 1.0, threshold=256 * 256)
+    assert O.rel_frobenius_lower(c, O.gram_blas(a)) <= 1e-10

@@ -1,0 +1,156 @@
+"""Host planner logic on the CPU: workspace sizes and exact multiplication
+counts against the reference's golden values, and plan semantics through the
+NumPy plan interpreter against the oracle."""
+import numpy as np
+import pytest
+from hypothesis import given
+from hypothesis import strategies as st
+
+import plan_interp
+from oracle import atamul_oracle as O
+from paper_2110_13042_b200 import planner
+from paper_2110_13042_b200.workspace import ata_calls, calls_sizes, workspace_for_calls
+from paper_2110_13042_b200.strassen import workspace_for
+from paper_2110_13042_b200.ata import workspace_for_ata
+
+
+def _ata_plan(m, n, t, fuse=True):
+    ws = workspace_for_ata(m, n, t)
+    return planner.plan_ata_reference(m, n, n, n, t, ws.level_offsets(), fuse=fuse), ws
+
+
+def _interp_ata(plan, ws, a, alpha=1.0, sentinel=None):
+    n = a.shape[1]
+    c = np.zeros((n, n), dtype=a.dtype)
+    if sentinel is not None:
+        c[np.triu_indices(n, 1)] = sentinel
+    wsbuf = np.zeros(max(1, ws.total_scalars), dtype=a.dtype)
+    plan_interp.run(plan.ops, a, c, alpha, WS=wsbuf)
+    return c
+
+
+def test_workspace_sizes_match_reference(golden):
+    meta, _ = golden
+    for key, want in meta["workspace"].items():
+        parts = key.split("_")
+        if parts[0] == "strassen":
+            m, n, k, t = int(parts[1]), int(parts[2]), int(parts[3]), int(parts[4][1:])
+            ws = workspace_for(m, n, k, t)
+        else:
+            m, n, t = int(parts[1]), int(parts[2]), int(parts[3][1:])
+            ws = workspace_for_ata(m, n, t)
+        got = [[lv.prod.size, lv.lhs.size, lv.rhs.size] for lv in ws.levels]
+        assert got == want["levels"], key
+        assert list(ws.base_sizes) == want["base"], key
+
+
+def test_space_bound():
+    for n in (16, 64, 256):
+        assert workspace_for(n, n, n, 1).total_scalars <= 1.5 * n * n
+
+
+def test_covers():
+    ws = workspace_for(32, 32, 32, 4)
+    assert ws.covers(32, 32, 32, 4) and ws.covers(16, 16, 16, 4)
+    assert not ws.covers(33, 32, 32, 4)
+    assert not ws.covers(16, 20, 9, 4)
+    assert workspace_for(16, 20, 9, 4).covers(16, 20, 9, 4)
+
+
+@pytest.mark.parametrize("fuse", [True, False])
+def test_reference_plan_counts(golden, fuse):
+    meta, _ = golden
+    for key, want in meta["counts"].items():
+        parts = key.split("_")
+        if parts[0] == "ata" and parts[1] == "square":
+            n, t = int(parts[2]), int(parts[3][1:])
+            m = n
+        elif parts[0] == "ata":
+            m, n = map(int, parts[1].split("x"))
+            t = int(parts[2][1:])
+        else:
+            n = int(parts[2])
+            ws = workspace_for(n, n, n, 1)
+            p = planner.plan_strassen_reference(n, n, n, n, n, n, 1, ws.level_offsets(), fuse=fuse)
+            assert p.mults == want, key
+            continue
+        p, _ = _ata_plan(m, n, t, fuse)
+        assert p.mults == want, key
+
+
+@pytest.mark.parametrize("fuse", [True, False])
+def test_reference_plan_semantics(golden, fuse):
+    meta, arrays = golden
+    for case in meta["cases"]:
+        key = case["key"]
+        if case["kind"] == "ata":
+            a = arrays[key + "_A"]
+            m, n = a.shape
+            p, ws = _ata_plan(m, n, case["threshold"], fuse)
+            c = _interp_ata(p, ws, a, case["alpha"], sentinel=1.0e30)
+            ref = arrays[key + "_C"]
+            il, jl = np.tril_indices(n)
+            tol = 1e-12 if a.dtype == np.float64 else 1e-5
+            assert O.rel_frobenius_lower(c, ref) <= tol, key
+            assert np.all(c[np.triu_indices(n, 1)] == 1.0e30), key
+        else:
+            a, b, c0 = arrays[key + "_A"], arrays[key + "_B"], arrays[key + "_C0"]
+            m, n = a.shape
+            k = b.shape[1]
+            ws = workspace_for(m, n, k, case["threshold"])
+            p = planner.plan_strassen_reference(m, n, k, n, k, k, case["threshold"],
+                                                ws.level_offsets(), fuse=fuse)
+            c = c0.copy()
+            plan_interp.run(p.ops, a, c, 1.0, WS=np.zeros(max(1, ws.total_scalars)), B=b)
+            ref = arrays[key + "_C"]
+            assert np.abs(c - ref).max() <= 1e-12 * m, key
+
+
+def test_fused_plan_has_fewer_ops():
+    p_f, _ = _ata_plan(256, 256, 1024, True)
+    p_u, _ = _ata_plan(256, 256, 1024, False)
+    assert p_f.mults == p_u.mults
+    assert len(p_f.ops) < len(p_u.ops)
+
+
+@given(m=st.integers(1, 300), n=st.integers(1, 300), leaf=st.sampled_from([8, 16, 33, 64]),
+       smin=st.sampled_from([4, 16, 10**9]), seed=st.integers(0, 2**16))
+def test_auto_plan_semantics(m, n, leaf, smin, seed):
+    a = np.random.default_rng(seed).uniform(-1, 1, (m, n))
+    params = planner.AutoParams(leaf_cols=leaf, strassen_min=smin)
+    p = planner.plan_ata_auto(m, n, n, n, params)
+    c = np.zeros((n, n))
+    c[np.triu_indices(n, 1)] = 7.0
+    plan_interp.run(p.ops, a, c, 1.0)
+    assert np.all(c[np.triu_indices(n, 1)] == 7.0)
+    assert O.rel_frobenius_lower(c, O.gram(a)) <= 1e-12
+
+
+def _dest_cells(op, n_ld):
+    cells = set()
+    for j in range(int(op["nd"])):
+        d = op["d"][j]
+        rows, cols, off, ld = int(d["rows"]), int(d["cols"]), int(d["off"]), int(d["ld"])
+        for r in range(rows):
+            for c in range(cols):
+                if int(op["type"]) == 1 and c > r:
+                    continue
+                cells.add((int(d["base"]), off + r * ld + c))
+    return cells
+
+
+def test_auto_plan_groups_write_disjoint():
+    p = planner.plan_ata_auto(200, 150, 150, 150, planner.AutoParams(leaf_cols=16, strassen_min=8))
+    groups = {}
+    for op in p.ops:
+        g = int(op["group"])
+        if g < 0:
+            continue
+        groups.setdefault(g, []).append(op)
+    assert groups
+    for g, ops in groups.items():
+        seen = set()
+        for op in ops:
+            cells = _dest_cells(op, 150)
+            assert not (cells & seen), f"group {g} has overlapping destinations"
+            seen |= cells
