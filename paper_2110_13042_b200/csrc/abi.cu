@@ -91,12 +91,6 @@ template <>
 cudaError_t launch_batch<float>(const ata::BatchArgs<float>& a, cudaStream_t s, int dtype) {
   return ata::launch_batch_f32(a, s, dtype != ATA_TF32);
 }
-template <typename T>
-int tile_rows();
-template <>
-int tile_rows<double>() { return ata::tile_rows_f64(); }
-template <>
-int tile_rows<float>() { return ata::tile_rows_f32(); }
 
 int validate_op(const ata_op& op, const Bases& b, int i) {
   int rc;
@@ -157,7 +151,6 @@ int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, double alpha, cudaS
     int rc = validate_op(ops[i], b, i);
     if (rc) return rc;
   }
-  const int TR = tile_rows<T>();
   ata::BatchArgs<T> batch;
   std::memset(&batch, 0, sizeof(batch));
   batch.alpha = alpha;
@@ -166,7 +159,6 @@ int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, double alpha, cudaS
     if (batch.count == 0) return ATA_OK;
     cudaError_t e = launch_batch<T>(batch, s, dtype);
     batch.count = 0;
-    batch.total_tiles = 0;
     if (e != cudaSuccess) return cuda_fail(e, "product launch");
     return ATA_OK;
   };
@@ -190,14 +182,7 @@ int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, double alpha, cudaS
       for (int j = 0; j < op.ns; ++j) p.s[j] = term_of<T>(op.s[j], b);
       for (int j = 0; j < p.nt; ++j) p.t[j] = term_of<T>(op.t[j], b);
       for (int j = 0; j < op.nd; ++j) p.d[j] = dest_of<T>(op.d[j], b);
-      p.tn = (op.n + TR - 1) / TR;
-      p.tk = (op.k + TR - 1) / TR;
-      const long long tiles = p.kind == ata::kSyrk ? (long long)p.tn * (p.tn + 1) / 2
-                                                   : (long long)p.tn * p.tk;
-      if (batch.total_tiles + tiles > 0x7fffffffLL) return fail(ATA_E_UNSUPPORTED, "too many tiles");
-      p.tile_begin = batch.total_tiles;
-      batch.total_tiles += (int)tiles;
-      batch.count++;
+      batch.count++;  // tiling is chosen by the launcher for its tile shape
       batch_group = op.group;
       if (op.group < 0 && (rc = flush())) return rc;
       continue;

@@ -55,9 +55,8 @@ struct EwArgs {  // elementwise op: rows x cols iteration space
 
 // ---- host launchers (defined in gemm_*.cu / elementwise.cu) ----
 cudaError_t launch_batch_f64(const BatchArgs<double>& a, cudaStream_t s);
+cudaError_t launch_batch_f64_ws(const BatchArgs<double>& a, cudaStream_t s);
 cudaError_t launch_batch_f32(const BatchArgs<float>& a, cudaStream_t s, bool split);
-int tile_rows_f64();
-int tile_rows_f32();
 template <typename T> cudaError_t launch_combo(const EwArgs<T>& a, cudaStream_t s);
 template <typename T> cudaError_t launch_update(const EwArgs<T>& a, cudaStream_t s);
 template <typename T> cudaError_t launch_fill(T* p, long long ld, int rows, int cols, cudaStream_t s);

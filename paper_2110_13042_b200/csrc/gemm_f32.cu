@@ -271,7 +271,18 @@ static cudaError_t launch_cfg_f32(const BatchArgs<float>& a, cudaStream_t s) {
 }
 
 template <bool SPLIT>
-static cudaError_t launch_batch_f32_t(const BatchArgs<float>& a, cudaStream_t s) {
+static cudaError_t launch_batch_f32_t(BatchArgs<float> a, cudaStream_t s) {
+  long long total = 0;
+  for (int i = 0; i < a.count; ++i) {
+    DProd<float>& p = a.p[i];
+    p.tn = (p.n + f32cfg::BM - 1) / f32cfg::BM;
+    p.tk = (p.k + f32cfg::BN - 1) / f32cfg::BN;
+    p.tile_begin = (int)total;
+    total += p.kind == kSyrk ? (long long)p.tn * (p.tn + 1) / 2 : (long long)p.tn * p.tk;
+  }
+  if (total <= 0) return cudaSuccess;
+  if (total > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  a.total_tiles = (int)total;
   int ns = 1, nt = 1;
   for (int i = 0; i < a.count; ++i) {
     ns = max(ns, a.p[i].ns);
@@ -284,10 +295,8 @@ static cudaError_t launch_batch_f32_t(const BatchArgs<float>& a, cudaStream_t s)
 }
 
 cudaError_t launch_batch_f32(const BatchArgs<float>& a, cudaStream_t s, bool split) {
-  if (a.total_tiles <= 0) return cudaSuccess;
   return split ? launch_batch_f32_t<true>(a, s) : launch_batch_f32_t<false>(a, s);
 }
 
-int tile_rows_f32() { return f32cfg::BM; }
 
 }  // namespace ata
