@@ -135,10 +135,10 @@ def launch_units(plan):
                 flops += m * n * (n + 1)
         units.append((i, j, t in (nat.OP_GEMM, nat.OP_SYRK), flops))
         i = j
-    # the executor splits groups beyond 32 products into several launches
+    # the executor splits groups beyond 64 products into several launches
     launches = 0
     for (i, j, is_prod, _) in units:
-        launches += -(-(j - i) // 32) if is_prod else 1
+        launches += -(-(j - i) // 64) if is_prod else 1
     return units, launches
 
 
@@ -294,7 +294,7 @@ def main():
                 prod_flops += fl
             else:
                 ew_ms += d
-    prod_launches = sum(-(-(j - i) // 32) for (i, j, p, _) in units if p) * args.steps
+    prod_launches = sum(-(-(j - i) // 64) for (i, j, p, _) in units if p) * args.steps
     achieved = prod_flops / (prod_ms * 1e-3) / 1e12 if prod_ms > 0 else 0.0
     peak = FP64_PEAK_TFLOPS if f64 else TF32_PEAK_TFLOPS
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",

@@ -65,7 +65,9 @@ typedef struct ata_ref {
   int64_t off;   /* element offset from the base pointer */
   int64_t ld;    /* leading dimension (row stride) in elements */
   int32_t cols;
-  int32_t _pad;
+  int32_t region; /* destinations only: 0 = written by this op alone in its launch;
+                     r > 0 = a window shared with other ops of the same launch group,
+                     accumulated tile by tile in op order (deterministic) */
   double sign;   /* +1 / -1 coefficient */
 } ata_ref;
 
@@ -124,10 +126,15 @@ int ata_unpack_lower(int dtype, const void* packed, int32_t n, void* C, int64_t 
  * auto planner) on one stream.  Bases: A (input), B (second operand, may
  * equal A), C (output), WS (workspace of ws_elems elements).  Every ref is
  * bounds-checked against its base before any launch; ATA_E_WORKSPACE if a
- * workspace ref overruns ws_elems. */
+ * workspace ref overruns ws_elems.  `sync` is a caller-owned device int32
+ * buffer of sync_ints entries for the persistent kernels' work counter and
+ * per-tile turn counters (ata_sync_ints_needed tells how many). */
 int ata_run_plan(int dtype, const ata_op* ops, int32_t n_ops, const void* A, int64_t a_elems,
                  const void* B, int64_t b_elems, void* C, int64_t c_elems, void* WS,
-                 int64_t ws_elems, double alpha, void* stream);
+                 int64_t ws_elems, void* sync, int64_t sync_ints, double alpha, void* stream);
+
+/* int32 entries of `sync` that ata_run_plan needs for this op list (host-only query). */
+int64_t ata_sync_ints_needed(int dtype, const ata_op* ops, int32_t n_ops);
 
 #ifdef __cplusplus
 }

@@ -23,7 +23,7 @@ MAX_TERMS, MAX_DESTS = 2, 4
 
 # numpy mirrors of ata_ref / ata_op (include/atamul_b200.h)
 REF_DTYPE = np.dtype([("base", "<i4"), ("rows", "<i4"), ("off", "<i8"), ("ld", "<i8"),
-                      ("cols", "<i4"), ("_pad", "<i4"), ("sign", "<f8")], align=True)
+                      ("cols", "<i4"), ("region", "<i4"), ("sign", "<f8")], align=True)
 OP_DTYPE = np.dtype([("type", "<i4"), ("m", "<i4"), ("n", "<i4"), ("k", "<i4"),
                      ("ns", "<i4"), ("nt", "<i4"), ("nd", "<i4"), ("accumulate", "<i4"),
                      ("group", "<i4"), ("_pad", "<i4"),
@@ -33,7 +33,7 @@ OP_DTYPE = np.dtype([("type", "<i4"), ("m", "<i4"), ("n", "<i4"), ("k", "<i4"),
 EXPORTS = [
     "ata_last_error", "ata_strerror", "ata_version", "ata_abi_op_size",
     "ata_syrk_lower", "ata_gemm_atb", "ata_add_truncated", "ata_mirror_lower",
-    "ata_pack_lower", "ata_unpack_lower", "ata_run_plan",
+    "ata_pack_lower", "ata_unpack_lower", "ata_run_plan", "ata_sync_ints_needed",
 ]
 
 _CODE_TO_EXC = {
@@ -74,7 +74,9 @@ def load() -> ctypes.CDLL:
     lib.ata_pack_lower.argtypes = [ctypes.c_int, c_vp, c_i64, c_i32, c_vp, c_vp]
     lib.ata_unpack_lower.argtypes = [ctypes.c_int, c_vp, c_i32, c_vp, c_i64, c_i32, c_vp]
     lib.ata_run_plan.argtypes = [ctypes.c_int, c_vp, c_i32, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64,
-                                 c_vp, c_i64, c_dbl, c_vp]
+                                 c_vp, c_i64, c_vp, c_i64, c_dbl, c_vp]
+    lib.ata_sync_ints_needed.argtypes = [ctypes.c_int, c_vp, c_i32]
+    lib.ata_sync_ints_needed.restype = ctypes.c_int64
     for name in EXPORTS:
         getattr(lib, name).restype = getattr(lib, name).restype or ctypes.c_int
     if lib.ata_abi_op_size() != OP_DTYPE.itemsize:

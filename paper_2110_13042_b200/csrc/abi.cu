@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstring>
 #include <string>
+#include <algorithm>
 #include <vector>
 
 #include "../../include/atamul_b200.h"
@@ -17,6 +18,8 @@
 namespace {
 
 thread_local std::string g_last_error;
+
+
 
 int fail(int code, const std::string& msg) {
   g_last_error = msg;
@@ -145,32 +148,101 @@ int validate_op(const ata_op& op, const Bases& b, int i) {
 }
 
 template <typename T>
-int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, double alpha, cudaStream_t s,
-               int dtype) {
-  for (int i = 0; i < n_ops; ++i) {
-    int rc = validate_op(ops[i], b, i);
-    if (rc) return rc;
-  }
-  ata::BatchArgs<T> batch;
-  std::memset(&batch, 0, sizeof(batch));
-  batch.alpha = alpha;
-  int batch_group = -1;
-  auto flush = [&]() -> int {
-    if (batch.count == 0) return ATA_OK;
-    cudaError_t e = launch_batch<T>(batch, s, dtype);
-    batch.count = 0;
-    if (e != cudaSuccess) return cuda_fail(e, "product launch");
-    return ATA_OK;
+bool supports_ordering();
+template <>
+bool supports_ordering<double>() { return ata::f64_supports_ordering(); }
+template <>
+bool supports_ordering<float>() { return false; }
+
+// Walk the op list with the executor's batching rule, calling on_batch(first, last)
+// for every product launch [first, last) and on_ew(i) for every elementwise op.
+// Consecutive GEMM/SYRK ops with equal group >= 0 share a launch (at most
+// kMaxBatch); when the launcher cannot order shared destinations, a product
+// whose region already occurs in the open batch starts a new launch.
+template <typename F1, typename F2>
+int walk_batches(const ata_op* ops, int n_ops, bool ordering, F1 on_batch, F2 on_ew) {
+  int first = -1, group = -1, count = 0;
+  std::vector<int> regions;
+  auto flush = [&](int end) -> int {
+    int rc = ATA_OK;
+    if (count > 0) rc = on_batch(first, end);
+    first = -1;
+    count = 0;
+    regions.clear();
+    return rc;
   };
   for (int i = 0; i < n_ops; ++i) {
     const ata_op& op = ops[i];
     int rc;
     if (op.type == ATA_OP_GEMM || op.type == ATA_OP_SYRK) {
-      const bool join = batch.count > 0 && op.group >= 0 && op.group == batch_group &&
-                        batch.count < ata::kMaxBatch;
-      if (!join && (rc = flush())) return rc;
-      ata::DProd<T>& p = batch.p[batch.count];
-      std::memset(&p, 0, sizeof(p));
+      bool join = count > 0 && op.group >= 0 && op.group == group && count < ata::kMaxBatch;
+      if (join && !ordering) {
+        for (int j = 0; j < op.nd && join; ++j)
+          if (op.d[j].region > 0)
+            for (int r : regions)
+              if (r == op.d[j].region) join = false;
+      }
+      if (!join && (rc = flush(i))) return rc;
+      if (count == 0) first = i;
+      ++count;
+      group = op.group;
+      for (int j = 0; j < op.nd; ++j)
+        if (op.d[j].region > 0) regions.push_back(op.d[j].region);
+      if (op.group < 0 && (rc = flush(i + 1))) return rc;
+      continue;
+    }
+    if ((rc = flush(i))) return rc;
+    if ((rc = on_ew(i))) return rc;
+  }
+  return flush(n_ops);
+}
+
+// Turn counters one launch needs: 1 work counter + one per tile of each shared region.
+int64_t batch_sync_ints(const ata_op* ops, int first, int last) {
+  const int TILE = 128;
+  std::vector<std::pair<int, std::pair<int, int>>> reg;  // region -> (tile rows, tile cols)
+  int64_t total = 1;
+  for (int i = first; i < last; ++i)
+    for (int j = 0; j < ops[i].nd; ++j) {
+      const int r = ops[i].d[j].region;
+      if (r <= 0) continue;
+      const int tn = (ops[i].n + TILE - 1) / TILE, tk = (ops[i].k + TILE - 1) / TILE;
+      bool found = false;
+      for (auto& e : reg)
+        if (e.first == r) {
+          e.second.first = std::max(e.second.first, tn);
+          e.second.second = std::max(e.second.second, tk);
+          found = true;
+        }
+      if (!found) reg.push_back({r, {tn, tk}});
+    }
+  for (auto& e : reg) total += (int64_t)e.second.first * e.second.second;
+  return total;
+}
+
+template <typename T>
+int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, int* sync, int64_t sync_ints,
+               double alpha, cudaStream_t s, int dtype) {
+  for (int i = 0; i < n_ops; ++i) {
+    int rc = validate_op(ops[i], b, i);
+    if (rc) return rc;
+  }
+  const bool ordering = supports_ordering<T>();
+  ata::BatchArgs<T> batch;
+  auto on_batch = [&](int first, int last) -> int {
+    std::memset(&batch, 0, sizeof(batch));
+    batch.alpha = alpha;
+    const int64_t need = batch_sync_ints(ops, first, last);
+    if (ordering && need > 1 && (sync == nullptr || need > sync_ints))
+      return fail(ATA_E_WORKSPACE, "workspace undersized: sync buffer needs " +
+                                       std::to_string(need) + " ints, have " +
+                                       std::to_string(sync_ints));
+    batch.sync = sync;
+    batch.n_sync = (int)(sync_ints < 0x7fffffff ? sync_ints : 0x7fffffff);
+    std::vector<int> ids;  // batch-local region numbering (1-based)
+    for (int i = first; i < last; ++i) {
+      const ata_op& op = ops[i];
+      ata::DProd<T>& p = batch.p[batch.count++];
       p.kind = op.type == ATA_OP_SYRK ? ata::kSyrk : ata::kGemm;
       p.m = op.m;
       p.n = op.n;
@@ -181,13 +253,27 @@ int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, double alpha, cudaS
       p.accumulate = op.accumulate;
       for (int j = 0; j < op.ns; ++j) p.s[j] = term_of<T>(op.s[j], b);
       for (int j = 0; j < p.nt; ++j) p.t[j] = term_of<T>(op.t[j], b);
-      for (int j = 0; j < op.nd; ++j) p.d[j] = dest_of<T>(op.d[j], b);
-      batch.count++;  // tiling is chosen by the launcher for its tile shape
-      batch_group = op.group;
-      if (op.group < 0 && (rc = flush())) return rc;
-      continue;
+      for (int j = 0; j < op.nd; ++j) {
+        p.d[j] = dest_of<T>(op.d[j], b);
+        p.d[j].sem = 0;
+        if (ordering && op.d[j].region > 0) {
+          int id = 0;
+          for (size_t q = 0; q < ids.size(); ++q)
+            if (ids[q] == op.d[j].region) id = (int)q + 1;
+          if (id == 0) {
+            ids.push_back(op.d[j].region);
+            id = (int)ids.size();
+          }
+          p.d[j].sem = id;
+        }
+      }
     }
-    if ((rc = flush())) return rc;
+    cudaError_t e = launch_batch<T>(batch, s, dtype);
+    if (e != cudaSuccess) return cuda_fail(e, "product launch");
+    return ATA_OK;
+  };
+  auto on_ew = [&](int i) -> int {
+    const ata_op& op = ops[i];
     cudaError_t e = cudaSuccess;
     if (op.type == ATA_OP_COMBO || op.type == ATA_OP_UPDATE) {
       ata::EwArgs<T> a;
@@ -213,8 +299,9 @@ int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, double alpha, cudaS
       e = ata::launch_fill<T>(d.p, d.ld, d.rows, d.cols, s);
     }
     if (e != cudaSuccess) return cuda_fail(e, "elementwise launch");
-  }
-  return flush();
+    return ATA_OK;
+  };
+  return walk_batches(ops, n_ops, ordering, on_batch, on_ew);
 }
 
 }  // namespace
@@ -240,9 +327,23 @@ const char* ata_strerror(int code) {
 int ata_version(void) { return 100; }
 int ata_abi_op_size(void) { return (int)sizeof(ata_op); }
 
+int64_t ata_sync_ints_needed(int dtype, const ata_op* ops, int32_t n_ops) {
+  if (n_ops <= 0 || ops == nullptr) return 1;
+  const bool ordering = dtype == ATA_F64 ? ata::f64_supports_ordering() : false;
+  int64_t need = 1;
+  walk_batches(
+      ops, n_ops, ordering,
+      [&](int first, int last) -> int {
+        need = std::max(need, batch_sync_ints(ops, first, last));
+        return ATA_OK;
+      },
+      [](int) -> int { return ATA_OK; });
+  return need;
+}
+
 int ata_run_plan(int dtype, const ata_op* ops, int32_t n_ops, const void* A, int64_t a_elems,
                  const void* B, int64_t b_elems, void* C, int64_t c_elems, void* WS,
-                 int64_t ws_elems, double alpha, void* stream) {
+                 int64_t ws_elems, void* sync, int64_t sync_ints, double alpha, void* stream) {
   if (n_ops < 0 || (n_ops > 0 && ops == nullptr)) return fail(ATA_E_ARG, "null op list");
   Bases b;
   b.ptr[ATA_BASE_A] = static_cast<const char*>(A);
@@ -256,11 +357,11 @@ int ata_run_plan(int dtype, const ata_op* ops, int32_t n_ops, const void* A, int
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   if (dtype == ATA_F64) {
     b.esize = 8;
-    return run_plan_t<double>(ops, n_ops, b, alpha, s, dtype);
+    return run_plan_t<double>(ops, n_ops, b, static_cast<int*>(sync), sync_ints, alpha, s, dtype);
   }
   if (dtype == ATA_F32 || dtype == ATA_TF32) {
     b.esize = 4;
-    return run_plan_t<float>(ops, n_ops, b, alpha, s, dtype);
+    return run_plan_t<float>(ops, n_ops, b, static_cast<int*>(sync), sync_ints, alpha, s, dtype);
   }
   return fail(ATA_E_ARG, "unknown dtype");
 }
@@ -293,7 +394,7 @@ int ata_syrk_lower(int dtype, const void* A, int64_t lda, int32_t m, int32_t n, 
   op.s[0] = mkref(ATA_BASE_A, lda, m, n);
   op.d[0] = mkref(ATA_BASE_C, ldc, n, n);
   const long long ae = (long long)(m - 1) * lda + n, ce = (long long)(n - 1) * ldc + n;
-  return ata_run_plan(dtype, &op, 1, A, ae, nullptr, 0, C, ce, nullptr, 0, alpha, stream);
+  return ata_run_plan(dtype, &op, 1, A, ae, nullptr, 0, C, ce, nullptr, 0, nullptr, 0, alpha, stream);
 }
 
 int ata_gemm_atb(int dtype, const void* A, int64_t lda, const void* B, int64_t ldb, int32_t m,
@@ -315,7 +416,7 @@ int ata_gemm_atb(int dtype, const void* A, int64_t lda, const void* B, int64_t l
   op.d[0] = mkref(ATA_BASE_C, ldc, n, k);
   const long long ae = (long long)(m - 1) * lda + n, be = (long long)(m - 1) * ldb + k,
                   ce = (long long)(n - 1) * ldc + k;
-  return ata_run_plan(dtype, &op, 1, A, ae, B, be, C, ce, nullptr, 0, alpha, stream);
+  return ata_run_plan(dtype, &op, 1, A, ae, B, be, C, ce, nullptr, 0, nullptr, 0, alpha, stream);
 }
 
 int ata_add_truncated(int dtype, void* dst, int64_t ldd, int32_t dr, int32_t dc, const void* src,
@@ -336,7 +437,7 @@ int ata_add_truncated(int dtype, void* dst, int64_t ldd, int32_t dr, int32_t dc,
   op.d[0] = mkref(ATA_BASE_C, ldd, r, c);
   op.d[0].sign = scale;
   const long long se = (long long)(sr - 1) * lds + sc, de = (long long)(dr - 1) * ldd + dc;
-  return ata_run_plan(dtype, &op, 1, src, se, nullptr, 0, dst, de, nullptr, 0, 1.0, stream);
+  return ata_run_plan(dtype, &op, 1, src, se, nullptr, 0, dst, de, nullptr, 0, nullptr, 0, 1.0, stream);
 }
 
 int ata_mirror_lower(int dtype, void* C, int64_t ldc, int32_t n, void* stream) {

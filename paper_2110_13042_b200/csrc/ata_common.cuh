@@ -5,7 +5,7 @@
 
 namespace ata {
 
-constexpr int kMaxBatch = 32;  // products per grouped launch (kernel-param by value)
+constexpr int kMaxBatch = 64;  // products per grouped launch (kernel-param by value, < 32 KB)
 
 template <typename T>
 struct DTerm {  // zero-extended read window
@@ -21,6 +21,10 @@ struct DDest {  // truncated write window
   long long ld;
   int rows, cols;
   double sign;
+  int sem;     // >= 0: base of this region's per-tile turn counters (ordered accumulation)
+  int sem_ld;  // tile columns of the region (counter row pitch)
+  int turn;    // this product's position in the region's accumulation order
+  int _pad;
 };
 
 enum : int { kGemm = 0, kSyrk = 1 };
@@ -43,6 +47,9 @@ struct BatchArgs {
   int count;
   int total_tiles;
   double alpha;
+  int* sync;  // [0] = work counter, [1..] = destination turn counters (zeroed per launch)
+  int n_sync;  // ints available at sync
+  int dynamic; // 1: tiles handed out by the work counter (needed for ordered destinations)
   DProd<T> p[kMaxBatch];
 };
 
@@ -56,6 +63,7 @@ struct EwArgs {  // elementwise op: rows x cols iteration space
 // ---- host launchers (defined in gemm_*.cu / elementwise.cu) ----
 cudaError_t launch_batch_f64(const BatchArgs<double>& a, cudaStream_t s);
 cudaError_t launch_batch_f64_ws(const BatchArgs<double>& a, cudaStream_t s);
+bool f64_supports_ordering();
 cudaError_t launch_batch_f32(const BatchArgs<float>& a, cudaStream_t s, bool split);
 template <typename T> cudaError_t launch_combo(const EwArgs<T>& a, cudaStream_t s);
 template <typename T> cudaError_t launch_update(const EwArgs<T>& a, cudaStream_t s);

@@ -307,6 +307,8 @@ static int pick_cfg() {
   return cfg;
 }
 
+bool f64_supports_ordering() { return pick_cfg() == 4; }
+
 template <int NS, int NT>
 static cudaError_t launch_terms(const BatchArgs<double>& a, cudaStream_t s) {
   switch (pick_cfg()) {

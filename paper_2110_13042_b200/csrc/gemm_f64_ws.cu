@@ -1,22 +1,31 @@
-// FP64 generalized-product kernel, warp-specialised (sm_100a, DMMA.8x8x4).
+// FP64 generalized-product kernel: persistent, warp-specialised (sm_100a, DMMA.8x8x4).
 //
-// Same product semantics as gemm_f64.cu (fused zero-extended operand terms =
-// Strassen pre-additions, strassen.py:195-203; fused truncated destinations =
-// post-additions, strassen.py:238-275 / matrix.py:218-239; SYRK lower tiles,
-// matrix.py:292-311).  Structure:
+// Product semantics (shared with gemm_f64.cu / gemm_f32.cu):
+//     D_d[:r_d, :c_d] (+)= sign_d * alpha * (sum_i s_i S_i)^T (sum_j t_j T_j)
+// - up to two zero-extended operand terms per side: the Strassen pre-additions
+//   (strassen.py:195-203) fused into the tile load;
+// - up to four truncated destinations: the Strassen post-additions
+//   (strassen.py:238-275 through add_truncated, matrix.py:218-239) fused into the
+//   epilogue;
+// - kind kSyrk = naive_syrk_lower (matrix.py:292-311) on lower-triangle tiles,
+//   diagonal tiles masked on store (strict upper never touched, ata.py:121-123).
 //
-//   warp 0      producer: cp.async (16 B, or 8 B for odd pitches) of the
-//               [BK x 128] operand windows into a STAGES-deep smem ring, with
-//               zero-fill outside each term window; two-term operands are
-//               combined in place by the producer once its copies land.
-//               Completion is published through per-stage "full" mbarriers.
-//   warps 1..8  consumers: 2 x 4 warps, 64 x 32 accumulator each (32 DMMA
-//               8x8x4 blocks, fragments straight from the padded smem rows),
-//               release a stage through its "empty" mbarrier; no CTA-wide
-//               barrier in the main loop.  Epilogue writes up to four signed,
-//               truncated destinations from registers.
-//
-// SYRK diagonal tiles load the operand panel once (both MMA operands read it).
+// Structure (one CTA per SM, persistent):
+//   warpgroup 0 (128 threads, 40 regs)  producer: fetches output tiles from a
+//       global work counter in launch order, streams [BK x 128] operand windows
+//       with cp.async (16 B, or 8 B for odd pitches; zero-fill outside each
+//       term window) into a STAGES-deep smem ring, combines two-term operands
+//       in place once its own copies land, publishes through "full" mbarriers.
+//   warpgroups 1-2 (256 threads, 232 regs)  consumers: 2 x 4 warps, 64 x 32
+//       accumulators of 8x8 DMMA blocks read straight from padded smem rows,
+//       release stages through "empty" mbarriers.  Epilogue: signed, truncated
+//       RMW of every destination; a destination shared by several products of
+//       the launch (a C quadrant of one Strassen node) is accumulated in
+//       product order through per-tile turn counters, so results are bitwise
+//       deterministic and a whole Strassen node (or level) is ONE launch
+//       (no wave-quantisation tail per product).
+// Deadlock freedom: tiles are handed out in increasing order and a tile only
+// waits for turns of strictly earlier tiles, which are already running.
 #include "ata_common.cuh"
 
 namespace ata {
@@ -28,6 +37,7 @@ constexpr int PRODUCER_REGS = 40, CONSUMER_REGS = 232;  // setmaxnreg split of t
 constexpr int WTM = 8, WTN = 4;  // 64 x 32 per consumer warp
 constexpr int BUF = BK * LD;     // doubles per operand buffer
 constexpr int SMEM_BUDGET = 225 * 1024;
+constexpr int TSLOTS = 2;        // tile-info ring
 }  // namespace ws64
 
 __device__ __forceinline__ void dmma_ws(double (&c)[2], double a, double b) {
@@ -57,16 +67,27 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;\n" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];\n" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;\n" ::"l"(p), "r"(v) : "memory");
+}
 
-// One producer warp copies a BK x 128 window of term t (rows l0.., cols c0..).
+// The producer warpgroup copies a BK x 128 window of term t (rows l0.., cols c0..).
 template <bool VEC16>
-__device__ __forceinline__ void ws_load(double* buf, const DTerm<double>& t, int l0, int c0, int lane) {
+__device__ __forceinline__ void ws_load(double* buf, const DTerm<double>& t, int l0, int c0, int pt) {
   using namespace ws64;
   if (VEC16) {
-#pragma unroll 8
+#pragma unroll
     for (int i = 0; i < BK * (BM / 2) / PRODUCERS; ++i) {
-      const int id = lane + i * PRODUCERS;
-      const int r = id >> 6;            // BM/2 = 64 chunks per row
+      const int id = pt + i * PRODUCERS;
+      const int r = id >> 6;  // BM/2 = 64 chunks per row
       const int c = (id & 63) * 2;
       const int gl = l0 + r, gc = c0 + c;
       int bytes = 0;
@@ -78,9 +99,9 @@ __device__ __forceinline__ void ws_load(double* buf, const DTerm<double>& t, int
       cp_async_16(buf + r * LD + c, src, bytes);
     }
   } else {
-#pragma unroll 8
+#pragma unroll
     for (int i = 0; i < BK * BM / PRODUCERS; ++i) {
-      const int id = lane + i * PRODUCERS;
+      const int id = pt + i * PRODUCERS;
       const int r = id >> 7;
       const int c = id & 127;
       const int gl = l0 + r, gc = c0 + c;
@@ -92,12 +113,12 @@ __device__ __forceinline__ void ws_load(double* buf, const DTerm<double>& t, int
 }
 
 template <bool VEC16>
-__device__ __forceinline__ void ws_combine(double* x, const double* y, double sign, int lane) {
+__device__ __forceinline__ void ws_combine(double* x, const double* y, double sign, int pt) {
   using namespace ws64;
   if (VEC16) {
-#pragma unroll 8
+#pragma unroll
     for (int i = 0; i < BK * (BM / 2) / PRODUCERS; ++i) {
-      const int id = lane + i * PRODUCERS;
+      const int id = pt + i * PRODUCERS;
       const int r = id >> 6;
       const int c = (id & 63) * 2;
       double2* px = reinterpret_cast<double2*>(x + r * LD + c);
@@ -108,9 +129,9 @@ __device__ __forceinline__ void ws_combine(double* x, const double* y, double si
       *px = v;
     }
   } else {
-#pragma unroll 8
+#pragma unroll
     for (int i = 0; i < BK * BM / PRODUCERS; ++i) {
-      const int id = lane + i * PRODUCERS;
+      const int id = pt + i * PRODUCERS;
       const int r = id >> 7;
       const int c = id & 127;
       x[r * LD + c] = fma(sign, y[r * LD + c], x[r * LD + c]);
@@ -122,6 +143,36 @@ __device__ __forceinline__ bool vec16_ok(const DTerm<double>& t) {
   return ((reinterpret_cast<uintptr_t>(t.p) & 15) == 0) && ((t.ld & 1) == 0);
 }
 
+struct TileInfo {
+  int pi, ti, tj;
+};
+
+__device__ __forceinline__ TileInfo decode_tile(const BatchArgs<double>& args, int tile) {
+  int pi = 0;
+  while (pi + 1 < args.count && tile >= args.p[pi + 1].tile_begin) ++pi;
+  const DProd<double>& P = args.p[pi];
+  const int local = tile - P.tile_begin;
+  TileInfo t;
+  t.pi = pi;
+  if (P.kind == kSyrk) {
+    int r = (int)((sqrt(8.0 * (double)local + 1.0) - 1.0) * 0.5);
+    while ((r + 1) * (r + 2) / 2 <= local) ++r;
+    while (r * (r + 1) / 2 > local) --r;
+    t.ti = r;
+    t.tj = local - r * (r + 1) / 2;
+  } else {
+    // grouped raster: 8 tile-rows per group, column-major inside the group
+    const int per_group = 8 * P.tk;
+    const int grp = local / per_group;
+    const int first = grp * 8;
+    const int gsz = min(P.tn - first, 8);
+    const int in = local - grp * per_group;
+    t.ti = first + in % gsz;
+    t.tj = in / gsz;
+  }
+  return t;
+}
+
 template <int NS, int NT, int STAGES>
 __global__ void __launch_bounds__(ws64::THREADS, 1)
     prod_f64_ws_kernel(const __grid_constant__ BatchArgs<double> args) {
@@ -130,42 +181,22 @@ __global__ void __launch_bounds__(ws64::THREADS, 1)
   extern __shared__ __align__(128) double smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
   uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + TSLOTS;
+  int* tinfo = reinterpret_cast<int*>(tempty + TSLOTS);  // TSLOTS entries
+  int* bcast = tinfo + TSLOTS;                            // producer-internal broadcast
 
   const int tid = threadIdx.x;
-  const int lane = tid & 31, warp = tid >> 5;
-
-  // ---- locate product and output tile ----
-  const int tile = blockIdx.x;
-  int pi = 0;
-  while (pi + 1 < args.count && tile >= args.p[pi + 1].tile_begin) ++pi;
-  const DProd<double>& P = args.p[pi];
-  const int local = tile - P.tile_begin;
-  int ti, tj;
-  if (P.kind == kSyrk) {
-    int r = (int)((sqrt(8.0 * (double)local + 1.0) - 1.0) * 0.5);
-    while ((r + 1) * (r + 2) / 2 <= local) ++r;
-    while (r * (r + 1) / 2 > local) --r;
-    ti = r;
-    tj = local - r * (r + 1) / 2;
-  } else {
-    const int per_group = 8 * P.tk;
-    const int grp = local / per_group;
-    const int first = grp * 8;
-    const int gsz = min(P.tn - first, 8);
-    const int in = local - grp * per_group;
-    ti = first + in % gsz;
-    tj = in / gsz;
-  }
-  const int i0 = ti * BM, j0 = tj * BN;
-  const bool syrk = (P.kind == kSyrk);
-  const bool same = syrk && ti == tj;  // diagonal SYRK tile: one operand panel
-  const int ns = P.ns, nt = syrk ? 1 : P.nt;
-  const int KT = (P.m + BK - 1) / BK;
+  const int warp = tid >> 5;
 
   if (tid == 0) {
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], PRODUCERS);
       mbar_init(&empty[s], CONSUMERS);
+    }
+    for (int s = 0; s < TSLOTS; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], CONSUMERS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
@@ -174,138 +205,218 @@ __global__ void __launch_bounds__(ws64::THREADS, 1)
   if (tid < PRODUCERS) {
     // ===================== producer warpgroup =====================
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PRODUCER_REGS));
-    const int lane = tid;  // producer thread index
-    const DTerm<double>& S0 = P.s[0];
-    const DTerm<double>& S1 = P.s[1];
-    const DTerm<double>& T0 = syrk ? P.s[0] : P.t[0];
-    const DTerm<double>& T1 = P.t[1];
-    const bool vs = vec16_ok(S0) && (ns < 2 || vec16_ok(S1));
-    const bool vt = vec16_ok(T0) && (nt < 2 || vec16_ok(T1));
-    const bool comb = (NS == 2 && ns == 2) || (NT == 2 && nt == 2);
-    auto issue = [&](int kt) {
-      double* base = smem + (kt % STAGES) * STAGE;
-      const int l0 = kt * BK;
-      if (vs) ws_load<true>(base, S0, l0, i0, lane);
-      else ws_load<false>(base, S0, l0, i0, lane);
-      if (NS == 2 && ns == 2) {
-        if (vs) ws_load<true>(base + BUF, S1, l0, i0, lane);
-        else ws_load<false>(base + BUF, S1, l0, i0, lane);
+    const int pt = tid;
+    int kstep = 0;  // global k-step counter (stage ring position)
+    for (int it = 0;; ++it) {
+      if (pt == 0) *bcast = args.dynamic ? atomicAdd(args.sync, 1) : (int)(blockIdx.x + it * gridDim.x);
+      named_sync(1, PRODUCERS);
+      const int tile = *bcast;
+      named_sync(1, PRODUCERS);
+      const int slot = it % TSLOTS;
+      if (pt == 0) {
+        if (it >= TSLOTS) mbar_wait(&tempty[slot], ((it / TSLOTS) - 1) & 1);
+        tinfo[slot] = tile;
+        mbar_arrive(&tfull[slot]);
       }
-      if (!same) {
-        double* tb = base + NS * BUF;
-        if (vt) ws_load<true>(tb, T0, l0, j0, lane);
-        else ws_load<false>(tb, T0, l0, j0, lane);
+      if (tile >= args.total_tiles) break;
+      const TileInfo tl = decode_tile(args, tile);
+      const DProd<double>& P = args.p[tl.pi];
+      const bool syrk = P.kind == kSyrk;
+      const bool same = syrk && tl.ti == tl.tj;
+      const int ns = P.ns, nt = syrk ? 1 : P.nt;
+      const int i0 = tl.ti * BM, j0 = tl.tj * BN;
+      const DTerm<double>& S0 = P.s[0];
+      const DTerm<double>& S1 = P.s[1];
+      const DTerm<double>& T0 = syrk ? P.s[0] : P.t[0];
+      const DTerm<double>& T1 = P.t[1];
+      const bool vs = vec16_ok(S0) && (ns < 2 || vec16_ok(S1));
+      const bool vt = vec16_ok(T0) && (nt < 2 || vec16_ok(T1));
+      const bool comb = (NS == 2 && ns == 2) || (NT == 2 && nt == 2);
+      const int KT = (P.m + BK - 1) / BK;
+      auto issue = [&](int kt, int ring) {
+        double* base = smem + (ring % STAGES) * STAGE;
+        const int l0 = kt * BK;
+        if (vs) ws_load<true>(base, S0, l0, i0, pt);
+        else ws_load<false>(base, S0, l0, i0, pt);
+        if (NS == 2 && ns == 2) {
+          if (vs) ws_load<true>(base + BUF, S1, l0, i0, pt);
+          else ws_load<false>(base + BUF, S1, l0, i0, pt);
+        }
+        if (!same) {
+          double* tb = base + NS * BUF;
+          if (vt) ws_load<true>(tb, T0, l0, j0, pt);
+          else ws_load<false>(tb, T0, l0, j0, pt);
+          if (NT == 2 && nt == 2) {
+            if (vt) ws_load<true>(tb + BUF, T1, l0, j0, pt);
+            else ws_load<false>(tb + BUF, T1, l0, j0, pt);
+          }
+        }
+      };
+      auto finish = [&](int ring) {  // combine two-term operands of a stage, publish it
+        double* base = smem + (ring % STAGES) * STAGE;
+        if (NS == 2 && ns == 2) {
+          if (vs) ws_combine<true>(base, base + BUF, S1.sign, pt);
+          else ws_combine<false>(base, base + BUF, S1.sign, pt);
+        }
         if (NT == 2 && nt == 2) {
-          if (vt) ws_load<true>(tb + BUF, T1, l0, j0, lane);
-          else ws_load<false>(tb + BUF, T1, l0, j0, lane);
+          double* tb = base + NS * BUF;
+          if (vt) ws_combine<true>(tb, tb + BUF, T1.sign, pt);
+          else ws_combine<false>(tb, tb + BUF, T1.sign, pt);
+        }
+        mbar_arrive(&full[ring % STAGES]);
+      };
+      for (int kt = 0; kt < KT; ++kt, ++kstep) {
+        const int s = kstep % STAGES;
+        if (kstep >= STAGES) mbar_wait(&empty[s], ((kstep / STAGES) - 1) & 1);
+        issue(kt, kstep);
+        if (!comb) {
+          mbar_arrive_cpasync(&full[s]);
+        } else {
+          cp_async_commit();
+          if (kt >= 1) {
+            cp_async_wait<1>();
+            finish(kstep - 1);
+          }
         }
       }
-    };
-    auto finish = [&](int kt) {  // combine two-term operands of stage kt, publish it
-      double* base = smem + (kt % STAGES) * STAGE;
-      if (NS == 2 && ns == 2) {
-        if (vs) ws_combine<true>(base, base + BUF, S1.sign, lane);
-        else ws_combine<false>(base, base + BUF, S1.sign, lane);
-      }
-      if (NT == 2 && nt == 2) {
-        double* tb = base + NS * BUF;
-        if (vt) ws_combine<true>(tb, tb + BUF, T1.sign, lane);
-        else ws_combine<false>(tb, tb + BUF, T1.sign, lane);
-      }
-      mbar_arrive(&full[kt % STAGES]);
-    };
-    for (int kt = 0; kt < KT; ++kt) {
-      const int s = kt % STAGES;
-      if (kt >= STAGES) mbar_wait(&empty[s], ((kt / STAGES) - 1) & 1);
-      issue(kt);
-      if (!comb) {
-        mbar_arrive_cpasync(&full[s]);
-      } else {
-        cp_async_commit();
-        if (kt >= 1) {
-          cp_async_wait<1>();
-          finish(kt - 1);
-        }
+      if (comb) {
+        cp_async_wait<0>();
+        finish(kstep - 1);
       }
     }
-    if (comb && KT >= 1) {
-      cp_async_wait<0>();
-      finish(KT - 1);
-    }
+    cp_async_wait<0>();
     return;
   }
 
-  // ===================== consumers =====================
+  // ===================== consumer warpgroups =====================
   asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(CONSUMER_REGS));
+  const int ctid = tid - PRODUCERS;
+  const int lane = tid & 31;
   const int cw = warp - PRODUCERS / 32;
   const int wm = cw >> 2, wn = cw & 3;  // 2 x 4 consumer warps
   const int g = lane >> 2, q = lane & 3;
-  double acc[WTM][WTN][2];
-#pragma unroll
-  for (int r = 0; r < WTM; ++r)
-#pragma unroll
-    for (int c = 0; c < WTN; ++c) acc[r][c][0] = acc[r][c][1] = 0.0;
-
-  const int aoff = wm * (WTM * 8) + g + q * LD;
-  const int boff = (same ? 0 : NS * BUF) + wn * (WTN * 8) + g + q * LD;
-  for (int kt = 0; kt < KT; ++kt) {
-    const int s = kt % STAGES;
-    mbar_wait(&full[s], (kt / STAGES) & 1);
-    const double* As = smem + s * STAGE + aoff;
-    const double* Bs = smem + s * STAGE + boff;
-#pragma unroll
-    for (int kk = 0; kk < BK / 4; ++kk) {
-      double a[WTM], b[WTN];
-#pragma unroll
-      for (int r = 0; r < WTM; ++r) a[r] = As[kk * 4 * LD + r * 8];
-#pragma unroll
-      for (int c = 0; c < WTN; ++c) b[c] = Bs[kk * 4 * LD + c * 8];
-#pragma unroll
-      for (int r = 0; r < WTM; ++r)
-#pragma unroll
-        for (int c = 0; c < WTN; ++c) dmma_ws(acc[r][c], a[r], b[c]);
-    }
+  int kstep = 0;
+  for (int it = 0;; ++it) {
+    const int slot = it % TSLOTS;
+    mbar_wait(&tfull[slot], (it / TSLOTS) & 1);
+    const int tile = tinfo[slot];
     __syncwarp();
-    if (lane == 0) mbar_arrive(&empty[s]);
-  }
+    if (lane == 0) mbar_arrive(&tempty[slot]);
+    if (tile >= args.total_tiles) break;
+    const TileInfo tl = decode_tile(args, tile);
+    const DProd<double>& P = args.p[tl.pi];
+    const bool syrk = P.kind == kSyrk;
+    const bool same = syrk && tl.ti == tl.tj;
+    const int i0 = tl.ti * BM, j0 = tl.tj * BN;
+    const int KT = (P.m + BK - 1) / BK;
 
-  // ---- epilogue: fused post-additions into up to four destinations ----
-  const int nd = P.nd;
-  const bool accumulate = P.accumulate != 0;
-  for (int d = 0; d < nd; ++d) {
-    const DDest<double>& D = P.d[d];
-    const double scale = args.alpha * D.sign;
+    double acc[WTM][WTN][2];
 #pragma unroll
-    for (int r = 0; r < WTM; ++r) {
-      const int row = i0 + wm * (WTM * 8) + r * 8 + g;
-      if (row >= D.rows) continue;
-      double* drow = D.p + (long long)row * D.ld;
+    for (int r = 0; r < WTM; ++r)
 #pragma unroll
-      for (int c = 0; c < WTN; ++c) {
-        const int col = j0 + wn * (WTN * 8) + c * 8 + q * 2;
-        if (col + 1 < D.cols && (!syrk || col + 1 <= row) &&
-            ((reinterpret_cast<uintptr_t>(drow + col) & 15) == 0)) {
-          double2* p2 = reinterpret_cast<double2*>(drow + col);
-          double2 v = make_double2(scale * acc[r][c][0], scale * acc[r][c][1]);
-          if (accumulate) {
-            const double2 o = *p2;
-            v.x += o.x;
-            v.y += o.y;
+      for (int c = 0; c < WTN; ++c) acc[r][c][0] = acc[r][c][1] = 0.0;
+
+    const int aoff = wm * (WTM * 8) + g + q * LD;
+    const int boff = (same ? 0 : NS * BUF) + wn * (WTN * 8) + g + q * LD;
+    for (int kt = 0; kt < KT; ++kt, ++kstep) {
+      const int s = kstep % STAGES;
+      mbar_wait(&full[s], (kstep / STAGES) & 1);
+      const double* As = smem + s * STAGE + aoff;
+      const double* Bs = smem + s * STAGE + boff;
+#pragma unroll
+      for (int kk = 0; kk < BK / 4; ++kk) {
+        double a[WTM], b[WTN];
+#pragma unroll
+        for (int r = 0; r < WTM; ++r) a[r] = As[kk * 4 * LD + r * 8];
+#pragma unroll
+        for (int c = 0; c < WTN; ++c) b[c] = Bs[kk * 4 * LD + c * 8];
+#pragma unroll
+        for (int r = 0; r < WTM; ++r)
+#pragma unroll
+          for (int c = 0; c < WTN; ++c) dmma_ws(acc[r][c], a[r], b[c]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+
+    // ---- epilogue: fused post-additions into up to four destinations ----
+    const int nd = P.nd;
+    const bool accumulate = P.accumulate != 0;
+    for (int d = 0; d < nd; ++d) {
+      const DDest<double>& D = P.d[d];
+      const double scale = args.alpha * D.sign;
+      if (i0 >= D.rows || j0 >= D.cols) continue;  // tile entirely outside this window
+      int* sem = nullptr;
+      int turn = 0;
+      if (D.sem >= 0) {
+        // turn = earlier products of the launch whose window in this region covers the tile
+        for (int q = 0; q < tl.pi; ++q)
+          for (int e = 0; e < args.p[q].nd; ++e) {
+            const DDest<double>& E = args.p[q].d[e];
+            if (E.sem == D.sem && i0 < E.rows && j0 < E.cols) ++turn;
           }
-          *p2 = v;
-        } else {
+        sem = args.sync + D.sem + tl.ti * D.sem_ld + tl.tj;
+        if (ctid == 0) {
+          // bounded wait: a broken ordering invariant traps (launch error) instead of hanging
+          uint64_t t0;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+          while (ld_acquire(sem) != turn) {
+            __nanosleep(64);
+            uint64_t t1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            if (t1 - t0 > 20000000000ull) __trap();
+          }
+        }
+        named_sync(2, CONSUMERS * 32);
+      }
 #pragma unroll
-          for (int e = 0; e < 2; ++e) {
-            const int cc = col + e;
-            if (cc < D.cols && (!syrk || cc <= row)) {
-              const double v = scale * acc[r][c][e];
-              drow[cc] = accumulate ? drow[cc] + v : v;
+      for (int r = 0; r < WTM; ++r) {
+        const int row = i0 + wm * (WTM * 8) + r * 8 + g;
+        if (row >= D.rows) continue;
+        double* drow = D.p + (long long)row * D.ld;
+#pragma unroll
+        for (int c = 0; c < WTN; ++c) {
+          const int col = j0 + wn * (WTN * 8) + c * 8 + q * 2;
+          if (col + 1 < D.cols && (!syrk || col + 1 <= row) &&
+              ((reinterpret_cast<uintptr_t>(drow + col) & 15) == 0)) {
+            double2* p2 = reinterpret_cast<double2*>(drow + col);
+            double2 v = make_double2(scale * acc[r][c][0], scale * acc[r][c][1]);
+            if (accumulate) {
+              const double2 o = __ldcg(p2);  // L2: another SM may have written it this launch
+              v.x += o.x;
+              v.y += o.y;
+            }
+            __stcg(p2, v);
+          } else {
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+              const int cc = col + e;
+              if (cc < D.cols && (!syrk || cc <= row)) {
+                const double v = scale * acc[r][c][e];
+                __stcg(drow + cc, accumulate ? __ldcg(drow + cc) + v : v);
+              }
             }
           }
         }
       }
+      if (sem != nullptr) {
+        __threadfence();
+        named_sync(2, CONSUMERS * 32);
+        if (ctid == 0) st_release(sem, turn + 1);
+      }
     }
   }
+}
+
+static int num_sms() {
+  static int n = 0;
+  if (n == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+    if (n <= 0) n = 148;
+  }
+  return n;
 }
 
 template <int NS, int NT>
@@ -322,18 +433,61 @@ static cudaError_t launch_ws(BatchArgs<double> a, cudaStream_t s) {
   if (total <= 0) return cudaSuccess;
   if (total > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
   a.total_tiles = (int)total;
+  // turn counters: regions were numbered by the executor (DDest.sem = region id + 1, 0 = none)
+  int n_sync = 1;
+  {
+    int region_base[kMaxBatch * 4];
+    int region_ld[kMaxBatch * 4];
+    int region_rows[kMaxBatch * 4];
+    int region_seen[kMaxBatch * 4];
+    for (int r = 0; r < kMaxBatch * 4; ++r) region_base[r] = -1, region_ld[r] = 0, region_rows[r] = 0, region_seen[r] = 0;
+    for (int i = 0; i < a.count; ++i)
+      for (int d = 0; d < a.p[i].nd; ++d) {
+        const int rg = a.p[i].d[d].sem;
+        if (rg <= 0 || rg > kMaxBatch * 4) continue;
+        region_ld[rg - 1] = max(region_ld[rg - 1], a.p[i].tk);
+        region_rows[rg - 1] = max(region_rows[rg - 1], a.p[i].tn);
+      }
+    for (int r = 0; r < kMaxBatch * 4; ++r)
+      if (region_ld[r] > 0) {
+        region_base[r] = n_sync;
+        n_sync += region_ld[r] * region_rows[r];
+      }
+    for (int i = 0; i < a.count; ++i)
+      for (int d = 0; d < a.p[i].nd; ++d) {
+        DDest<double>& D = a.p[i].d[d];
+        const int rg = D.sem;
+        if (rg <= 0 || rg > kMaxBatch * 4) {
+          D.sem = -1;
+          continue;
+        }
+        D.sem = region_base[rg - 1];
+        D.sem_ld = region_ld[rg - 1];
+        D.turn = region_seen[rg - 1]++;
+      }
+  }
+  cudaError_t e = cudaSuccess;
+  a.dynamic = n_sync > 1;
+  if (a.dynamic) {
+    if (a.sync == nullptr || n_sync > a.n_sync) return cudaErrorInvalidValue;
+    e = cudaMemsetAsync(a.sync, 0, (size_t)n_sync * sizeof(int), s);
+    if (e != cudaSuccess) return e;
+  }
   constexpr int STAGE_BYTES = (NS + NT) * BUF * 8;
-  constexpr int STAGES = (SMEM_BUDGET - 1024) / STAGE_BYTES > 8 ? 8 : (SMEM_BUDGET - 1024) / STAGE_BYTES;
+  constexpr int STAGES =
+      (SMEM_BUDGET - 1024) / STAGE_BYTES > 8 ? 8 : (SMEM_BUDGET - 1024) / STAGE_BYTES;
   static_assert(STAGES >= 2, "smem");
-  const size_t smem = (size_t)STAGES * STAGE_BYTES + 2 * STAGES * sizeof(uint64_t);
+  const size_t smem = (size_t)STAGES * STAGE_BYTES + (2 * STAGES + 2 * TSLOTS) * sizeof(uint64_t) +
+                      (TSLOTS + 2) * sizeof(int);
   auto kern = prod_f64_ws_kernel<NS, NT, STAGES>;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
     attr_set = true;
   }
-  kern<<<a.total_tiles, THREADS, smem, s>>>(a);
+  const int grid = (int)(total < num_sms() ? total : num_sms());
+  kern<<<grid, THREADS, smem, s>>>(a);
   return cudaGetLastError();
 }
 

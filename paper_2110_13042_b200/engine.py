@@ -1,9 +1,9 @@
-"""Plan execution: plan cache + one native call per plan (+ optional CUDA graph).
+"""Plan execution: plan cache + one native call per plan.
 
 The executor itself is native (``ata_run_plan`` in csrc/abi.cu); this module
 keeps plans keyed by shape/layout/threshold so repeated calls skip planning,
-and can capture a plan into a ``torch.cuda.CUDAGraph`` for launch-bound
-(reference-faithful, small-leaf) plans.
+and owns the per-device int32 "sync" buffer the persistent kernels use for
+their work counter and destination turn counters.
 """
 from __future__ import annotations
 
@@ -16,6 +16,7 @@ from . import _native as nat
 
 _PLAN_CACHE: "OrderedDict[tuple, object]" = OrderedDict()
 _PLAN_CACHE_MAX = 64
+_SYNC: dict = {}
 
 
 def cached_plan(key, builder):
@@ -30,8 +31,35 @@ def cached_plan(key, builder):
     return p
 
 
+def sync_ints_needed(plan, dtype_code) -> int:
+    need = getattr(plan, "_sync_need", {}).get(dtype_code)
+    if need is None:
+        ops = np.ascontiguousarray(plan.ops)
+        need = int(nat.load().ata_sync_ints_needed(dtype_code, ops.ctypes.data_as(ctypes.c_void_p),
+                                                   len(ops)))
+        try:
+            plan._sync_need = {**getattr(plan, "_sync_need", {}), dtype_code: need}
+        except AttributeError:
+            pass
+    return need
+
+
+def sync_buffer(device, ints: int):
+    """Per-(device, stream) int32 scratch, grown on demand.  Keyed by stream so
+    concurrent plans on different streams never share counters."""
+    import torch
+    stream = torch.cuda.current_stream(device)
+    key = (device.index if device.index is not None else torch.cuda.current_device(),
+           int(stream.cuda_stream))
+    buf = _SYNC.get(key)
+    if buf is None or buf.numel() < ints:
+        buf = torch.zeros(max(ints, 1 << 16), dtype=torch.int32, device=device)
+        _SYNC[key] = buf
+    return buf
+
+
 def run_plan(plan, dtype_code, A, a_elems, C, c_elems, alpha, ws=None, ws_elems=0, B=None,
-             b_elems=0, stream=None):
+             b_elems=0, stream=None, device=None, sync=None):
     """Issue every op of `plan` on `stream` (default: torch's current stream).
     A/B/C/ws are device pointers (ints)."""
     import torch
@@ -41,7 +69,11 @@ def run_plan(plan, dtype_code, A, a_elems, C, c_elems, alpha, ws=None, ws_elems=
     ops = plan.ops
     if not ops.flags.c_contiguous:
         ops = np.ascontiguousarray(ops)
+    if sync is None:
+        dev = device if device is not None else torch.device("cuda", torch.cuda.current_device())
+        sync = sync_buffer(dev, sync_ints_needed(plan, dtype_code))
     rc = lib.ata_run_plan(dtype_code, ops.ctypes.data_as(ctypes.c_void_p), len(ops),
                           A, a_elems, B if B is not None else A, b_elems if B is not None else a_elems,
-                          C, c_elems, ws or 0, ws_elems, float(alpha), stream)
+                          C, c_elems, ws or 0, ws_elems, int(sync.data_ptr()), int(sync.numel()),
+                          float(alpha), stream)
     nat.check(rc)

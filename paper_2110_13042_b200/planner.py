@@ -56,8 +56,8 @@ class Win(NamedTuple):
         return Win(self.base, self.off, self.ld, min(rows, self.rows), min(cols, self.cols))
 
 
-def _ref(w: Win, sign: float = 1.0):
-    return (w.base, w.rows, w.off, w.ld, w.cols, 0, float(sign))
+def _ref(w: Win, sign: float = 1.0, region: int = 0):
+    return (w.base, w.rows, w.off, w.ld, w.cols, int(region), float(sign))
 
 
 @dataclass
@@ -85,15 +85,26 @@ class PlanBuilder:
         if w.base == nat.BASE_WS and w.rows > 0 and w.cols > 0:
             self.ws_hi = max(self.ws_hi, w.off + (w.rows - 1) * w.ld + w.cols)
 
+    def new_group(self) -> int:
+        self._groups = getattr(self, "_groups", 0) + 1
+        return self._groups
+
+    def new_region(self) -> int:
+        self._regions = getattr(self, "_regions", 0) + 1
+        return self._regions
+
     def product(self, kind, m, n, k, S, T, D, accumulate=1, group=-1, count=True):
-        """S, T: [(Win, sign)] operand terms; D: [(Win, sign)] destinations."""
+        """S, T: [(Win, sign)] operand terms; D: [(Win, sign[, region])]
+        destinations (region > 0: window shared with other products of the
+        same group, accumulated in op order)."""
         if len(S) > nat.MAX_TERMS or len(T) > nat.MAX_TERMS or len(D) > nat.MAX_DESTS:
             raise ValueError("too many product terms")
-        for w, _ in list(S) + list(T) + list(D):
+        for w, *_ in list(S) + list(T) + list(D):
             self._touch(w)
         s = [_ref(w.clip(m, n), sg) for w, sg in S] + [_EMPTY] * (nat.MAX_TERMS - len(S))
         t = [_ref(w.clip(m, k), sg) for w, sg in T] + [_EMPTY] * (nat.MAX_TERMS - len(T))
-        d = [_ref(w.clip(n, k), sg) for w, sg in D] + [_EMPTY] * (nat.MAX_DESTS - len(D))
+        d = [_ref(dd[0].clip(n, k), dd[1], dd[2] if len(dd) > 2 else 0) for dd in D] \
+            + [_EMPTY] * (nat.MAX_DESTS - len(D))
         op = nat.OP_SYRK if kind == "syrk" else nat.OP_GEMM
         self.rows.append((op, m, n, k, len(S), len(T), len(D), accumulate, group, 0, s, t, d))
         if group < 0 or group != self._last_group:
@@ -128,9 +139,17 @@ class PlanBuilder:
 
 # ------------------------------------------------------------------ Strassen
 
-def _strassen_products(a: Win, b: Win, c: Win):
+def _strassen_products(a: Win, b: Win, c: Win, regions=None):
     """The seven products of one node (strassen.py:234-275) as
-    (S-shape, S-terms, T-shape, T-terms, dests); shape None = plain view."""
+    (S-shape, S-terms, T-shape, T-terms, dests); shape None = plain view.
+    `regions` = region ids of (C11, C12, C21, C22) when the products are
+    launched together (ordered accumulation into shared quadrants)."""
+    if regions is not None:
+        def tag(blocks):
+            return [(w, sg, regions[q]) for (w, sg, q) in blocks]
+    else:
+        def tag(blocks):
+            return [(w, sg) for (w, sg, q) in blocks]
     m, n = a.rows, a.cols
     k = b.cols
     m1, n1, k1 = m // 2, n // 2, k // 2
@@ -141,21 +160,22 @@ def _strassen_products(a: Win, b: Win, c: Win):
     B21, B22 = b.sub(m1, 0, m2, k1), b.sub(m1, k1, m2, k2)
     C11, C12 = c.sub(0, 0, n1, k1), c.sub(0, k1, n1, k2)
     C21, C22 = c.sub(n1, 0, n2, k1), c.sub(n1, k1, n2, k2)
+    Q11, Q12, Q21, Q22 = 0, 1, 2, 3
     return [
         ((m2, n2), [(A22, 1.0), (A11, 1.0)], (m2, k2), [(B22, 1.0), (B11, 1.0)],
-         [(C11, 1.0), (C22, 1.0)]),
+         tag([(C11, 1.0, Q11), (C22, 1.0, Q22)])),
         ((m1, n2), [(A12, 1.0), (A22.top(m1), 1.0)], None, [(B11, 1.0)],
-         [(C21, 1.0), (C22, -1.0)]),
+         tag([(C21, 1.0, Q21), (C22, -1.0, Q22)])),
         (None, [(A11, 1.0)], (m1, k2), [(B12, 1.0), (B22.top(m1), -1.0)],
-         [(C12, 1.0), (C22, 1.0)]),
+         tag([(C12, 1.0, Q12), (C22, 1.0, Q22)])),
         (None, [(A22, 1.0)], (m2, k1), [(B21, 1.0), (B11, -1.0)],
-         [(C11, 1.0), (C21, 1.0)]),
+         tag([(C11, 1.0, Q11), (C21, 1.0, Q21)])),
         ((m2, n1), [(A21, 1.0), (A11, 1.0)], None, [(B22, 1.0)],
-         [(C11, -1.0), (C12, 1.0)]),
+         tag([(C11, -1.0, Q11), (C12, 1.0, Q12)])),
         ((m1, n2), [(A12, 1.0), (A11, -1.0)], (m1, k2), [(B12, 1.0), (B11, 1.0)],
-         [(C22, 1.0)]),
+         tag([(C22, 1.0, Q22)])),
         ((m2, n2), [(A21, 1.0), (A22, -1.0)], (m2, k2), [(B22, 1.0), (B21, 1.0)],
-         [(C11, 1.0)]),
+         tag([(C11, 1.0, Q11)])),
     ]
 
 
@@ -175,13 +195,18 @@ class _ReferencePlanner:
             from .errors import WorkspaceUndersizedError
             raise WorkspaceUndersizedError(f"workspace undersized: no level {depth} for ({m},{n},{k})")
         prod_off, lhs_off, rhs_off = self.lv[depth]
-        for s_shape, s_terms, t_shape, t_terms, dests in _strassen_products(a, b, c):
+        # fused leaf products of this node share one launch; their C quadrants
+        # are ordered regions (accumulated in the reference's product order)
+        regions = tuple(self.pb.new_region() for _ in range(4)) if self.fuse else None
+        group = self.pb.new_group()
+        for s_shape, s_terms, t_shape, t_terms, dests in _strassen_products(a, b, c, regions):
             ms, ns = s_shape if s_shape else (s_terms[0][0].rows, s_terms[0][0].cols)
             mt, kt = t_shape if t_shape else (t_terms[0][0].rows, t_terms[0][0].cols)
             assert ms == mt
             if self.fuse and is_base_case(ms, ns, kt, self.t):
-                self.pb.product("gemm", ms, ns, kt, s_terms, t_terms, dests)
+                self.pb.product("gemm", ms, ns, kt, s_terms, t_terms, dests, group=group)
                 continue
+            dests = [(w, sg) for (w, sg, *_) in dests]
             if s_shape:
                 S = Win(nat.BASE_WS, lhs_off, ns, ms, ns)
                 self.pb.combo(S, s_terms)
@@ -273,14 +298,17 @@ def plan_ata_auto(m, n, lda, ldc, params: AutoParams = AutoParams()) -> Plan:
                            [(c, 1.0)], group=group)
             group += 1
         if fused:
-            per_node = [_strassen_products(a, b, c) for (a, b, c) in fused]
+            # all 7 products of every node of this level in one persistent launch;
+            # each node's C quadrants are ordered regions
+            per_node = [_strassen_products(a, b, c, tuple(pb.new_region() for _ in range(4)))
+                        for (a, b, c) in fused]
             for pi in range(7):
                 for prods in per_node:
                     s_shape, s_terms, t_shape, t_terms, dests = prods[pi]
                     ms, ns = s_shape if s_shape else (s_terms[0][0].rows, s_terms[0][0].cols)
                     _, kt = t_shape if t_shape else (t_terms[0][0].rows, t_terms[0][0].cols)
                     pb.product("gemm", ms, ns, kt, s_terms, t_terms, dests, group=group)
-                group += 1
+            group += 1
         nodes = nxt
     for (c0, w) in sorted(nodes):
         pb.product("syrk", m, w, w, [(A.sub(0, c0, m, w), 1.0)], [], [(C.sub(c0, c0, w, w), 1.0)],

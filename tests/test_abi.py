@@ -52,12 +52,12 @@ def test_plan_validation_without_gpu():
     lib = nat.load()
     fake = ctypes.c_void_p(16)  # never dereferenced: validation fails first
     rc = lib.ata_run_plan(0, plan.ops.ctypes.data_as(ctypes.c_void_p), len(plan.ops), fake, 256,
-                          fake, 256, fake, 256, fake, 8, 1.0, None)
+                          fake, 256, fake, 256, fake, 8, None, 0, 1.0, None)
     assert rc == -3
     with pytest.raises(WorkspaceUndersizedError):
         nat.check(rc)
     bad = plan.ops.copy()
     bad[0]["s"][0]["rows"] = 999
     rc = lib.ata_run_plan(0, bad.ctypes.data_as(ctypes.c_void_p), len(bad), fake, 256,
-                          fake, 256, fake, 256, fake, 10**6, 1.0, None)
+                          fake, 256, fake, 256, fake, 10**6, None, 0, 1.0, None)
     assert rc == -1

@@ -127,7 +127,8 @@ def test_auto_plan_semantics(m, n, leaf, smin, seed):
 
 
 def _dest_cells(op, n_ld):
-    cells = set()
+    """(base, element) -> region id of every destination element of an op."""
+    cells = {}
     for j in range(int(op["nd"])):
         d = op["d"][j]
         rows, cols, off, ld = int(d["rows"]), int(d["cols"]), int(d["off"]), int(d["ld"])
@@ -135,7 +136,7 @@ def _dest_cells(op, n_ld):
             for c in range(cols):
                 if int(op["type"]) == 1 and c > r:
                     continue
-                cells.add((int(d["base"]), off + r * ld + c))
+                cells[(int(d["base"]), off + r * ld + c)] = int(d["region"])
     return cells
 
 
@@ -149,8 +150,11 @@ def test_auto_plan_groups_write_disjoint():
         groups.setdefault(g, []).append(op)
     assert groups
     for g, ops in groups.items():
-        seen = set()
+        seen = {}
         for op in ops:
             cells = _dest_cells(op, 150)
-            assert not (cells & seen), f"group {g} has overlapping destinations"
-            seen |= cells
+            for cell, region in cells.items():
+                if cell in seen:
+                    # a shared cell must belong to the same ordered region in both ops
+                    assert region > 0 and seen[cell] == region, f"group {g}: unordered overlap"
+                seen[cell] = region
