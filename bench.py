@@ -53,7 +53,8 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--leaf-cols", type=int, default=None)
-    p.add_argument("--strassen-min", type=int, default=None)
+    p.add_argument("--max-depth", type=int, default=None)
+    p.add_argument("--min-dim", type=int, default=None)
     return p.parse_args()
 
 
@@ -133,12 +134,15 @@ def launch_units(plan):
                 flops += 2 * m * n * k
             elif ot == nat.OP_SYRK:
                 flops += m * n * (n + 1)
+            else:  # elementwise: algorithmic elements moved (each source read once, each output written)
+                flops += sum(int(r["rows"]) * int(r["cols"]) for r in op["s"][:int(op["ns"])])
+                flops += sum(int(r["rows"]) * int(r["cols"]) for r in op["d"][:int(op["nd"])])
         units.append((i, j, t in (nat.OP_GEMM, nat.OP_SYRK), flops))
         i = j
-    # the executor splits groups beyond 64 products into several launches
+    # the executor splits groups beyond 48 products into several launches
     launches = 0
     for (i, j, is_prod, _) in units:
-        launches += -(-(j - i) // 64) if is_prod else 1
+        launches += -(-(j - i) // 48) if is_prod else 1
     return units, launches
 
 
@@ -198,7 +202,7 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=dev)
     import paper_2110_13042_b200 as P
-    from paper_2110_13042_b200 import _native as nat, dist as pdist, engine, planner
+    from paper_2110_13042_b200 import _native as nat, auto_plan, dist as pdist, engine, planner
     from paper_2110_13042_b200.measure import CONFIGS
 
     cfg = CONFIGS[args.config]
@@ -218,12 +222,14 @@ def main():
     A = torch.from_numpy(host).to(dev)
     C = torch.zeros((n, n), dtype=A.dtype, device=dev)
     packed = torch.empty(n * (n + 1) // 2, dtype=A.dtype, device=dev) if world > 1 else None
-    params = planner.AutoParams(**{k: v for k, v in (("leaf_cols", args.leaf_cols),
-                                                      ("strassen_min", args.strassen_min)) if v})
+    params = auto_plan.AutoParams(**{k: v for k, v in (("leaf_cols", args.leaf_cols),
+                                                        ("max_depth", args.max_depth),
+                                                        ("min_dim", args.min_dim)) if v is not None})
     mloc = r1 - r0
     if threshold == "auto":
-        plan = planner.plan_ata_auto(mloc, n, n, n, params)
-        wsbuf = None
+        plan = auto_plan.plan_ata_auto(mloc, n, n, n, params)
+        wsbuf = torch.empty(max(1, plan.ws_scalars), dtype=A.dtype, device=dev) \
+            if plan.ws_scalars else None
     else:
         ws = P.workspace_for_ata(mloc, n, threshold, dtype=np_dt)
         plan = planner.plan_ata_reference(mloc, n, n, n, threshold, ws.level_offsets())
@@ -285,7 +291,7 @@ def main():
     ms_step = total_ms / args.steps
     value = m * n * n / (ms_step * 1e-3) / 1e9
     # ---- roofline of the dominant kernel (fused product kernel) ----
-    prod_ms, prod_flops, ew_ms = 0.0, 0, 0.0
+    prod_ms, prod_flops, ew_ms, ew_elems = 0.0, 0, 0.0, 0
     for s in range(args.steps):
         for u, (i, j, is_prod, fl) in enumerate(units):
             d = ev[s][u][0].elapsed_time(ev[s][u][1])
@@ -294,7 +300,8 @@ def main():
                 prod_flops += fl
             else:
                 ew_ms += d
-    prod_launches = sum(-(-(j - i) // 64) for (i, j, p, _) in units if p) * args.steps
+                ew_elems += fl
+    prod_launches = sum(-(-(j - i) // 48) for (i, j, p, _) in units if p) * args.steps
     achieved = prod_flops / (prod_ms * 1e-3) / 1e12 if prod_ms > 0 else 0.0
     peak = FP64_PEAK_TFLOPS if f64 else TF32_PEAK_TFLOPS
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
@@ -307,6 +314,16 @@ def main():
                 "executed_flops_per_step": prod_flops // args.steps,
                 "algorithmic_flops_per_step": m * n * n,
                 "avg_launch_ms": prod_ms / max(1, prod_launches)}
+    hbm_peak = 6549.4
+    try:
+        hbm_peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except Exception:
+        pass
+    ew_gbs = ew_elems * A.element_size() / (ew_ms * 1e-3) / 1e9 if ew_ms > 0 else None
+    roofline["secondary"] = {"kernel": "combo4_kernel (Strassen operand sums)", "bound": "hbm",
+                             "achieved": ew_gbs, "peak": hbm_peak, "unit": "GB/s",
+                             "frac": ew_gbs / hbm_peak if ew_gbs else None,
+                             "share_of_step": ew_ms / total_ms if total_ms else None}
     line = {"metric": "AtA effective GFLOP/s (m*n^2/time)", "value": value, "unit": "GFLOP/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,

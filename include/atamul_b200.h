@@ -52,8 +52,16 @@ extern "C" {
 #define ATA_BASE_WS 2 /* the caller's HBM workspace */
 #define ATA_BASE_B 3  /* the second operand B (fast_strassen) */
 
-#define ATA_MAX_TERMS 2
-#define ATA_MAX_DESTS 4
+/* GEMM/SYRK use s[0..1], t[0..1] (two zero-extended terms per operand) and up to
+ * 8 destinations (post-additions of up to three fused Strassen levels).
+ * ATA_OP_COMBO4 reads up to 4 sources s[0..3] (the quadrants of one operand) and
+ * writes up to 8 sums d[j] = sum_q c_jq * zero-extended s[q], truncated to d[j]'s
+ * extent; c_jq is packed in d[j].region as base-4 digits (digit q: 0 -> 0,
+ * 1 -> +1, 2 -> -1).  One pass over the quadrants produces all of a Strassen
+ * node's operand sums (strassen.py:234-273). */
+#define ATA_OP_COMBO4 5
+#define ATA_MAX_TERMS 4
+#define ATA_MAX_DESTS 8
 
 /* A rectangular window of one base buffer: element (r, c) lives at
  * base + off + r*ld + c.  Reads outside [rows) x [cols) are zero

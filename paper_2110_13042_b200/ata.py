@@ -7,7 +7,7 @@ triangle of C is never read or written by any kernel (ata.py:121-123).
 ``threshold`` keeps the reference's element-count meaning (ata.py:23-26,
 strassen.py:38-41) and then reproduces the reference recursion exactly (same
 leaves, same exact multiplication count).  ``threshold="auto"`` selects the
-GPU plan (planner.plan_ata_auto).  Inputs are torch CUDA tensors (zero copy)
+GPU plan (auto_plan.plan_ata_auto).  Inputs are torch CUDA tensors (zero copy)
 or anything the reference accepts (staged through the device).
 """
 from __future__ import annotations
@@ -15,7 +15,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import _native as nat
-from . import engine, planner
+from . import auto_plan, engine, planner
 from .errors import ShapeMismatchError, UnsupportedSizeError
 from .matrix import (DenseMatrix, DeviceOperand, MultCounter, as_array, mirror_lower_to_upper)
 from .workspace import (DEFAULT_THRESHOLD, StrassenWorkspace, ata_calls, check_ata_workspace,
@@ -36,9 +36,9 @@ def workspace_for_ata(m: int, n: int, threshold=DEFAULT_THRESHOLD, dtype=np.floa
 
 def _plan_for(m, n, lda, ldc, threshold, ws, auto_params=None):
     if threshold == AUTO:
-        params = auto_params or planner.AutoParams()
+        params = auto_params or auto_plan.AutoParams()
         key = ("ata-auto", m, n, lda, ldc, params)
-        return engine.cached_plan(key, lambda: planner.plan_ata_auto(m, n, lda, ldc, params))
+        return engine.cached_plan(key, lambda: auto_plan.plan_ata_auto(m, n, lda, ldc, params))
     offs = tuple(ws.level_offsets())
     key = ("ata-ref", m, n, lda, ldc, int(threshold), offs)
     return engine.cached_plan(
@@ -66,7 +66,8 @@ def ata(A, C, alpha=1.0, threshold=DEFAULT_THRESHOLD, ws: StrassenWorkspace | No
     elif threshold != AUTO:
         check_ata_workspace(ws, m, n, threshold)
     plan = _plan_for(m, n, A_.ld, C_.ld, threshold, ws, auto_params)
-    wbuf = ws.ensure(C_.t.device) if plan.ws_scalars > 0 else None
+    wbuf = ws.ensure(C_.t.device, extra=plan.ws_scalars if threshold == AUTO else 0) \
+        if plan.ws_scalars > 0 else None
     engine.run_plan(plan, nat.dtype_code(C_.t.dtype, precision), A_.ptr, A_.elems, C_.ptr, C_.elems, alpha,
                     ws=int(wbuf.data_ptr()) if wbuf is not None else 0,
                     ws_elems=int(wbuf.numel()) if wbuf is not None else 0)

@@ -112,6 +112,8 @@ int validate_op(const ata_op& op, const Bases& b, int i) {
       if (op.m < 1 || op.n < 1 || op.k < 1 || op.ns < 1 || op.nd < 1 ||
           (op.type == ATA_OP_GEMM && op.nt < 1))
         return fail(ATA_E_SHAPE, "shape mismatch: empty product in op " + std::to_string(i));
+      if (op.ns > 2 || op.nt > 2)
+        return fail(ATA_E_ARG, "products take at most two terms per operand (op " + std::to_string(i) + ")");
       if (op.s[0].sign != 1.0 || (op.type == ATA_OP_GEMM && op.t[0].sign != 1.0))
         return fail(ATA_E_ARG, "leading operand term must have sign +1 (op " + std::to_string(i) + ")");
       for (int j = 0; j < op.ns; ++j)
@@ -141,6 +143,16 @@ int validate_op(const ata_op& op, const Bases& b, int i) {
       return ATA_OK;
     case ATA_OP_FILL:
       if (op.nd != 1) return fail(ATA_E_ARG, "fill needs 1 dest");
+      return ATA_OK;
+    case ATA_OP_COMBO4:
+      if (op.ns < 1 || op.nd < 1) return fail(ATA_E_ARG, "combo4 needs sources and dests");
+      for (int j = 0; j < op.nd; ++j) {
+        int code = op.d[j].region;
+        if (code < 0 || code >= (1 << (2 * op.ns)))
+          return fail(ATA_E_ARG, "combo4: bad coefficient code in op " + std::to_string(i));
+        for (int q = 0; q < op.ns; ++q, code >>= 2)
+          if ((code & 3) == 3) return fail(ATA_E_ARG, "combo4: bad coefficient digit");
+      }
       return ATA_OK;
     default:
       return fail(ATA_E_ARG, "unknown op type " + std::to_string(op.type));
@@ -297,6 +309,19 @@ int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, int* sync, int64_t 
     } else if (op.type == ATA_OP_FILL) {
       ata::DDest<T> d = dest_of<T>(op.d[0], b);
       e = ata::launch_fill<T>(d.p, d.ld, d.rows, d.cols, s);
+    } else if (op.type == ATA_OP_COMBO4) {
+      ata::EwArgs<T> a;
+      std::memset(&a, 0, sizeof(a));
+      a.nsrc = op.ns;
+      a.ndst = op.nd;
+      for (int j = 0; j < op.ns; ++j) a.src[j] = term_of<T>(op.s[j], b);
+      for (int j = 0; j < op.nd; ++j) {
+        a.dst[j] = dest_of<T>(op.d[j], b);
+        a.dst[j].coef = op.d[j].region;
+        a.rows = a.rows > op.d[j].rows ? a.rows : op.d[j].rows;
+        a.cols = a.cols > op.d[j].cols ? a.cols : op.d[j].cols;
+      }
+      e = ata::launch_combo4<T>(a, s);
     }
     if (e != cudaSuccess) return cuda_fail(e, "elementwise launch");
     return ATA_OK;

@@ -5,7 +5,8 @@
 
 namespace ata {
 
-constexpr int kMaxBatch = 64;  // products per grouped launch (kernel-param by value, < 32 KB)
+constexpr int kMaxBatch = 48;  // products per grouped launch (kernel-param by value, < 32 KB)
+constexpr int kMaxDests = 8;  // destinations per product (ATA_MAX_DESTS)
 
 template <typename T>
 struct DTerm {  // zero-extended read window
@@ -24,7 +25,7 @@ struct DDest {  // truncated write window
   int sem;     // >= 0: base of this region's per-tile turn counters (ordered accumulation)
   int sem_ld;  // tile columns of the region (counter row pitch)
   int turn;    // this product's position in the region's accumulation order
-  int _pad;
+  int coef;    // COMBO4 outputs: base-4 coefficient code over the sources
 };
 
 enum : int { kGemm = 0, kSyrk = 1 };
@@ -39,7 +40,7 @@ struct DProd {
   int tile_begin;  // prefix offset of this product in the launch's tile space
   int _pad;
   DTerm<T> s[2], t[2];
-  DDest<T> d[4];
+  DDest<T> d[kMaxDests];
 };
 
 template <typename T>
@@ -56,8 +57,8 @@ struct BatchArgs {
 template <typename T>
 struct EwArgs {  // elementwise op: rows x cols iteration space
   int rows, cols, nsrc, ndst;
-  DTerm<T> src[2];
-  DDest<T> dst[4];
+  DTerm<T> src[4];
+  DDest<T> dst[kMaxDests];
 };
 
 // ---- host launchers (defined in gemm_*.cu / elementwise.cu) ----
@@ -67,6 +68,7 @@ bool f64_supports_ordering();
 cudaError_t launch_batch_f32(const BatchArgs<float>& a, cudaStream_t s, bool split);
 template <typename T> cudaError_t launch_combo(const EwArgs<T>& a, cudaStream_t s);
 template <typename T> cudaError_t launch_update(const EwArgs<T>& a, cudaStream_t s);
+template <typename T> cudaError_t launch_combo4(const EwArgs<T>& a, cudaStream_t s);
 template <typename T> cudaError_t launch_fill(T* p, long long ld, int rows, int cols, cudaStream_t s);
 template <typename T> cudaError_t launch_mirror(T* C, long long ldc, int n, cudaStream_t s);
 template <typename T> cudaError_t launch_pack(const T* C, long long ldc, int n, T* packed, cudaStream_t s);

@@ -46,6 +46,48 @@ __global__ void combo_kernel(const __grid_constant__ EwArgs<T> a) {
   }
 }
 
+// combo4: one pass over up to 4 source quadrants produces up to 8 operand sums
+// dst_j[r,c] = sum_q c_jq * src_q[r,c] (zero outside src_q, truncated to dst_j).
+// Sources are read once per element position with read-only/streaming loads;
+// each thread handles two adjacent columns (16-byte accesses when aligned).
+template <typename T>
+__global__ void combo4_kernel(const __grid_constant__ EwArgs<T> a) {
+  const int c0 = (blockIdx.x * blockDim.x + threadIdx.x) * 2;
+  if (c0 >= a.cols) return;
+  for (int r = blockIdx.y * blockDim.y + threadIdx.y; r < a.rows; r += gridDim.y * blockDim.y) {
+    T v[4][2];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      v[q][0] = v[q][1] = T(0);
+      if (q < a.nsrc) {
+        const DTerm<T>& S = a.src[q];
+        if (r < S.rows) {
+          const T* p = S.p + (long long)r * S.ld + c0;
+          if (c0 < S.cols) v[q][0] = __ldcs(p);
+          if (c0 + 1 < S.cols) v[q][1] = __ldcs(p + 1);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < kMaxDests; ++j) {
+      if (j >= a.ndst) break;
+      const DDest<T>& D = a.dst[j];
+      if (r >= D.rows) continue;
+      T o0 = T(0), o1 = T(0);
+      int code = D.coef;
+#pragma unroll
+      for (int q = 0; q < 4; ++q, code >>= 2) {
+        const int cq = code & 3;
+        if (cq == 1) o0 += v[q][0], o1 += v[q][1];
+        else if (cq == 2) o0 -= v[q][0], o1 -= v[q][1];
+      }
+      T* p = D.p + (long long)r * D.ld + c0;
+      if (c0 < D.cols) __stcs(p, o0);
+      if (c0 + 1 < D.cols) __stcs(p + 1, o1);
+    }
+  }
+}
+
 // update: for each dest d, D_d[r,c] += sign_d * P[r,c] (r < D_d.rows, c < D_d.cols)
 template <typename T>
 __global__ void update_kernel(const __grid_constant__ EwArgs<T> a) {
@@ -55,7 +97,7 @@ __global__ void update_kernel(const __grid_constant__ EwArgs<T> a) {
   for (int r = blockIdx.y * blockDim.y + threadIdx.y; r < a.rows; r += gridDim.y * blockDim.y) {
     const T v = S.p[(long long)r * S.ld + c];
 #pragma unroll
-    for (int d = 0; d < 4; ++d) {
+    for (int d = 0; d < kMaxDests; ++d) {
       if (d < a.ndst) {
         const DDest<T>& D = a.dst[d];
         if (r < D.rows && c < D.cols) {
@@ -140,6 +182,15 @@ cudaError_t launch_combo(const EwArgs<T>& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 template <typename T>
+cudaError_t launch_combo4(const EwArgs<T>& a, cudaStream_t s) {
+  if (a.rows <= 0 || a.cols <= 0) return cudaSuccess;
+  dim3 blk(kEwThreadsX, kEwThreadsY);
+  const int gx = (a.cols + 2 * kEwThreadsX - 1) / (2 * kEwThreadsX);
+  dim3 grd(gx, ew_grid_y(a.rows, gx));
+  combo4_kernel<T><<<grd, blk, 0, s>>>(a);
+  return cudaGetLastError();
+}
+template <typename T>
 cudaError_t launch_update(const EwArgs<T>& a, cudaStream_t s) {
   if (a.rows <= 0 || a.cols <= 0) return cudaSuccess;
   dim3 blk(kEwThreadsX, kEwThreadsY);
@@ -187,6 +238,7 @@ cudaError_t launch_unpack(const T* packed, int n, T* C, long long ldc, int acc, 
 
 #define ATA_INST(T)                                                                       \
   template cudaError_t launch_combo<T>(const EwArgs<T>&, cudaStream_t);                   \
+  template cudaError_t launch_combo4<T>(const EwArgs<T>&, cudaStream_t);                  \
   template cudaError_t launch_update<T>(const EwArgs<T>&, cudaStream_t);                  \
   template cudaError_t launch_fill<T>(T*, long long, int, int, cudaStream_t);             \
   template cudaError_t launch_mirror<T>(T*, long long, int, cudaStream_t);                \

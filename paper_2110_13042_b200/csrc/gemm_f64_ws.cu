@@ -436,19 +436,19 @@ static cudaError_t launch_ws(BatchArgs<double> a, cudaStream_t s) {
   // turn counters: regions were numbered by the executor (DDest.sem = region id + 1, 0 = none)
   int n_sync = 1;
   {
-    int region_base[kMaxBatch * 4];
-    int region_ld[kMaxBatch * 4];
-    int region_rows[kMaxBatch * 4];
-    int region_seen[kMaxBatch * 4];
-    for (int r = 0; r < kMaxBatch * 4; ++r) region_base[r] = -1, region_ld[r] = 0, region_rows[r] = 0, region_seen[r] = 0;
+    int region_base[kMaxBatch * kMaxDests];
+    int region_ld[kMaxBatch * kMaxDests];
+    int region_rows[kMaxBatch * kMaxDests];
+    int region_seen[kMaxBatch * kMaxDests];
+    for (int r = 0; r < kMaxBatch * kMaxDests; ++r) region_base[r] = -1, region_ld[r] = 0, region_rows[r] = 0, region_seen[r] = 0;
     for (int i = 0; i < a.count; ++i)
       for (int d = 0; d < a.p[i].nd; ++d) {
         const int rg = a.p[i].d[d].sem;
-        if (rg <= 0 || rg > kMaxBatch * 4) continue;
+        if (rg <= 0 || rg > kMaxBatch * kMaxDests) continue;
         region_ld[rg - 1] = max(region_ld[rg - 1], a.p[i].tk);
         region_rows[rg - 1] = max(region_rows[rg - 1], a.p[i].tn);
       }
-    for (int r = 0; r < kMaxBatch * 4; ++r)
+    for (int r = 0; r < kMaxBatch * kMaxDests; ++r)
       if (region_ld[r] > 0) {
         region_base[r] = n_sync;
         n_sync += region_ld[r] * region_rows[r];
@@ -457,7 +457,7 @@ static cudaError_t launch_ws(BatchArgs<double> a, cudaStream_t s) {
       for (int d = 0; d < a.p[i].nd; ++d) {
         DDest<double>& D = a.p[i].d[d];
         const int rg = D.sem;
-        if (rg <= 0 || rg > kMaxBatch * 4) {
+        if (rg <= 0 || rg > kMaxBatch * kMaxDests) {
           D.sem = -1;
           continue;
         }

@@ -97,7 +97,7 @@ class PlanBuilder:
         """S, T: [(Win, sign)] operand terms; D: [(Win, sign[, region])]
         destinations (region > 0: window shared with other products of the
         same group, accumulated in op order)."""
-        if len(S) > nat.MAX_TERMS or len(T) > nat.MAX_TERMS or len(D) > nat.MAX_DESTS:
+        if len(S) > nat.PROD_MAX_TERMS or len(T) > nat.PROD_MAX_TERMS or len(D) > nat.MAX_DESTS:
             raise ValueError("too many product terms")
         for w, *_ in list(S) + list(T) + list(D):
             self._touch(w)
@@ -131,6 +131,26 @@ class PlanBuilder:
 
     def fill(self, dst: Win):
         self._ew(nat.OP_FILL, [], [(dst, 1.0)])
+
+    def combo4(self, sources, outputs):
+        """One pass over up to 4 source windows writing up to 8 sums:
+        outputs = [(dst Win, (c_0, .., c_{ns-1}))] with c_q in {0, +1, -1}."""
+        if len(sources) > nat.MAX_TERMS or len(outputs) > nat.MAX_DESTS:
+            raise ValueError("combo4: too many sources/outputs")
+        for w in list(sources) + [o[0] for o in outputs]:
+            self._touch(w)
+        s = [_ref(w) for w in sources] + [_EMPTY] * (nat.MAX_TERMS - len(sources))
+        d = []
+        for w, coefs in outputs:
+            code = 0
+            for q, cq in enumerate(coefs):
+                code |= (1 if cq > 0 else 2 if cq < 0 else 0) << (2 * q)
+            d.append(_ref(w, 1.0, code))
+        d += [_EMPTY] * (nat.MAX_DESTS - len(outputs))
+        self.rows.append((nat.OP_COMBO4, 0, 0, 0, len(sources), 0, len(outputs), 0, -1, 0, s,
+                          [_EMPTY] * nat.MAX_TERMS, d))
+        self.launches += 1
+        self._last_group = None
 
     def finish(self) -> Plan:
         ops = np.array(self.rows, dtype=nat.OP_DTYPE) if self.rows else np.zeros(0, nat.OP_DTYPE)
@@ -259,12 +279,12 @@ TILE = 128
 
 
 @dataclass(frozen=True)
-class AutoParams:
+class AutoParamsV1:
     leaf_cols: int = 1024        # stop the column recursion at this width
     strassen_min: int = 1024     # use a fused Strassen level when both C21 sides >= this
 
 
-def plan_ata_auto(m, n, lda, ldc, params: AutoParams = AutoParams()) -> Plan:
+def plan_ata_auto_v1(m, n, lda, ldc, params: AutoParamsV1 = AutoParamsV1()) -> Plan:
     """GPU plan for lower(C) += alpha A^T A (see module docstring)."""
     if m < 1 or n < 1:
         raise ShapeMismatchError("shape mismatch: empty operand")

@@ -6,7 +6,7 @@ without a GPU.  Never used by the product path.
 """
 import numpy as np
 
-OP_GEMM, OP_SYRK, OP_COMBO, OP_UPDATE, OP_FILL = 0, 1, 2, 3, 4
+OP_GEMM, OP_SYRK, OP_COMBO, OP_UPDATE, OP_FILL, OP_COMBO4 = 0, 1, 2, 3, 4, 5
 
 
 def _win(bases, r, write=False):
@@ -67,6 +67,19 @@ def run(ops, A, C, alpha=1.0, WS=None, B=None):
                 w += float(op["d"][j]["sign"]) * src[:w.shape[0], :w.shape[1]]
         elif t == OP_FILL:
             _win(bases, op["d"][0], write=True)[...] = 0
+        elif t == OP_COMBO4:
+            srcs = [_win(bases, op["s"][q]) for q in range(int(op["ns"]))]
+            for j in range(int(op["nd"])):
+                d = _win(bases, op["d"][j], write=True)
+                code = int(op["d"][j]["region"])
+                acc = np.zeros(d.shape, dtype=dtype)
+                for q, w in enumerate(srcs):
+                    cq = (code >> (2 * q)) & 3
+                    if cq == 0 or w is None:
+                        continue
+                    r, c = min(w.shape[0], d.shape[0]), min(w.shape[1], d.shape[1])
+                    acc[:r, :c] += (1.0 if cq == 1 else -1.0) * w[:r, :c]
+                d[...] = acc
         else:
             raise ValueError(t)
     return C

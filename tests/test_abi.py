@@ -33,7 +33,7 @@ def test_library_builds_and_exports_header_symbols():
 
 def test_abi_struct_layout_and_errors():
     lib = nat.load()
-    assert lib.ata_abi_op_size() == nat.OP_DTYPE.itemsize == 360
+    assert lib.ata_abi_op_size() == nat.OP_DTYPE.itemsize == 680
     assert lib.ata_version() >= 100
     assert lib.ata_strerror(-3) == b"workspace undersized"
 

@@ -64,10 +64,10 @@ def test_reference_plan_vs_oracle(shape, t, rng):
 def test_auto_plan_vs_oracle(shape, rng):
     torch = pytest.importorskip("torch")
     import paper_2110_13042_b200 as P
-    from paper_2110_13042_b200.planner import AutoParams
+    from paper_2110_13042_b200.auto_plan import AutoParams
     a = rng.standard_normal(shape)
     n = shape[1]
-    for params in (AutoParams(), AutoParams(leaf_cols=256, strassen_min=256)):
+    for params in (AutoParams(), AutoParams(leaf_cols=256, min_dim=128, hbm_gbs=1e9)):
         A = torch.from_numpy(a).cuda()
         C = torch.triu(torch.full((n, n), 7.0, dtype=torch.float64, device="cuda"), 1)
         P.ata(A, C, 1.0, threshold="auto", auto_params=params)

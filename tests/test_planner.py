@@ -8,7 +8,7 @@ from hypothesis import strategies as st
 
 import plan_interp
 from oracle import atamul_oracle as O
-from paper_2110_13042_b200 import planner
+from paper_2110_13042_b200 import auto_plan, planner
 from paper_2110_13042_b200.workspace import ata_calls, calls_sizes, workspace_for_calls
 from paper_2110_13042_b200.strassen import workspace_for
 from paper_2110_13042_b200.ata import workspace_for_ata
@@ -114,14 +114,15 @@ def test_fused_plan_has_fewer_ops():
 
 
 @given(m=st.integers(1, 300), n=st.integers(1, 300), leaf=st.sampled_from([8, 16, 33, 64]),
-       smin=st.sampled_from([4, 16, 10**9]), seed=st.integers(0, 2**16))
-def test_auto_plan_semantics(m, n, leaf, smin, seed):
+       mind=st.sampled_from([2, 4, 16, 10**9]), depth=st.sampled_from([1, 2, 3]),
+       seed=st.integers(0, 2**16))
+def test_auto_plan_semantics(m, n, leaf, mind, depth, seed):
     a = np.random.default_rng(seed).uniform(-1, 1, (m, n))
-    params = planner.AutoParams(leaf_cols=leaf, strassen_min=smin)
-    p = planner.plan_ata_auto(m, n, n, n, params)
+    params = auto_plan.AutoParams(leaf_cols=leaf, min_dim=mind, max_depth=depth, hbm_gbs=1e9)
+    p = auto_plan.plan_ata_auto(m, n, n, n, params)
     c = np.zeros((n, n))
     c[np.triu_indices(n, 1)] = 7.0
-    plan_interp.run(p.ops, a, c, 1.0)
+    plan_interp.run(p.ops, a, c, 1.0, WS=np.zeros(max(1, p.ws_scalars)))
     assert np.all(c[np.triu_indices(n, 1)] == 7.0)
     assert O.rel_frobenius_lower(c, O.gram(a)) <= 1e-12
 
@@ -141,7 +142,8 @@ def _dest_cells(op, n_ld):
 
 
 def test_auto_plan_groups_write_disjoint():
-    p = planner.plan_ata_auto(200, 150, 150, 150, planner.AutoParams(leaf_cols=16, strassen_min=8))
+    p = auto_plan.plan_ata_auto(200, 150, 150, 150,
+                                auto_plan.AutoParams(leaf_cols=16, min_dim=4, hbm_gbs=1e9))
     groups = {}
     for op in p.ops:
         g = int(op["group"])

@@ -10,7 +10,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch  # noqa: E402
 
 import paper_2110_13042_b200 as P  # noqa: E402
-from paper_2110_13042_b200 import planner, engine, _native as nat  # noqa: E402
+from paper_2110_13042_b200 import auto_plan, planner, engine, _native as nat  # noqa: E402
 
 
 def timed(fn, reps, flops, name):
@@ -43,15 +43,18 @@ def main():
         # one Strassen level of C21 += A_r^T A_l, all 7 fused products
         N = n
         C = torch.zeros(N, N, dtype=dt, device="cuda")
-        plan = planner.plan_ata_auto(m, N, N, N, planner.AutoParams(leaf_cols=N // 2, strassen_min=1))
-        prods = plan.ops[[int(o["type"]) == nat.OP_GEMM for o in plan.ops]]
+        plan = auto_plan.plan_ata_auto(m, N, N, N, auto_plan.AutoParams(leaf_cols=N // 2, max_depth=1, min_dim=1, hbm_gbs=1e9))
+        keep = [int(o["type"]) != nat.OP_SYRK for o in plan.ops]
 
         class SP:
-            ops = prods
-        fl = sum(2.0 * int(o["m"]) * int(o["n"]) * int(o["k"]) for o in prods)
+            ops = plan.ops[keep]
+        fl = sum(2.0 * int(o["m"]) * int(o["n"]) * int(o["k"]) for o in SP.ops
+                 if int(o["type"]) == nat.OP_GEMM)
+        ws = torch.empty(max(1, plan.ws_scalars), dtype=dt, device="cuda")
         timed(lambda: engine.run_plan(SP, nat.ATA_F64, int(A.data_ptr()), A.numel(),
-                                      int(C.data_ptr()), C.numel(), 1.0), reps, fl,
-              f"fused strassen level m={m} n={N} (7 products)")
+                                      int(C.data_ptr()), C.numel(), 1.0, ws=int(ws.data_ptr()),
+                                      ws_elems=ws.numel()), reps, fl,
+              f"strassen level m={m} n={N} (2 combo4 + 7 products), executed-flop rate")
 
 
 if __name__ == "__main__":
