@@ -55,6 +55,7 @@ def parse():
     p.add_argument("--leaf-cols", type=int, default=None)
     p.add_argument("--max-depth", type=int, default=None)
     p.add_argument("--min-dim", type=int, default=None)
+    p.add_argument("--dump-units", default=None, help="write per-launch timings (JSON) here")
     return p.parse_args()
 
 
@@ -320,6 +321,17 @@ def main():
     except Exception:
         pass
     ew_gbs = ew_elems * A.element_size() / (ew_ms * 1e-3) / 1e9 if ew_ms > 0 else None
+    if args.dump_units and rank == 0:
+        rows = []
+        for u, (i, j, is_prod, fl) in enumerate(units):
+            ms = statistics.median(ev[s][u][0].elapsed_time(ev[s][u][1]) for s in range(args.steps))
+            ops_u = plan.ops[i:j]
+            tiles = sum(((int(o["n"]) + 127) // 128) * ((int(o["k"]) + 127) // 128) for o in ops_u) \
+                if is_prod else 0
+            rows.append({"unit": u, "type": int(ops_u[0]["type"]), "ops": j - i, "tiles": tiles,
+                         "m": int(ops_u[0]["m"]), "n": int(ops_u[0]["n"]), "k": int(ops_u[0]["k"]),
+                         "ms": ms, "rate": fl / (ms * 1e-3) / (1e12 if is_prod else 1e9 / A.element_size())})
+        json.dump(rows, open(args.dump_units, "w"), indent=0)
     roofline["secondary"] = {"kernel": "combo4_kernel (Strassen operand sums)", "bound": "hbm",
                              "achieved": ew_gbs, "peak": hbm_peak, "unit": "GB/s",
                              "frac": ew_gbs / hbm_peak if ew_gbs else None,

@@ -65,6 +65,7 @@ class AutoParams:
     dmma_tflops: float = 33.5      # measured product-kernel rate (profiles/)
     hbm_gbs: float = 5500.0        # achieved combo-kernel bandwidth (profiles/)
     gain: float = 1.5              # split only when saved time > gain * added time
+    ws_budget_gb: float = 40.0     # breadth-first operand sums of one AtA level up to this size
 
 
 def _ceil2(d: int) -> int:
@@ -166,6 +167,13 @@ class _AutoPlanner:
                 continue  # an all-zero operand contributes nothing
             self.pb.product("gemm", m, n, k, S, T, D, group=group)
 
+    def _dry_ws(self, a: Win, b: Win) -> int:
+        """Workspace a breadth-first plan of this block's Strassen tree needs."""
+        probe = _AutoPlanner(self.p)
+        probe.strassen(a, b, a.rows, a.cols, b.cols, [(Win(nat.BASE_C, 0, b.cols, a.cols, b.cols), 1.0)],
+                       self.p.max_depth, [])
+        return probe.ws_peak
+
     def atb(self, a: Win, b: Win, c: Win):
         """c += a^T b for one C21 block (a, b: m x n2 / m x n1 windows of A).
         Depth-first over the top node's 7 products: only one subtree's sums are
@@ -187,17 +195,51 @@ class _AutoPlanner:
     def ata(self, m: int, n: int, lda: int, ldc: int):
         A = Win(nat.BASE_A, 0, lda, m, n)
         C = Win(nat.BASE_C, 0, ldc, n, n)
-        nodes = [(0, n)]
+        level = [(0, n)]
         leaves = []
-        while nodes:
-            c0, w = nodes.pop(0)
-            if w <= self.p.leaf_cols or w < 2:
-                leaves.append((c0, w))
-                continue
-            n1 = w // 2
-            n2 = w - n1
-            self.atb(A.sub(0, c0 + n1, m, n2), A.sub(0, c0, m, n1), C.sub(c0 + n1, c0, n2, n1))
-            nodes += [(c0, n1), (c0 + n1, n2)]
+        budget = int(self.p.ws_budget_gb * 1e9 / 8)
+        while level:
+            blocks, nxt = [], []
+            for (c0, w) in level:
+                if w <= self.p.leaf_cols or w < 2:
+                    leaves.append((c0, w))
+                    continue
+                n1 = w // 2
+                n2 = w - n1
+                blocks.append((A.sub(0, c0 + n1, m, n2), A.sub(0, c0, m, n1),
+                               C.sub(c0 + n1, c0, n2, n1)))
+                nxt += [(c0, n1), (c0 + n1, n2)]
+            if blocks:
+                # the C21 blocks of one AtA level are disjoint: plan them breadth-first
+                # into ONE leaf group when their operand sums fit the workspace budget
+                need = sum(self._dry_ws(a, b) for (a, b, _) in blocks)
+                if need <= budget:
+                    lv_leaves = []
+                    for (a, b, c) in blocks:
+                        self.strassen(a, b, a.rows, a.cols, b.cols, [(c, 1.0)], self.p.max_depth,
+                                      lv_leaves)
+                    self.emit_leaves(lv_leaves)
+                    self.ws_top = 0  # stream order: the next level may reuse the sums
+                else:
+                    # top-child-major: all blocks' top-level sums, then subtree i of
+                    # every block as one leaf group (only one subtree per block alive)
+                    tops = []
+                    for (a, b, c) in blocks:
+                        m_, n_, k_ = a.rows, a.cols, b.cols
+                        if self.worth_split(m_, n_, k_, self.p.max_depth):
+                            tops.append(self.split(a, b, m_, n_, k_, [(c, 1.0)]))
+                        else:
+                            self.emit_leaves([(m_, n_, k_, a, b, [(c, 1.0)])])
+                    mark = self.ws_top
+                    for i in range(7):
+                        lv_leaves = []
+                        for children in tops:
+                            if i < len(children):
+                                self.strassen(*children[i], self.p.max_depth - 1, lv_leaves)
+                        self.emit_leaves(lv_leaves)
+                        self.ws_top = mark
+                    self.ws_top = 0
+            level = nxt
         group = self.pb.new_group()
         for (c0, w) in sorted(leaves):
             self.pb.product("syrk", m, w, w, [(A.sub(0, c0, m, w), 1.0)], [],
