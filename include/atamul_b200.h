@@ -60,6 +60,14 @@ extern "C" {
  * 1 -> +1, 2 -> -1).  One pass over the quadrants produces all of a Strassen
  * node's operand sums (strassen.py:234-273). */
 #define ATA_OP_COMBO4 5
+/* ATA_OP_POSTADD7: Strassen post-addition of one node in one pass
+ * (strassen.py:238-275 restated as the 4-output form): children P1..P7 are
+ * s[0..3], t[0..2] (equal-shape windows, an empty window counts as zero);
+ * outputs d[0..3] = (C11, C12, C21, C22) of the node, truncated:
+ *   C11 (+)= s0*(P1 + P4 - P5 + P7)   C12 (+)= s1*(P3 + P5)
+ *   C21 (+)= s2*(P2 + P4)             C22 (+)= s3*(P1 - P2 + P3 + P6)
+ * with accumulate selecting += (into C) or = (into a parent's product buffer). */
+#define ATA_OP_POSTADD7 6
 #define ATA_MAX_TERMS 4
 #define ATA_MAX_DESTS 8
 

@@ -7,28 +7,31 @@ Shape of the plan (all windows into A, C and one HBM workspace):
    The reference also halves the rows (the contraction) at every level; on
    the GPU the contraction stays whole inside each product's K loop, so the
    two C21 addends of ata.py:114-115 are one product over all m rows.
-2. Every C21 product is a breadth-first Strassen tree (strassen.py:234-275)
-   of depth up to ``max_depth``, chosen per node from a cost model (flops
-   saved at the measured DMMA rate vs. bytes moved by the operand sums at HBM
-   rate):
-     * the operand sums of a node (5 S-sums, 5 T-sums; the other 4 operands
-       are plain quadrant views) are written by ONE multi-output combo kernel
-       per operand (reads each quadrant once) into the workspace;
-     * leaf products read plain windows (1 term per operand) and their
-       post-additions are fused into the epilogue: a depth-d leaf writes its
-       signed contribution straight into up to 2^d C sub-blocks (no product
-       buffers, no update kernels);
-     * leaves of one subtree share launches of the persistent product kernel;
-       C sub-blocks written by several leaves are ordered regions
-       (deterministic accumulation in product order).
-   Quadrant splits are ceil-first (first half = ceil, the second half is the
-   zero-extended one), so every node of a level has identical product shapes
-   and every C sub-block has a single origin shared by all its writers.
+2. Every C21 block is a Strassen tree (strassen.py:234-275) whose depth is
+   chosen per node by a cost model (flops saved at the measured product
+   rate vs. bytes moved by the operand sums and post-additions at the measured
+   HBM rate), evaluated with three HBM-bound one-pass kernels around the
+   tensor-core leaves:
+     * pre-addition: ONE multi-output pass per operand and node (``combo4``:
+       reads the four quadrants once, writes the five operand sums; the other
+       two operands of the seven products are plain quadrant views);
+     * leaves: plain products (one term per operand) writing private product
+       buffers -- no shared destinations, no read-modify-write, one
+       persistent launch per leaf group;
+     * post-addition: ONE pass per node (``postadd7``: reads the seven child
+       products once, writes the node's four output quadrants, accumulating
+       into C at the root).  This replaces the reference's 12 read-modify-
+       write updates per node (strassen.py:238-275) and is executed bottom-up.
+   Quadrant splits are ceil-first (first half = ceil, the trailing half is
+   the zero-extended one), so every node of a level has identical shapes.
 3. Diagonal leaves are SYRK-lower products, one group.
+The Strassen trees of one AtA level are planned breadth-first (one leaf group)
+when their workspace fits ``ws_budget_gb``; otherwise depth-first over each
+block's top-level children (one leaf group per subtree).
 
-Exact arithmetic is the reference's (zero-extended Strassen, classical
-leaves); only the recursion shape differs from an integer-threshold run,
-hence the multiplication count differs (reported as plan.mults).
+Arithmetic is the reference's (zero-extended Strassen, classical leaves); only
+the recursion shape differs from an integer-threshold run, hence the
+multiplication count differs (reported as plan.mults).
 """
 from __future__ import annotations
 
@@ -40,48 +43,46 @@ from .planner import Plan, PlanBuilder, Win
 
 # Strassen in the transposed orientation (strassen.py:234-275) for
 # c = a^T b, quadrants X11 X12 / X21 X22 (rows = contraction):
-#   P1 = (A11+A22)^T (B11+B22) -> +C11 +C22
-#   P2 = (A12+A22)^T  B11      -> +C21 -C22
-#   P3 =  A11^T (B12-B22)      -> +C12 +C22
-#   P4 =  A22^T (B21-B11)      -> +C11 +C21
-#   P5 = (A11+A21)^T  B22      -> -C11 +C12
-#   P6 = (A12-A11)^T (B11+B12) -> +C22
-#   P7 = (A21-A22)^T (B21+B22) -> +C11
+#   P1 = (A11+A22)^T (B11+B22)     P5 = (A11+A21)^T  B22
+#   P2 = (A12+A22)^T  B11          P6 = (A12-A11)^T (B11+B12)
+#   P3 =  A11^T (B12-B22)          P7 = (A21-A22)^T (B21+B22)
+#   P4 =  A22^T (B21-B11)
+#   C11 = P1+P4-P5+P7  C12 = P3+P5  C21 = P2+P4  C22 = P1-P2+P3+P6
 # Operand coefficient vectors over (X11, X12, X21, X22):
 _S = [(1, 0, 0, 1), (0, 1, 0, 1), (1, 0, 0, 0), (0, 0, 0, 1), (1, 0, 1, 0), (-1, 1, 0, 0),
       (0, 0, 1, -1)]
 _T = [(1, 0, 0, 1), (1, 0, 0, 0), (0, 1, 0, -1), (-1, 0, 1, 0), (0, 0, 0, 1), (1, 1, 0, 0),
       (0, 0, 1, 1)]
-# destinations: (quadrant index 0..3 = C11, C12, C21, C22, sign)
-_D = [[(0, 1), (3, 1)], [(2, 1), (3, -1)], [(1, 1), (3, 1)], [(0, 1), (2, 1)],
-      [(0, -1), (1, 1)], [(3, 1)], [(0, 1)]]
 
 
 @dataclass(frozen=True)
 class AutoParams:
     leaf_cols: int = 1024          # SYRK leaf width of the column recursion
-    max_depth: int = 3             # Strassen levels per C21 product (dests <= 2^depth <= 8)
+    max_depth: int = 4             # Strassen levels per C21 block
     min_dim: int = 512             # never split a Strassen node below this output side
-    dmma_tflops: float = 33.5      # measured product-kernel rate (profiles/)
-    hbm_gbs: float = 5500.0        # achieved combo-kernel bandwidth (profiles/)
-    gain: float = 1.5              # split only when saved time > gain * added time
-    ws_budget_gb: float = 40.0     # breadth-first operand sums of one AtA level up to this size
+    dmma_tflops: float = 33.5      # measured leaf-product rate (profiles/)
+    hbm_gbs: float = 5800.0        # achieved one-pass kernel bandwidth (profiles/)
+    gain: float = 1.25             # split only when saved time > gain * added time
+    ws_budget_gb: float = 40.0     # workspace for breadth-first planning of one AtA level
 
 
 def _ceil2(d: int) -> int:
     return (d + 1) // 2
 
 
+def _clip(w: Win, r0: int, c0: int, h: int, wd: int) -> Win:
+    h = max(0, min(h, w.rows - r0))
+    wd = max(0, min(wd, w.cols - c0))
+    if h == 0 or wd == 0:
+        return Win(w.base, w.off, w.ld, 0, 0)
+    return w.sub(r0, c0, h, wd)
+
+
 def _quads(w: Win, r1: int, c1: int):
     """Ceil-first quadrants of a window whose logical extent is (2*r1) x (2*c1);
     quadrants beyond the actual extent are empty windows (zero-extended)."""
-    def clip(r0, c0, h, wd):
-        h = max(0, min(h, w.rows - r0))
-        wd = max(0, min(wd, w.cols - c0))
-        if h == 0 or wd == 0:
-            return Win(w.base, w.off, w.ld, 0, 0)
-        return w.sub(r0, c0, h, wd)
-    return [clip(0, 0, r1, c1), clip(0, c1, r1, c1), clip(r1, 0, r1, c1), clip(r1, c1, r1, c1)]
+    return [_clip(w, 0, 0, r1, c1), _clip(w, 0, c1, r1, c1), _clip(w, r1, 0, r1, c1),
+            _clip(w, r1, c1, r1, c1)]
 
 
 class _AutoPlanner:
@@ -90,7 +91,6 @@ class _AutoPlanner:
         self.pb = PlanBuilder("auto")
         self.ws_top = 0          # bump allocator over the workspace (elements)
         self.ws_peak = 0
-        self.region_of = {}      # (base, off) -> region id, per leaf group
 
     # ---------------------------------------------------------------- workspace
     def alloc(self, rows: int, cols: int) -> Win:
@@ -104,105 +104,90 @@ class _AutoPlanner:
         if depth_left <= 0 or min(n, k) < 2 * self.p.min_dim or m < 2:
             return False
         saved_s = 2.0 * m * n * k / 8 / (self.p.dmma_tflops * 1e12)
-        # one multi-output combo per operand: read the whole operand, write 5 quarter sums
-        moved = 8.0 * (m * n * (1 + 5 / 4) + m * k * (1 + 5 / 4))
+        # pre: read both operands, write 5 + 5 quarter sums; post: write 7 child
+        # products (leaf epilogue), read them back, write (or RMW) 4 quadrants
+        moved = 8.0 * (m * n * (1 + 5 / 4) + m * k * (1 + 5 / 4) + n * k * (7 / 4 + 7 / 4 + 2))
         added_s = moved / (self.p.hbm_gbs * 1e9)
         return saved_s > self.p.gain * added_s
 
     # --------------------------------------------------------------- Strassen
-    def split(self, a: Win, b: Win, m: int, n: int, k: int, dests):
-        """Emit one node's operand sums; return its 7 children as
-        (a, b, m, n, k, dests) with composed destinations."""
+    def _sums(self, a: Win, b: Win, m: int, n: int, k: int):
+        """Emit one node's operand sums; return (S[7], T[7], m1, n1, k1)."""
         m1, n1, k1 = _ceil2(m), _ceil2(n), _ceil2(k)
-        Aq = _quads(a, m1, n1)
-        Bq = _quads(b, m1, k1)
-        S = [None] * 7
-        T = [None] * 7
-        for X, coefs, out, rows, cols in ((Aq, _S, S, m1, n1), (Bq, _T, T, m1, k1)):
+        S, T = [None] * 7, [None] * 7
+        for X, coefs, out, cols in ((_quads(a, m1, n1), _S, S, n1), (_quads(b, m1, k1), _T, T, k1)):
             outs = []
             for i, coef in enumerate(coefs):
                 if sorted(coef) == [0, 0, 0, 1]:
-                    out[i] = X[coef.index(1)]           # plain quadrant view
+                    out[i] = X[coef.index(1)]            # plain quadrant view
                 else:
-                    out[i] = self.alloc(rows, cols)
+                    out[i] = self.alloc(m1, cols)
                     outs.append((out[i], coef))
-            self.pb.combo4(X, outs)                     # one pass over the quadrants
-        qoff = [(0, 0), (0, k1), (n1, 0), (n1, k1)]
-        children = []
-        for i in range(7):
-            child = []
-            for q, sg in _D[i]:
-                r0, c0 = qoff[q]
-                for (W, s) in dests:
-                    h = min(n1, W.rows - r0)
-                    wd = min(k1, W.cols - c0)
-                    if h > 0 and wd > 0:
-                        child.append((W.sub(r0, c0, h, wd), s * sg))
-            if child:
-                children.append((S[i], T[i], m1, n1, k1, child))
-        return children
+            self.pb.combo4(X, outs)                      # one pass over the quadrants
+        return S, T, m1, n1, k1
 
-    def strassen(self, a: Win, b: Win, m: int, n: int, k: int, dests, depth_left: int, leaves):
-        """Plan c (+)= a^T b for LOGICAL extents m x n (a), m x k (b): windows may be
-        smaller (zero-extended).  dests = [(C window, sign)], origin = product (0,0)."""
-        if not self.worth_split(m, n, k, depth_left):
-            leaves.append((m, n, k, a, b, dests))
-            return
-        for ch in self.split(a, b, m, n, k, dests):
-            self.strassen(*ch, depth_left - 1, leaves)
+    def _post(self, kids, out: Win, sign: float, n1: int, k1: int, accumulate: bool):
+        q = [_clip(out, 0, 0, n1, k1), _clip(out, 0, k1, n1, k1), _clip(out, n1, 0, n1, k1),
+             _clip(out, n1, k1, n1, k1)]
+        self.pb.postadd7(kids, [(w, sign) for w in q], accumulate)
 
-    def emit_leaves(self, leaves):
-        group = self.pb.new_group()
-        regions = {}
-        for (m, n, k, a, b, dests) in leaves:
-            D = []
-            for (W, s) in dests:
-                key = (W.base, W.off)
-                if key not in regions:
-                    regions[key] = self.pb.new_region()
-                D.append((W, s, regions[key]))
-            S = [(a, 1.0)] if a.rows > 0 and a.cols > 0 else []
-            T = [(b, 1.0)] if b.rows > 0 and b.cols > 0 else []
-            if not S or not T:
-                continue  # an all-zero operand contributes nothing
-            self.pb.product("gemm", m, n, k, S, T, D, group=group)
-
-    def _dry_ws(self, a: Win, b: Win) -> int:
-        """Workspace a breadth-first plan of this block's Strassen tree needs."""
-        probe = _AutoPlanner(self.p)
-        probe.strassen(a, b, a.rows, a.cols, b.cols, [(Win(nat.BASE_C, 0, b.cols, a.cols, b.cols), 1.0)],
-                       self.p.max_depth, [])
-        return probe.ws_peak
-
-    def atb(self, a: Win, b: Win, c: Win):
-        """c += a^T b for one C21 block (a, b: m x n2 / m x n1 windows of A).
-        Depth-first over the top node's 7 products: only one subtree's sums are
-        alive beside the top-level sums; each subtree's leaves share launches."""
-        m, n, k = a.rows, a.cols, b.cols
-        depth = self.p.max_depth
+    def tree(self, a, b, m, n, k, out, sign, accumulate, depth, leaves, posts):
+        """Breadth-first: emit sums now (pre-order), collect leaves and post-adds."""
         if not self.worth_split(m, n, k, depth):
-            self.emit_leaves([(m, n, k, a, b, [(c, 1.0)])])
+            leaves.append((m, n, k, a, b, out, sign, accumulate))
+            return
+        S, T, m1, n1, k1 = self._sums(a, b, m, n, k)
+        kids = [self.alloc(n1, k1) for _ in range(7)]
+        for i in range(7):
+            self.tree(S[i], T[i], m1, n1, k1, kids[i], 1.0, False, depth - 1, leaves, posts)
+        posts.append((kids, out, sign, n1, k1, accumulate))
+
+    def emit(self, leaves, posts):
+        group = self.pb.new_group()
+        for (m, n, k, a, b, out, sign, accumulate) in leaves:
+            if a.rows == 0 or a.cols == 0 or b.rows == 0 or b.cols == 0:
+                if not accumulate:            # an all-zero operand: the product buffer is zero
+                    self.pb.fill(out)
+                continue
+            self.pb.product("gemm", m, n, k, [(a, 1.0)], [(b, 1.0)], [(out, sign)],
+                            accumulate=int(accumulate), group=group)
+        for (kids, out, sign, n1, k1, accumulate) in posts:
+            self._post(kids, out, sign, n1, k1, accumulate)
+
+    def node(self, a, b, m, n, k, out, sign, accumulate, depth):
+        """Depth-first at this node when its breadth-first workspace exceeds the budget."""
+        need = self._dry_ws(a, b, m, n, k, depth)
+        if self.ws_top + need <= self.budget or not self.worth_split(m, n, k, depth):
+            leaves, posts = [], []
+            mark = self.ws_top
+            self.tree(a, b, m, n, k, out, sign, accumulate, depth, leaves, posts)
+            self.emit(leaves, posts)
+            self.ws_top = mark
             return
         mark = self.ws_top
-        for ch in self.split(a, b, m, n, k, [(c, 1.0)]):
-            sub = self.ws_top
-            leaves = []
-            self.strassen(*ch, depth - 1, leaves)
-            self.emit_leaves(leaves)
-            self.ws_top = sub
+        S, T, m1, n1, k1 = self._sums(a, b, m, n, k)
+        kids = [self.alloc(n1, k1) for _ in range(7)]
+        for i in range(7):
+            self.node(S[i], T[i], m1, n1, k1, kids[i], 1.0, False, depth - 1)
+        self._post(kids, out, sign, n1, k1, accumulate)
         self.ws_top = mark
+
+    def _dry_ws(self, a, b, m, n, k, depth) -> int:
+        probe = _AutoPlanner(self.p)
+        probe.tree(a, b, m, n, k, Win(nat.BASE_C, 0, max(k, 1), n, k), 1.0, True, depth, [], [])
+        return probe.ws_peak
 
     def ata(self, m: int, n: int, lda: int, ldc: int):
         A = Win(nat.BASE_A, 0, lda, m, n)
         C = Win(nat.BASE_C, 0, ldc, n, n)
+        self.budget = int(self.p.ws_budget_gb * 1e9 / 8)
         level = [(0, n)]
-        leaves = []
-        budget = int(self.p.ws_budget_gb * 1e9 / 8)
+        diag = []
         while level:
             blocks, nxt = [], []
             for (c0, w) in level:
                 if w <= self.p.leaf_cols or w < 2:
-                    leaves.append((c0, w))
+                    diag.append((c0, w))
                     continue
                 n1 = w // 2
                 n2 = w - n1
@@ -210,38 +195,23 @@ class _AutoPlanner:
                                C.sub(c0 + n1, c0, n2, n1)))
                 nxt += [(c0, n1), (c0 + n1, n2)]
             if blocks:
-                # the C21 blocks of one AtA level are disjoint: plan them breadth-first
-                # into ONE leaf group when their operand sums fit the workspace budget
-                need = sum(self._dry_ws(a, b) for (a, b, _) in blocks)
-                if need <= budget:
-                    lv_leaves = []
+                # the C21 blocks of one AtA level are disjoint: one breadth-first
+                # leaf group for the whole level when it fits the budget
+                need = sum(self._dry_ws(a, b, a.rows, a.cols, b.cols, self.p.max_depth)
+                           for (a, b, _) in blocks)
+                if need <= self.budget:
+                    leaves, posts = [], []
                     for (a, b, c) in blocks:
-                        self.strassen(a, b, a.rows, a.cols, b.cols, [(c, 1.0)], self.p.max_depth,
-                                      lv_leaves)
-                    self.emit_leaves(lv_leaves)
-                    self.ws_top = 0  # stream order: the next level may reuse the sums
-                else:
-                    # top-child-major: all blocks' top-level sums, then subtree i of
-                    # every block as one leaf group (only one subtree per block alive)
-                    tops = []
-                    for (a, b, c) in blocks:
-                        m_, n_, k_ = a.rows, a.cols, b.cols
-                        if self.worth_split(m_, n_, k_, self.p.max_depth):
-                            tops.append(self.split(a, b, m_, n_, k_, [(c, 1.0)]))
-                        else:
-                            self.emit_leaves([(m_, n_, k_, a, b, [(c, 1.0)])])
-                    mark = self.ws_top
-                    for i in range(7):
-                        lv_leaves = []
-                        for children in tops:
-                            if i < len(children):
-                                self.strassen(*children[i], self.p.max_depth - 1, lv_leaves)
-                        self.emit_leaves(lv_leaves)
-                        self.ws_top = mark
+                        self.tree(a, b, a.rows, a.cols, b.cols, c, 1.0, True, self.p.max_depth,
+                                  leaves, posts)
+                    self.emit(leaves, posts)
                     self.ws_top = 0
+                else:
+                    for (a, b, c) in blocks:
+                        self.node(a, b, a.rows, a.cols, b.cols, c, 1.0, True, self.p.max_depth)
             level = nxt
         group = self.pb.new_group()
-        for (c0, w) in sorted(leaves):
+        for (c0, w) in sorted(diag):
             self.pb.product("syrk", m, w, w, [(A.sub(0, c0, m, w), 1.0)], [],
                             [(C.sub(c0, c0, w, w), 1.0)], group=group)
 

@@ -144,6 +144,21 @@ int validate_op(const ata_op& op, const Bases& b, int i) {
     case ATA_OP_FILL:
       if (op.nd != 1) return fail(ATA_E_ARG, "fill needs 1 dest");
       return ATA_OK;
+    case ATA_OP_POSTADD7:
+      if (op.ns != 4 || op.nt != 3 || op.nd != 4)
+        return fail(ATA_E_ARG, "postadd7 needs 7 children (s[0..3], t[0..2]) and 4 outputs");
+      {
+        int maxr = 0, maxc = 0;
+        for (int q = 0; q < 7; ++q) {
+          const ata_ref& c = q < 4 ? op.s[q] : op.t[q - 4];
+          maxr = std::max(maxr, c.rows);
+          maxc = std::max(maxc, c.cols);
+        }
+        for (int j = 0; j < 4; ++j)
+          if (op.d[j].rows > maxr || op.d[j].cols > maxc)
+            return fail(ATA_E_SHAPE, "shape mismatch: postadd7 output exceeds its children");
+      }
+      return ATA_OK;
     case ATA_OP_COMBO4:
       if (op.ns < 1 || op.nd < 1) return fail(ATA_E_ARG, "combo4 needs sources and dests");
       for (int j = 0; j < op.nd; ++j) {
@@ -322,6 +337,18 @@ int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, int* sync, int64_t 
         a.cols = a.cols > op.d[j].cols ? a.cols : op.d[j].cols;
       }
       e = ata::launch_combo4<T>(a, s);
+    } else if (op.type == ATA_OP_POSTADD7) {
+      ata::EwArgs<T> a;
+      std::memset(&a, 0, sizeof(a));
+      a.nsrc = 7;
+      a.ndst = 4;
+      for (int q = 0; q < 7; ++q) {
+        a.src[q] = term_of<T>(q < 4 ? op.s[q] : op.t[q - 4], b);
+        a.rows = a.rows > a.src[q].rows ? a.rows : a.src[q].rows;
+        a.cols = a.cols > a.src[q].cols ? a.cols : a.src[q].cols;
+      }
+      for (int j = 0; j < 4; ++j) a.dst[j] = dest_of<T>(op.d[j], b);
+      e = ata::launch_postadd7<T>(a, op.accumulate, s);
     }
     if (e != cudaSuccess) return cuda_fail(e, "elementwise launch");
     return ATA_OK;

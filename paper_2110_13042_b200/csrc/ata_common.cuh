@@ -51,13 +51,14 @@ struct BatchArgs {
   int* sync;  // [0] = work counter, [1..] = destination turn counters (zeroed per launch)
   int n_sync;  // ints available at sync
   int dynamic; // 1: tiles handed out by the work counter (needed for ordered destinations)
+  int dbg;     // experiment flags (ATA_DBG): 1 = skip ordering waits, 2 = skip epilogue
   DProd<T> p[kMaxBatch];
 };
 
 template <typename T>
 struct EwArgs {  // elementwise op: rows x cols iteration space
   int rows, cols, nsrc, ndst;
-  DTerm<T> src[4];
+  DTerm<T> src[8];
   DDest<T> dst[kMaxDests];
 };
 
@@ -69,6 +70,7 @@ cudaError_t launch_batch_f32(const BatchArgs<float>& a, cudaStream_t s, bool spl
 template <typename T> cudaError_t launch_combo(const EwArgs<T>& a, cudaStream_t s);
 template <typename T> cudaError_t launch_update(const EwArgs<T>& a, cudaStream_t s);
 template <typename T> cudaError_t launch_combo4(const EwArgs<T>& a, cudaStream_t s);
+template <typename T> cudaError_t launch_postadd7(const EwArgs<T>& a, int accumulate, cudaStream_t s);
 template <typename T> cudaError_t launch_fill(T* p, long long ld, int rows, int cols, cudaStream_t s);
 template <typename T> cudaError_t launch_mirror(T* C, long long ldc, int n, cudaStream_t s);
 template <typename T> cudaError_t launch_pack(const T* C, long long ldc, int n, T* packed, cudaStream_t s);

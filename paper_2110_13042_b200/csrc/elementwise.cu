@@ -88,6 +88,49 @@ __global__ void combo4_kernel(const __grid_constant__ EwArgs<T> a) {
   }
 }
 
+// postadd7: the 4 output quadrants of one Strassen node from its 7 children
+// (one read of each child, one write (or RMW) of each output quadrant).
+template <typename T>
+__global__ void postadd7_kernel(const __grid_constant__ EwArgs<T> a, int accumulate) {
+  const int c0 = (blockIdx.x * blockDim.x + threadIdx.x) * 2;
+  if (c0 >= a.cols) return;
+  for (int r = blockIdx.y * blockDim.y + threadIdx.y; r < a.rows; r += gridDim.y * blockDim.y) {
+    T p[7][2];
+#pragma unroll
+    for (int i = 0; i < 7; ++i) {
+      p[i][0] = p[i][1] = T(0);
+      const DTerm<T>& S = a.src[i];
+      if (r < S.rows) {
+        const T* q = S.p + (long long)r * S.ld + c0;
+        if (c0 < S.cols) p[i][0] = __ldcs(q);
+        if (c0 + 1 < S.cols) p[i][1] = __ldcs(q + 1);
+      }
+    }
+    T o[4][2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      o[0][e] = p[0][e] + p[3][e] - p[4][e] + p[6][e];
+      o[1][e] = p[2][e] + p[4][e];
+      o[2][e] = p[1][e] + p[3][e];
+      o[3][e] = p[0][e] - p[1][e] + p[2][e] + p[5][e];
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const DDest<T>& D = a.dst[j];
+      if (r >= D.rows) continue;
+      T* q = D.p + (long long)r * D.ld + c0;
+      const T sg = T(D.sign);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        if (c0 + e < D.cols) {
+          const T v = sg * o[j][e];
+          q[e] = accumulate ? q[e] + v : v;
+        }
+      }
+    }
+  }
+}
+
 // update: for each dest d, D_d[r,c] += sign_d * P[r,c] (r < D_d.rows, c < D_d.cols)
 template <typename T>
 __global__ void update_kernel(const __grid_constant__ EwArgs<T> a) {
@@ -191,6 +234,15 @@ cudaError_t launch_combo4(const EwArgs<T>& a, cudaStream_t s) {
   return cudaGetLastError();
 }
 template <typename T>
+cudaError_t launch_postadd7(const EwArgs<T>& a, int accumulate, cudaStream_t s) {
+  if (a.rows <= 0 || a.cols <= 0) return cudaSuccess;
+  dim3 blk(kEwThreadsX, kEwThreadsY);
+  const int gx = (a.cols + 2 * kEwThreadsX - 1) / (2 * kEwThreadsX);
+  dim3 grd(gx, ew_grid_y(a.rows, gx));
+  postadd7_kernel<T><<<grd, blk, 0, s>>>(a, accumulate);
+  return cudaGetLastError();
+}
+template <typename T>
 cudaError_t launch_update(const EwArgs<T>& a, cudaStream_t s) {
   if (a.rows <= 0 || a.cols <= 0) return cudaSuccess;
   dim3 blk(kEwThreadsX, kEwThreadsY);
@@ -239,6 +291,7 @@ cudaError_t launch_unpack(const T* packed, int n, T* C, long long ldc, int acc, 
 #define ATA_INST(T)                                                                       \
   template cudaError_t launch_combo<T>(const EwArgs<T>&, cudaStream_t);                   \
   template cudaError_t launch_combo4<T>(const EwArgs<T>&, cudaStream_t);                  \
+  template cudaError_t launch_postadd7<T>(const EwArgs<T>&, int, cudaStream_t);           \
   template cudaError_t launch_update<T>(const EwArgs<T>&, cudaStream_t);                  \
   template cudaError_t launch_fill<T>(T*, long long, int, int, cudaStream_t);             \
   template cudaError_t launch_mirror<T>(T*, long long, int, cudaStream_t);                \

@@ -26,16 +26,17 @@
 //       (no wave-quantisation tail per product).
 // Deadlock freedom: tiles are handed out in increasing order and a tile only
 // waits for turns of strictly earlier tiles, which are already running.
+#include <cstdlib>
+
 #include "ata_common.cuh"
 
 namespace ata {
 
 namespace ws64 {
-constexpr int BM = 128, BN = 128, BK = 16, LD = BM + 4;
+constexpr int BM = 128, BN = 128, LD = BM + 4;
 constexpr int CONSUMERS = 8, PRODUCERS = 128, THREADS = CONSUMERS * 32 + PRODUCERS;
-constexpr int PRODUCER_REGS = 40, CONSUMER_REGS = 232;  // setmaxnreg split of the 64K RF
+constexpr int PRODUCER_REGS = 40, CONSUMER_REGS = 232;  // 128*40 + 256*232 = 384*168 (the launch allocation)
 constexpr int WTM = 8, WTN = 4;  // 64 x 32 per consumer warp
-constexpr int BUF = BK * LD;     // doubles per operand buffer
 constexpr int SMEM_BUDGET = 225 * 1024;
 constexpr int TSLOTS = 2;        // tile-info ring
 }  // namespace ws64
@@ -80,7 +81,7 @@ __device__ __forceinline__ void st_release(int* p, int v) {
 }
 
 // The producer warpgroup copies a BK x 128 window of term t (rows l0.., cols c0..).
-template <bool VEC16>
+template <int BK, bool VEC16>
 __device__ __forceinline__ void ws_load(double* buf, const DTerm<double>& t, int l0, int c0, int pt) {
   using namespace ws64;
   if (VEC16) {
@@ -112,7 +113,7 @@ __device__ __forceinline__ void ws_load(double* buf, const DTerm<double>& t, int
   }
 }
 
-template <bool VEC16>
+template <int BK, bool VEC16>
 __device__ __forceinline__ void ws_combine(double* x, const double* y, double sign, int pt) {
   using namespace ws64;
   if (VEC16) {
@@ -173,10 +174,11 @@ __device__ __forceinline__ TileInfo decode_tile(const BatchArgs<double>& args, i
   return t;
 }
 
-template <int NS, int NT, int STAGES>
+template <int BK, int NS, int NT, int STAGES>
 __global__ void __launch_bounds__(ws64::THREADS, 1)
     prod_f64_ws_kernel(const __grid_constant__ BatchArgs<double> args) {
   using namespace ws64;
+  constexpr int BUF = BK * LD;  // doubles per operand buffer
   constexpr int STAGE = (NS + NT) * BUF;
   extern __shared__ __align__(128) double smem[];
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE);
@@ -236,32 +238,32 @@ __global__ void __launch_bounds__(ws64::THREADS, 1)
       auto issue = [&](int kt, int ring) {
         double* base = smem + (ring % STAGES) * STAGE;
         const int l0 = kt * BK;
-        if (vs) ws_load<true>(base, S0, l0, i0, pt);
-        else ws_load<false>(base, S0, l0, i0, pt);
+        if (vs) ws_load<BK, true>(base, S0, l0, i0, pt);
+        else ws_load<BK, false>(base, S0, l0, i0, pt);
         if (NS == 2 && ns == 2) {
-          if (vs) ws_load<true>(base + BUF, S1, l0, i0, pt);
-          else ws_load<false>(base + BUF, S1, l0, i0, pt);
+          if (vs) ws_load<BK, true>(base + BUF, S1, l0, i0, pt);
+          else ws_load<BK, false>(base + BUF, S1, l0, i0, pt);
         }
         if (!same) {
           double* tb = base + NS * BUF;
-          if (vt) ws_load<true>(tb, T0, l0, j0, pt);
-          else ws_load<false>(tb, T0, l0, j0, pt);
+          if (vt) ws_load<BK, true>(tb, T0, l0, j0, pt);
+          else ws_load<BK, false>(tb, T0, l0, j0, pt);
           if (NT == 2 && nt == 2) {
-            if (vt) ws_load<true>(tb + BUF, T1, l0, j0, pt);
-            else ws_load<false>(tb + BUF, T1, l0, j0, pt);
+            if (vt) ws_load<BK, true>(tb + BUF, T1, l0, j0, pt);
+            else ws_load<BK, false>(tb + BUF, T1, l0, j0, pt);
           }
         }
       };
       auto finish = [&](int ring) {  // combine two-term operands of a stage, publish it
         double* base = smem + (ring % STAGES) * STAGE;
         if (NS == 2 && ns == 2) {
-          if (vs) ws_combine<true>(base, base + BUF, S1.sign, pt);
-          else ws_combine<false>(base, base + BUF, S1.sign, pt);
+          if (vs) ws_combine<BK, true>(base, base + BUF, S1.sign, pt);
+          else ws_combine<BK, false>(base, base + BUF, S1.sign, pt);
         }
         if (NT == 2 && nt == 2) {
           double* tb = base + NS * BUF;
-          if (vt) ws_combine<true>(tb, tb + BUF, T1.sign, pt);
-          else ws_combine<false>(tb, tb + BUF, T1.sign, pt);
+          if (vt) ws_combine<BK, true>(tb, tb + BUF, T1.sign, pt);
+          else ws_combine<BK, false>(tb, tb + BUF, T1.sign, pt);
         }
         mbar_arrive(&full[ring % STAGES]);
       };
@@ -342,13 +344,13 @@ __global__ void __launch_bounds__(ws64::THREADS, 1)
     // ---- epilogue: fused post-additions into up to four destinations ----
     const int nd = P.nd;
     const bool accumulate = P.accumulate != 0;
-    for (int d = 0; d < nd; ++d) {
+    for (int d = 0; d < ((args.dbg & 2) ? 0 : nd); ++d) {
       const DDest<double>& D = P.d[d];
       const double scale = args.alpha * D.sign;
       if (i0 >= D.rows || j0 >= D.cols) continue;  // tile entirely outside this window
       int* sem = nullptr;
       int turn = 0;
-      if (D.sem >= 0) {
+      if (D.sem >= 0 && !(args.dbg & 1)) {
         // turn = earlier products of the launch whose window in this region covers the tile
         for (int q = 0; q < tl.pi; ++q)
           for (int e = 0; e < args.p[q].nd; ++e) {
@@ -419,7 +421,7 @@ static int num_sms() {
   return n;
 }
 
-template <int NS, int NT>
+template <int BK, int NS, int NT>
 static cudaError_t launch_ws(BatchArgs<double> a, cudaStream_t s) {
   using namespace ws64;
   long long total = 0;
@@ -468,18 +470,19 @@ static cudaError_t launch_ws(BatchArgs<double> a, cudaStream_t s) {
   }
   cudaError_t e = cudaSuccess;
   a.dynamic = n_sync > 1;
+  { const char* e = std::getenv("ATA_DBG"); a.dbg = e ? std::atoi(e) : 0; }
   if (a.dynamic) {
     if (a.sync == nullptr || n_sync > a.n_sync) return cudaErrorInvalidValue;
     e = cudaMemsetAsync(a.sync, 0, (size_t)n_sync * sizeof(int), s);
     if (e != cudaSuccess) return e;
   }
-  constexpr int STAGE_BYTES = (NS + NT) * BUF * 8;
+  constexpr int STAGE_BYTES = (NS + NT) * BK * LD * 8;
   constexpr int STAGES =
       (SMEM_BUDGET - 1024) / STAGE_BYTES > 8 ? 8 : (SMEM_BUDGET - 1024) / STAGE_BYTES;
   static_assert(STAGES >= 2, "smem");
   const size_t smem = (size_t)STAGES * STAGE_BYTES + (2 * STAGES + 2 * TSLOTS) * sizeof(uint64_t) +
                       (TSLOTS + 2) * sizeof(int);
-  auto kern = prod_f64_ws_kernel<NS, NT, STAGES>;
+  auto kern = prod_f64_ws_kernel<BK, NS, NT, STAGES>;
   static bool attr_set = false;
   if (!attr_set) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -497,10 +500,21 @@ cudaError_t launch_batch_f64_ws(const BatchArgs<double>& a, cudaStream_t s) {
     ns = max(ns, a.p[i].ns);
     if (a.p[i].kind != kSyrk) nt = max(nt, a.p[i].nt);
   }
-  if (ns == 1 && nt == 1) return launch_ws<1, 1>(a, s);
-  if (ns == 2 && nt == 1) return launch_ws<2, 1>(a, s);
-  if (ns == 1 && nt == 2) return launch_ws<1, 2>(a, s);
-  return launch_ws<2, 2>(a, s);
+  static int bk = -1;
+  if (bk < 0) {
+    const char* e = std::getenv("ATA_WS_BK");
+    bk = e ? std::atoi(e) : 16;
+  }
+  if (bk == 32) {
+    if (ns == 1 && nt == 1) return launch_ws<32, 1, 1>(a, s);
+    if (ns == 2 && nt == 1) return launch_ws<16, 2, 1>(a, s);
+    if (ns == 1 && nt == 2) return launch_ws<16, 1, 2>(a, s);
+    return launch_ws<16, 2, 2>(a, s);
+  }
+  if (ns == 1 && nt == 1) return launch_ws<16, 1, 1>(a, s);
+  if (ns == 2 && nt == 1) return launch_ws<16, 2, 1>(a, s);
+  if (ns == 1 && nt == 2) return launch_ws<16, 1, 2>(a, s);
+  return launch_ws<16, 2, 2>(a, s);
 }
 
 }  // namespace ata

@@ -152,6 +152,18 @@ class PlanBuilder:
         self.launches += 1
         self._last_group = None
 
+    def postadd7(self, children, outputs, accumulate: bool):
+        """Strassen post-addition of one node: children = 7 product windows
+        (P1..P7), outputs = [(C11 win, sign), (C12..), (C21..), (C22..)]."""
+        for w in list(children) + [o[0] for o in outputs]:
+            self._touch(w)
+        s = [_ref(w) for w in children[:4]]
+        t = [_ref(w) for w in children[4:]] + [_EMPTY]
+        d = [_ref(w, sg) for (w, sg) in outputs] + [_EMPTY] * (nat.MAX_DESTS - 4)
+        self.rows.append((nat.OP_POSTADD7, 0, 0, 0, 4, 3, 4, int(accumulate), -1, 0, s, t, d))
+        self.launches += 1
+        self._last_group = None
+
     def finish(self) -> Plan:
         ops = np.array(self.rows, dtype=nat.OP_DTYPE) if self.rows else np.zeros(0, nat.OP_DTYPE)
         return Plan(ops, self.mults, self.ws_hi, self.launches, self.kind)

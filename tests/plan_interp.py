@@ -6,7 +6,7 @@ without a GPU.  Never used by the product path.
 """
 import numpy as np
 
-OP_GEMM, OP_SYRK, OP_COMBO, OP_UPDATE, OP_FILL, OP_COMBO4 = 0, 1, 2, 3, 4, 5
+OP_GEMM, OP_SYRK, OP_COMBO, OP_UPDATE, OP_FILL, OP_COMBO4, OP_POSTADD7 = 0, 1, 2, 3, 4, 5, 6
 
 
 def _win(bases, r, write=False):
@@ -67,6 +67,27 @@ def run(ops, A, C, alpha=1.0, WS=None, B=None):
                 w += float(op["d"][j]["sign"]) * src[:w.shape[0], :w.shape[1]]
         elif t == OP_FILL:
             _win(bases, op["d"][0], write=True)[...] = 0
+        elif t == OP_POSTADD7:
+            kids = [op["s"][q] for q in range(4)] + [op["t"][q] for q in range(3)]
+            wins = [_win(bases, r) for r in kids]
+            R = max((w.shape[0] for w in wins if w is not None), default=0)
+            Cc = max((w.shape[1] for w in wins if w is not None), default=0)
+            P = []
+            for w in wins:
+                z = np.zeros((R, Cc), dtype=dtype)
+                if w is not None:
+                    z[:w.shape[0], :w.shape[1]] = w
+                P.append(z)
+            Q = [P[0] + P[3] - P[4] + P[6], P[2] + P[4], P[1] + P[3], P[0] - P[1] + P[2] + P[5]]
+            for j in range(4):
+                d = _win(bases, op["d"][j], write=True)
+                if d is None:
+                    continue
+                v = float(op["d"][j]["sign"]) * Q[j][:d.shape[0], :d.shape[1]]
+                if int(op["accumulate"]):
+                    d += v
+                else:
+                    d[...] = v
         elif t == OP_COMBO4:
             srcs = [_win(bases, op["s"][q]) for q in range(int(op["ns"]))]
             for j in range(int(op["nd"])):
