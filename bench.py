@@ -164,6 +164,13 @@ def cpu_sample_rate(cfg_name, cores):
     return r * c * c / dt / 1e9, dt, sample
 
 
+def workload_name(name):
+    from paper_2110_13042_b200.measure import CONFIGS
+    c = CONFIGS[name]
+    return (f"{name}: A {c['m']}x{c['n']} {c['dtype']} {c['dist']} seed {c['seed']}, "
+            f"lower(A^T A), threshold {c['threshold']}")
+
+
 def run_reference(args, world, rank):
     if rank != 0:
         return
@@ -181,8 +188,7 @@ def run_reference(args, world, rank):
             "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64" if cfg["dtype"] == "f64" else "f32", "data": "synthetic",
-            "config": {"workload": f"{args.config}: A {cfg['m']}x{cfg['n']} {cfg['dtype']}",
-                       "sample": sample},
+            "config": {"workload": workload_name(args.config), "sample": sample},
             "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": cores, "kind": "port",
                              "sample": sample},
             "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
@@ -340,9 +346,7 @@ def main():
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64" if f64 else "f32 (tf32 products)", "data": "synthetic",
-            "config": {"workload": f"{args.config}: A {m}x{n} {cfg['dtype']} "
-                                   f"{cfg['dist']} seed {cfg['seed']}, lower(A^T A), "
-                                   f"threshold {threshold}",
+            "config": {"workload": workload_name(args.config),
                        "parallelism": f"row-shard x{world}" if world > 1 else "single GPU",
                        "l2": "inputs larger than L2 (A is %.1f GB)" % (A.numel() * A.element_size() / 1e9),
                        "plan": {"kind": plan.kind, "ops": len(plan.ops), "launches": n_launch,

@@ -57,7 +57,8 @@ extern "C" {
  * ATA_OP_COMBO4 reads up to 4 sources s[0..3] (the quadrants of one operand) and
  * writes up to 8 sums d[j] = sum_q c_jq * zero-extended s[q], truncated to d[j]'s
  * extent; c_jq is packed in d[j].region as base-4 digits (digit q: 0 -> 0,
- * 1 -> +1, 2 -> -1).  One pass over the quadrants produces all of a Strassen
+ * 1 -> +1, 2 -> -1); accumulate = 1 restricts every output to its lower
+ * triangle (col <= row), which is how split-contraction SYRK partials are summed.  One pass over the quadrants produces all of a Strassen
  * node's operand sums (strassen.py:234-273). */
 #define ATA_OP_COMBO4 5
 /* ATA_OP_POSTADD7: Strassen post-addition of one node in one pass

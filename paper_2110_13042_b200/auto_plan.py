@@ -64,6 +64,12 @@ class AutoParams:
     hbm_gbs: float = 5800.0        # achieved one-pass kernel bandwidth (profiles/)
     gain: float = 1.25             # split only when saved time > gain * added time
     ws_budget_gb: float = 40.0     # workspace for breadth-first planning of one AtA level
+    fill_waves: int = 2            # split the contraction of groups with fewer tiles than this
+    min_chunk: int = 8192          # ... into chunks of at least this many rows
+
+
+TILE = 128        # output tile of the product kernels
+NUM_SMS = 148     # B200
 
 
 def _ceil2(d: int) -> int:
@@ -143,16 +149,71 @@ class _AutoPlanner:
         posts.append((kids, out, sign, n1, k1, accumulate))
 
     def emit(self, leaves, posts):
-        group = self.pb.new_group()
+        prods = []
         for (m, n, k, a, b, out, sign, accumulate) in leaves:
             if a.rows == 0 or a.cols == 0 or b.rows == 0 or b.cols == 0:
                 if not accumulate:            # an all-zero operand: the product buffer is zero
                     self.pb.fill(out)
                 continue
-            self.pb.product("gemm", m, n, k, [(a, 1.0)], [(b, 1.0)], [(out, sign)],
-                            accumulate=int(accumulate), group=group)
+            prods.append(("gemm", m, n, k, a, b, out, sign, accumulate))
+        self.emit_products(prods)
         for (kids, out, sign, n1, k1, accumulate) in posts:
             self._post(kids, out, sign, n1, k1, accumulate)
+
+    @staticmethod
+    def _tiles(kind, n, k):
+        t = -(-n // TILE)
+        return t * (t + 1) // 2 if kind == "syrk" else t * -(-k // TILE)
+
+    def emit_products(self, prods):
+        """One launch group.  When the group's output tiles cannot fill the GPU
+        (tall-skinny operands, config c5) the contraction is split into S
+        chunks: chunk products write private partial buffers, then one-pass
+        combo4 sums add them into the destination (lower triangle only for
+        SYRK), so no atomics and a fixed summation order."""
+        if not prods:
+            return
+        tiles = sum(self._tiles(p[0], p[2], p[3]) for p in prods)
+        target = self.p.fill_waves * NUM_SMS
+        S = 1
+        if tiles < target:
+            S = min(-(-target // tiles), min(p[1] for p in prods) // self.p.min_chunk)
+        group = self.pb.new_group()
+        if S <= 1:
+            for (kind, m, n, k, a, b, out, sign, accumulate) in prods:
+                T = [] if kind == "syrk" else [(b, 1.0)]
+                self.pb.product(kind, m, n, k, [(a, 1.0)], T, [(out, sign)],
+                                accumulate=int(accumulate), group=group)
+            return
+        reductions = []
+        for (kind, m, n, k, a, b, out, sign, accumulate) in prods:
+            mc = -(-m // S)
+            parts = []
+            for c in range(S):
+                r0 = c * mc
+                rows = min(mc, m - r0)
+                if rows <= 0:
+                    break
+                ac = _clip(a, r0, 0, rows, a.cols)
+                bc = ac if b is None else _clip(b, r0, 0, rows, b.cols)
+                if ac.rows == 0 or bc.rows == 0:
+                    continue
+                P = self.alloc(n, k)
+                T = [] if kind == "syrk" else [(bc, 1.0)]
+                self.pb.product(kind, rows, n, k, [(ac, 1.0)], T, [(P, 1.0)], accumulate=0,
+                                group=group)
+                parts.append(P)
+            reductions.append((kind, out, sign, accumulate, parts))
+        for (kind, out, sign, accumulate, parts) in reductions:
+            srcs = list(parts)
+            first = True
+            while srcs or first:
+                head = [] if (first and not accumulate) else [out]
+                take = srcs[:4 - len(head)]
+                srcs = srcs[len(take):]
+                coefs = tuple([1] * len(head) + [int(sign)] * len(take))
+                self.pb.combo4(head + take, [(out, coefs)], lower=(kind == "syrk"))
+                first = False
 
     def node(self, a, b, m, n, k, out, sign, accumulate, depth):
         """Depth-first at this node when its breadth-first workspace exceeds the budget."""
@@ -210,10 +271,8 @@ class _AutoPlanner:
                     for (a, b, c) in blocks:
                         self.node(a, b, a.rows, a.cols, b.cols, c, 1.0, True, self.p.max_depth)
             level = nxt
-        group = self.pb.new_group()
-        for (c0, w) in sorted(diag):
-            self.pb.product("syrk", m, w, w, [(A.sub(0, c0, m, w), 1.0)], [],
-                            [(C.sub(c0, c0, w, w), 1.0)], group=group)
+        self.emit_products([("syrk", m, w, w, A.sub(0, c0, m, w), None, C.sub(c0, c0, w, w), 1.0,
+                             True) for (c0, w) in sorted(diag)])
 
 
 def plan_ata_auto(m: int, n: int, lda: int, ldc: int, params: AutoParams = AutoParams()) -> Plan:

@@ -329,6 +329,7 @@ int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, int* sync, int64_t 
       std::memset(&a, 0, sizeof(a));
       a.nsrc = op.ns;
       a.ndst = op.nd;
+      a.lower = op.accumulate;  // COMBO4: accumulate field = lower-triangular outputs
       for (int j = 0; j < op.ns; ++j) a.src[j] = term_of<T>(op.s[j], b);
       for (int j = 0; j < op.nd; ++j) {
         a.dst[j] = dest_of<T>(op.d[j], b);

@@ -58,6 +58,8 @@ struct BatchArgs {
 template <typename T>
 struct EwArgs {  // elementwise op: rows x cols iteration space
   int rows, cols, nsrc, ndst;
+  int lower;  // combo4: write only elements with col <= row of each output window
+  int _pad;
   DTerm<T> src[8];
   DDest<T> dst[kMaxDests];
 };

@@ -82,8 +82,9 @@ __global__ void combo4_kernel(const __grid_constant__ EwArgs<T> a) {
         else if (cq == 2) o0 -= v[q][0], o1 -= v[q][1];
       }
       T* p = D.p + (long long)r * D.ld + c0;
-      if (c0 < D.cols) __stcs(p, o0);
-      if (c0 + 1 < D.cols) __stcs(p + 1, o1);
+      const int cmax = a.lower ? min(D.cols, r + 1) : D.cols;
+      if (c0 < cmax) __stcs(p, o0);
+      if (c0 + 1 < cmax) __stcs(p + 1, o1);
     }
   }
 }

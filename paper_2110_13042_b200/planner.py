@@ -132,9 +132,10 @@ class PlanBuilder:
     def fill(self, dst: Win):
         self._ew(nat.OP_FILL, [], [(dst, 1.0)])
 
-    def combo4(self, sources, outputs):
+    def combo4(self, sources, outputs, lower: bool = False):
         """One pass over up to 4 source windows writing up to 8 sums:
-        outputs = [(dst Win, (c_0, .., c_{ns-1}))] with c_q in {0, +1, -1}."""
+        outputs = [(dst Win, (c_0, .., c_{ns-1}))] with c_q in {0, +1, -1};
+        lower=True writes only the lower triangle of each output window."""
         if len(sources) > nat.MAX_TERMS or len(outputs) > nat.MAX_DESTS:
             raise ValueError("combo4: too many sources/outputs")
         for w in list(sources) + [o[0] for o in outputs]:
@@ -147,7 +148,7 @@ class PlanBuilder:
                 code |= (1 if cq > 0 else 2 if cq < 0 else 0) << (2 * q)
             d.append(_ref(w, 1.0, code))
         d += [_EMPTY] * (nat.MAX_DESTS - len(outputs))
-        self.rows.append((nat.OP_COMBO4, 0, 0, 0, len(sources), 0, len(outputs), 0, -1, 0, s,
+        self.rows.append((nat.OP_COMBO4, 0, 0, 0, len(sources), 0, len(outputs), int(lower), -1, 0, s,
                           [_EMPTY] * nat.MAX_TERMS, d))
         self.launches += 1
         self._last_group = None

@@ -100,7 +100,11 @@ def run(ops, A, C, alpha=1.0, WS=None, B=None):
                         continue
                     r, c = min(w.shape[0], d.shape[0]), min(w.shape[1], d.shape[1])
                     acc[:r, :c] += (1.0 if cq == 1 else -1.0) * w[:r, :c]
-                d[...] = acc
+                if int(op["accumulate"]):   # lower-triangular outputs
+                    mask = np.tril(np.ones(d.shape, dtype=bool))
+                    d[mask] = acc[mask]
+                else:
+                    d[...] = acc
         else:
             raise ValueError(t)
     return C
