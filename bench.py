@@ -234,7 +234,7 @@ def main():
                                                         ("min_dim", args.min_dim)) if v is not None})
     mloc = r1 - r0
     if threshold == "auto":
-        plan = auto_plan.plan_ata_auto(mloc, n, n, n, params)
+        plan = auto_plan.plan_ata_auto(mloc, n, n, n, params, round_tf32=not f64)
         wsbuf = torch.empty(max(1, plan.ws_scalars), dtype=A.dtype, device=dev) \
             if plan.ws_scalars else None
     else:

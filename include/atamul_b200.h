@@ -69,6 +69,9 @@ extern "C" {
  *   C21 (+)= s2*(P2 + P4)             C22 (+)= s3*(P1 - P2 + P3 + P6)
  * with accumulate selecting += (into C) or = (into a parent's product buffer). */
 #define ATA_OP_POSTADD7 6
+/* ATA_OP_ROUND: d[0] = round-to-nearest TF32 of s[0] (fp32 only; equal extents).
+ * Emitted once per operand by single-pass-TF32 plans before the tcgen05 products. */
+#define ATA_OP_ROUND 7
 #define ATA_MAX_TERMS 4
 #define ATA_MAX_DESTS 8
 

@@ -17,7 +17,8 @@ from . import errors
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libatamul_b200.so"
 
 ATA_F64, ATA_F32, ATA_TF32 = 0, 1, 2
-OP_GEMM, OP_SYRK, OP_COMBO, OP_UPDATE, OP_FILL, OP_COMBO4, OP_POSTADD7 = 0, 1, 2, 3, 4, 5, 6
+OP_GEMM, OP_SYRK, OP_COMBO, OP_UPDATE, OP_FILL, OP_COMBO4, OP_POSTADD7, OP_ROUND = \
+    0, 1, 2, 3, 4, 5, 6, 7
 BASE_A, BASE_C, BASE_WS, BASE_B = 0, 1, 2, 3
 MAX_TERMS, MAX_DESTS = 4, 8
 PROD_MAX_TERMS = 2

@@ -34,11 +34,12 @@ def workspace_for_ata(m: int, n: int, threshold=DEFAULT_THRESHOLD, dtype=np.floa
     return workspace_for_calls(calls, int(threshold), extra_base=base, dtype=dtype)
 
 
-def _plan_for(m, n, lda, ldc, threshold, ws, auto_params=None):
+def _plan_for(m, n, lda, ldc, threshold, ws, auto_params=None, round_tf32=False):
     if threshold == AUTO:
         params = auto_params or auto_plan.AutoParams()
-        key = ("ata-auto", m, n, lda, ldc, params)
-        return engine.cached_plan(key, lambda: auto_plan.plan_ata_auto(m, n, lda, ldc, params))
+        key = ("ata-auto", m, n, lda, ldc, params, round_tf32)
+        return engine.cached_plan(
+            key, lambda: auto_plan.plan_ata_auto(m, n, lda, ldc, params, round_tf32=round_tf32))
     offs = tuple(ws.level_offsets())
     key = ("ata-ref", m, n, lda, ldc, int(threshold), offs)
     return engine.cached_plan(
@@ -65,7 +66,9 @@ def ata(A, C, alpha=1.0, threshold=DEFAULT_THRESHOLD, ws: StrassenWorkspace | No
         ws = workspace_for_ata(m, n, threshold, dtype=C_.t.dtype)
     elif threshold != AUTO:
         check_ata_workspace(ws, m, n, threshold)
-    plan = _plan_for(m, n, A_.ld, C_.ld, threshold, ws, auto_params)
+    import torch
+    plan = _plan_for(m, n, A_.ld, C_.ld, threshold, ws, auto_params,
+                     round_tf32=(precision == "tf32" and C_.t.dtype == torch.float32))
     wbuf = ws.ensure(C_.t.device, extra=plan.ws_scalars if threshold == AUTO else 0) \
         if plan.ws_scalars > 0 else None
     engine.run_plan(plan, nat.dtype_code(C_.t.dtype, precision), A_.ptr, A_.elems, C_.ptr, C_.elems, alpha,

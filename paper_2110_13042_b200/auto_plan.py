@@ -97,6 +97,7 @@ class _AutoPlanner:
         self.pb = PlanBuilder("auto")
         self.ws_top = 0          # bump allocator over the workspace (elements)
         self.ws_peak = 0
+        self.ws_floor = 0        # persistent prefix (the rounded operand copy)
 
     # ---------------------------------------------------------------- workspace
     def alloc(self, rows: int, cols: int) -> Win:
@@ -238,9 +239,19 @@ class _AutoPlanner:
         probe.tree(a, b, m, n, k, Win(nat.BASE_C, 0, max(k, 1), n, k), 1.0, True, depth, [], [])
         return probe.ws_peak
 
-    def ata(self, m: int, n: int, lda: int, ldc: int):
+    def ata(self, m: int, n: int, lda: int, ldc: int, round_tf32: bool = False):
         A = Win(nat.BASE_A, 0, lda, m, n)
         C = Win(nat.BASE_C, 0, ldc, n, n)
+        if round_tf32:
+            # single-pass TF32: products read a TF32-rounded copy of A with a
+            # 128-byte-aligned pitch (TMA-legal), written once by ATA_OP_ROUND
+            ld = -(-n // 32) * 32
+            R = Win(nat.BASE_WS, self.ws_top, ld, m, n)
+            self.ws_top += m * ld
+            self.ws_peak = max(self.ws_peak, self.ws_top)
+            self.pb.round_tf32(A, R)
+            A = R
+            self.ws_floor = self.ws_top
         self.budget = int(self.p.ws_budget_gb * 1e9 / 8)
         level = [(0, n)]
         diag = []
@@ -266,7 +277,7 @@ class _AutoPlanner:
                         self.tree(a, b, a.rows, a.cols, b.cols, c, 1.0, True, self.p.max_depth,
                                   leaves, posts)
                     self.emit(leaves, posts)
-                    self.ws_top = 0
+                    self.ws_top = self.ws_floor
                 else:
                     for (a, b, c) in blocks:
                         self.node(a, b, a.rows, a.cols, b.cols, c, 1.0, True, self.p.max_depth)
@@ -275,12 +286,14 @@ class _AutoPlanner:
                              True) for (c0, w) in sorted(diag)])
 
 
-def plan_ata_auto(m: int, n: int, lda: int, ldc: int, params: AutoParams = AutoParams()) -> Plan:
-    """GPU plan for lower(C) += alpha A^T A (see module docstring)."""
+def plan_ata_auto(m: int, n: int, lda: int, ldc: int, params: AutoParams = AutoParams(),
+                  round_tf32: bool = False) -> Plan:
+    """GPU plan for lower(C) += alpha A^T A (see module docstring).  round_tf32:
+    single-pass TF32 plans (fp32 data, precision="tf32") first round A once."""
     if m < 1 or n < 1:
         raise ShapeMismatchError("shape mismatch: empty operand")
     ap = _AutoPlanner(params)
-    ap.ata(m, n, lda, ldc)
+    ap.ata(m, n, lda, ldc, round_tf32)
     plan = ap.pb.finish()
     plan.ws_scalars = max(plan.ws_scalars, ap.ws_peak)
     return plan

@@ -144,6 +144,11 @@ int validate_op(const ata_op& op, const Bases& b, int i) {
     case ATA_OP_FILL:
       if (op.nd != 1) return fail(ATA_E_ARG, "fill needs 1 dest");
       return ATA_OK;
+    case ATA_OP_ROUND:
+      if (op.ns != 1 || op.nd != 1 || op.s[0].rows != op.d[0].rows || op.s[0].cols != op.d[0].cols)
+        return fail(ATA_E_SHAPE, "shape mismatch: round needs one source and one equal-shape dest");
+      if (b.esize != 4) return fail(ATA_E_ARG, "round: fp32 plans only");
+      return ATA_OK;
     case ATA_OP_POSTADD7:
       if (op.ns != 4 || op.nt != 3 || op.nd != 4)
         return fail(ATA_E_ARG, "postadd7 needs 7 children (s[0..3], t[0..2]) and 4 outputs");
@@ -338,6 +343,11 @@ int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, int* sync, int64_t 
         a.cols = a.cols > op.d[j].cols ? a.cols : op.d[j].cols;
       }
       e = ata::launch_combo4<T>(a, s);
+    } else if (op.type == ATA_OP_ROUND) {
+      const ata::DTerm<T> src = term_of<T>(op.s[0], b);
+      const ata::DDest<T> dst = dest_of<T>(op.d[0], b);
+      e = ata::launch_round_tf32(reinterpret_cast<const float*>(src.p), src.ld, reinterpret_cast<float*>(dst.p),
+                                 dst.ld, dst.rows, dst.cols, s);
     } else if (op.type == ATA_OP_POSTADD7) {
       ata::EwArgs<T> a;
       std::memset(&a, 0, sizeof(a));

@@ -72,6 +72,8 @@ cudaError_t launch_batch_f32(const BatchArgs<float>& a, cudaStream_t s, bool spl
 template <typename T> cudaError_t launch_combo(const EwArgs<T>& a, cudaStream_t s);
 template <typename T> cudaError_t launch_update(const EwArgs<T>& a, cudaStream_t s);
 template <typename T> cudaError_t launch_combo4(const EwArgs<T>& a, cudaStream_t s);
+cudaError_t launch_round_tf32(const float* src, long long lds, float* dst, long long ldd, int rows, int cols,
+                              cudaStream_t s);
 template <typename T> cudaError_t launch_postadd7(const EwArgs<T>& a, int accumulate, cudaStream_t s);
 template <typename T> cudaError_t launch_fill(T* p, long long ld, int rows, int cols, cudaStream_t s);
 template <typename T> cudaError_t launch_mirror(T* C, long long ldc, int n, cudaStream_t s);

@@ -132,6 +132,48 @@ __global__ void postadd7_kernel(const __grid_constant__ EwArgs<T> a, int accumul
   }
 }
 
+// round: dst = round-to-nearest TF32(src) (fp32 storage).  The tcgen05 TF32
+// MMA reads the top 19 bits of each fp32 operand (truncation); rounding the
+// operand once here keeps the products unbiased (|bias| would reach ~7e-4 on
+// the Gram diagonal, above config c5's 1e-4 tolerance).
+__global__ void round_tf32_kernel(const float* __restrict__ src, long long lds, float* __restrict__ dst,
+                                  long long ldd, int rows, int cols) {
+  const int c0 = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (c0 >= cols) return;
+  const bool vec = c0 + 3 < cols && ((reinterpret_cast<uintptr_t>(src) & 15) == 0) && (lds % 4 == 0) &&
+                   ((reinterpret_cast<uintptr_t>(dst) & 15) == 0) && (ldd % 4 == 0);
+  for (int r = blockIdx.y * blockDim.y + threadIdx.y; r < rows; r += gridDim.y * blockDim.y) {
+    const float* s = src + (long long)r * lds + c0;
+    float* d = dst + (long long)r * ldd + c0;
+    if (vec) {
+      float4 v = __ldcs(reinterpret_cast<const float4*>(s));
+      uint32_t x, y, z, w;
+      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(x) : "f"(v.x));
+      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(y) : "f"(v.y));
+      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(z) : "f"(v.z));
+      asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(w) : "f"(v.w));
+      *reinterpret_cast<float4*>(d) =
+          make_float4(__uint_as_float(x), __uint_as_float(y), __uint_as_float(z), __uint_as_float(w));
+    } else {
+      for (int e = 0; e < 4 && c0 + e < cols; ++e) {
+        uint32_t x;
+        asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(x) : "f"(s[e]));
+        d[e] = __uint_as_float(x);
+      }
+    }
+  }
+}
+
+cudaError_t launch_round_tf32(const float* src, long long lds, float* dst, long long ldd, int rows, int cols,
+                              cudaStream_t s) {
+  if (rows <= 0 || cols <= 0) return cudaSuccess;
+  dim3 blk(kEwThreadsX, kEwThreadsY);
+  const int gx = (cols + 4 * kEwThreadsX - 1) / (4 * kEwThreadsX);
+  dim3 grd(gx, ew_grid_y(rows, gx));
+  round_tf32_kernel<<<grd, blk, 0, s>>>(src, lds, dst, ldd, rows, cols);
+  return cudaGetLastError();
+}
+
 // update: for each dest d, D_d[r,c] += sign_d * P[r,c] (r < D_d.rows, c < D_d.cols)
 template <typename T>
 __global__ void update_kernel(const __grid_constant__ EwArgs<T> a) {

@@ -5,6 +5,8 @@
 // reference call sites it replaces.  This is the general-shape f32 path; the
 // tall-skinny SYRK of config c5 goes through the tcgen05 kernel
 // (syrk_tf32_tc.cu) when its shape allows.
+#include <cstdlib>
+
 #include "ata_common.cuh"
 
 namespace ata {
@@ -294,8 +296,33 @@ static cudaError_t launch_batch_f32_t(BatchArgs<float> a, cudaStream_t s) {
   return launch_cfg_f32<2, 2, 3, SPLIT>(a, s);
 }
 
+bool tc_eligible(const DProd<float>& p);
+cudaError_t launch_tf32_tc(const DProd<float>* prods, int count, double alpha, cudaStream_t s);
+
 cudaError_t launch_batch_f32(const BatchArgs<float>& a, cudaStream_t s, bool split) {
-  return split ? launch_batch_f32_t<true>(a, s) : launch_batch_f32_t<false>(a, s);
+  if (split) return launch_batch_f32_t<true>(a, s);
+  // single-pass TF32: plain products go to the tcgen05/TMA kernel, the rest
+  // (fused multi-term / multi-destination products) to the mma.sync kernel
+  static int use_tc = -1;
+  if (use_tc < 0) {
+    const char* e = std::getenv("ATA_TF32_TC");
+    use_tc = e ? std::atoi(e) : 1;
+  }
+  if (!use_tc) return launch_batch_f32_t<false>(a, s);
+  DProd<float> tcp[kMaxBatch];
+  int ntc = 0;
+  BatchArgs<float> rest = a;
+  rest.count = 0;
+  for (int i = 0; i < a.count; ++i) {
+    if (tc_eligible(a.p[i])) tcp[ntc++] = a.p[i];
+    else rest.p[rest.count++] = a.p[i];
+  }
+  if (ntc > 0) {
+    cudaError_t e = launch_tf32_tc(tcp, ntc, a.alpha, s);
+    if (e != cudaSuccess) return e;
+  }
+  if (rest.count > 0) return launch_batch_f32_t<false>(rest, s);
+  return cudaSuccess;
 }
 
 

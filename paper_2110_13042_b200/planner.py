@@ -153,6 +153,10 @@ class PlanBuilder:
         self.launches += 1
         self._last_group = None
 
+    def round_tf32(self, src: Win, dst: Win):
+        """dst = round-to-nearest TF32(src) (ATA_OP_ROUND)."""
+        self._ew(nat.OP_ROUND, [(src, 1.0)], [(dst, 1.0)])
+
     def postadd7(self, children, outputs, accumulate: bool):
         """Strassen post-addition of one node: children = 7 product windows
         (P1..P7), outputs = [(C11 win, sign), (C12..), (C21..), (C22..)]."""

@@ -6,7 +6,7 @@ without a GPU.  Never used by the product path.
 """
 import numpy as np
 
-OP_GEMM, OP_SYRK, OP_COMBO, OP_UPDATE, OP_FILL, OP_COMBO4, OP_POSTADD7 = 0, 1, 2, 3, 4, 5, 6
+OP_GEMM, OP_SYRK, OP_COMBO, OP_UPDATE, OP_FILL, OP_COMBO4, OP_POSTADD7, OP_ROUND = 0, 1, 2, 3, 4, 5, 6, 7
 
 
 def _win(bases, r, write=False):
@@ -67,6 +67,11 @@ def run(ops, A, C, alpha=1.0, WS=None, B=None):
                 w += float(op["d"][j]["sign"]) * src[:w.shape[0], :w.shape[1]]
         elif t == OP_FILL:
             _win(bases, op["d"][0], write=True)[...] = 0
+        elif t == OP_ROUND:   # round-to-nearest (ties away) to TF32, fp32 storage
+            src = _win(bases, op["s"][0]).astype(np.float32)
+            bits = src.view(np.uint32).astype(np.uint64)
+            bits = ((bits + 0x1000) & ~np.uint64(0x1FFF)).astype(np.uint32)
+            _win(bases, op["d"][0], write=True)[...] = bits.view(np.float32)
         elif t == OP_POSTADD7:
             kids = [op["s"][q] for q in range(4)] + [op["t"][q] for q in range(3)]
             wins = [_win(bases, r) for r in kids]

@@ -138,3 +138,69 @@ def test_large_mirror_pack_roundtrip():
     assert torch.equal(pk.data, c[il[0], il[1]])
     P.mirror_lower_to_upper(c)
     assert torch.equal(c, c.T)
+
+
+def _tf32_round(x):
+    b = np.asarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    return (((b + 0x1000) & ~np.uint64(0x1FFF)).astype(np.uint32)).view(np.float32)
+
+
+@pytest.mark.parametrize("tc", ["1", "0"])
+def test_tf32_products_tcgen05_and_legacy(tc, rng, monkeypatch):
+    """Single-pass TF32 plain products through run_plan: the tcgen05/TMA kernel
+    (ATA_TF32_TC=1, default) and the mma.sync kernel agree with an fp64 product
+    of the TF32-rounded operands (GEMM and SYRK kinds, ragged edges)."""
+    import subprocess, sys, json, os
+    code = r'''
+import sys, json, numpy as np, torch
+sys.path.insert(0, "%s")
+from paper_2110_13042_b200 import planner, engine, _native as nat
+rng = np.random.default_rng(11)
+out = {}
+for (m, n, k) in [(3000, 300, 520), (777, 129, 257), (4096, 1024, 1024)]:
+    a = rng.standard_normal((m, n)).astype(np.float32); b = rng.standard_normal((m, k)).astype(np.float32)
+    ar = a.view(np.uint32).astype(np.uint64); ar = (((ar + 0x1000) & ~np.uint64(0x1FFF)).astype(np.uint32)).view(np.float32)
+    br = b.view(np.uint32).astype(np.uint64); br = (((br + 0x1000) & ~np.uint64(0x1FFF)).astype(np.uint32)).view(np.float32)
+    A = torch.from_numpy(ar).cuda(); B = torch.from_numpy(br).cuda()
+    pb = planner.PlanBuilder("t")
+    C = torch.zeros(n, k, device="cuda")
+    pb.product("gemm", m, n, k, [(planner.Win(0, 0, n, m, n), 1.0)], [(planner.Win(3, 0, k, m, k), 1.0)],
+               [(planner.Win(1, 0, k, n, k), 1.0)], accumulate=0, group=1)
+    engine.run_plan(pb.finish(), nat.ATA_TF32, A.data_ptr(), A.numel(), C.data_ptr(), C.numel(), 1.0,
+                    B=B.data_ptr(), b_elems=B.numel())
+    ref = ar.astype(np.float64).T @ br.astype(np.float64)
+    g = np.linalg.norm(C.cpu().numpy() - ref) / np.linalg.norm(ref)
+    pb = planner.PlanBuilder("t")
+    S = torch.full((n, n), 3.0, device="cuda")
+    pb.product("syrk", m, n, n, [(planner.Win(0, 0, n, m, n), 1.0)], [], [(planner.Win(1, 0, n, n, n), -1.0)],
+               accumulate=1, group=1)
+    engine.run_plan(pb.finish(), nat.ATA_TF32, A.data_ptr(), A.numel(), S.data_ptr(), S.numel(), 2.0)
+    s = S.cpu().numpy(); refs = 3.0 - 2.0 * (ar.astype(np.float64).T @ ar.astype(np.float64))
+    il = np.tril_indices(n)
+    e = np.linalg.norm(s[il] - refs[il]) / np.linalg.norm(refs[il])
+    up = bool(np.all(s[np.triu_indices(n, 1)] == 3.0))
+    out[f"{m}x{n}x{k}"] = [g, e, up]
+print(json.dumps(out))
+''' % os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, ATA_TF32_TC=tc)
+    r = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env, timeout=300)
+    assert r.returncode == 0, r.stderr[-3000:]
+    res = json.loads(r.stdout.strip().splitlines()[-1])
+    for key, (g, e, up) in res.items():
+        assert g <= 5e-5, (key, g)     # fp32 accumulation of TF32 products
+        assert e <= 5e-5, (key, e)
+        assert up, key
+
+
+def test_ata_tf32_tall_skinny():
+    """Config-c5-shaped (scaled) single-pass TF32 AtA: rel-Frobenius <= 1e-4
+    against the fp64 Gram of the fp32 input (the c5 tolerance)."""
+    import torch
+    import paper_2110_13042_b200 as P
+    a = np.random.default_rng(4).standard_normal((200000, 640)).astype(np.float32)
+    A = torch.from_numpy(a).cuda()
+    C = torch.zeros(640, 640, dtype=torch.float32, device="cuda")
+    P.ata(A, C, 1.0, threshold="auto", precision="tf32")
+    got = C.cpu().numpy()
+    assert np.all(np.triu(got, 1) == 0)
+    assert O.rel_frobenius_lower(got, O.gram_blas(a)) <= 1e-4

@@ -160,3 +160,19 @@ def test_auto_plan_groups_write_disjoint():
                     # a shared cell must belong to the same ordered region in both ops
                     assert region > 0 and seen[cell] == region, f"group {g}: unordered overlap"
                 seen[cell] = region
+
+
+def test_auto_plan_tf32_round_and_split_contraction():
+    """Single-pass-TF32 plans round A once into the workspace and split the
+    contraction of tall-skinny groups; checked through the interpreter."""
+    m, n = 6000, 96
+    a = np.random.default_rng(3).standard_normal((m, n)).astype(np.float32)
+    p = auto_plan.plan_ata_auto(m, n, n, n, auto_plan.AutoParams(leaf_cols=32, min_chunk=512),
+                                round_tf32=True)
+    types = [int(o["type"]) for o in p.ops]
+    assert types[0] == 7 and 5 in types          # ROUND first, combo4 partial sums present
+    c = np.zeros((n, n), dtype=np.float32)
+    c[np.triu_indices(n, 1)] = 5.0
+    plan_interp.run(p.ops, a, c, 1.0, WS=np.full(max(1, p.ws_scalars), np.nan, dtype=np.float32))
+    assert np.all(c[np.triu_indices(n, 1)] == 5.0)
+    assert O.rel_frobenius_lower(c, O.gram_blas(a)) <= 1e-4
