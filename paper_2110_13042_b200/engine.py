@@ -77,3 +77,26 @@ def run_plan(plan, dtype_code, A, a_elems, C, c_elems, alpha, ws=None, ws_elems=
                           C, c_elems, ws or 0, ws_elems, int(sync.data_ptr()), int(sync.numel()),
                           float(alpha), stream)
     nat.check(rc)
+
+
+class PlanGraph:
+    """One plan execution with fixed pointers captured as a CUDA graph.
+
+    Reference-faithful plans with small leaves issue thousands of launches
+    (config c2 at t = 256^2: ~8000); replaying a captured graph removes the
+    host-side launch cost.  The caller must have run the plan once eagerly
+    (function attributes, sync buffer) before constructing the graph."""
+
+    def __init__(self, plan, dtype_code, A, a_elems, C, c_elems, alpha, ws=None, ws_elems=0,
+                 B=None, b_elems=0):
+        import torch
+        self.graph = torch.cuda.CUDAGraph()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.graph(self.graph, stream=side):
+            run_plan(plan, dtype_code, A, a_elems, C, c_elems, alpha, ws=ws, ws_elems=ws_elems,
+                     B=B, b_elems=b_elems, stream=int(side.cuda_stream))
+        torch.cuda.current_stream().wait_stream(side)
+
+    def replay(self):
+        self.graph.replay()
