@@ -204,11 +204,16 @@ def main():
         run_reference(args, world, rank)
         return
     import torch
+    local = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("ATA_DIST_BACKEND", "nccl")   # gloo: shared-GPU path checks
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
     import paper_2110_13042_b200 as P
     from paper_2110_13042_b200 import _native as nat, auto_plan, dist as pdist, engine, planner
     from paper_2110_13042_b200.measure import CONFIGS

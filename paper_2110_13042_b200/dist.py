@@ -35,6 +35,12 @@ def uniform_rows(m: int, n: int, seed: int, r0: int, r1: int, dtype=np.float64):
 def reduce_packed(packed, root: int = 0, group=None):
     """Sum packed lower triangles of every rank into `packed` on `root`."""
     import torch.distributed as dist
+    if packed.is_cuda and dist.get_backend(group) == "gloo":
+        # host-staged reduction for the gloo backend (CPU tests, shared-GPU checks)
+        host = packed.cpu()
+        dist.reduce(host, dst=root, op=dist.ReduceOp.SUM, group=group)
+        packed.copy_(host)
+        return packed
     dist.reduce(packed, dst=root, op=dist.ReduceOp.SUM, group=group)
     return packed
 
