@@ -60,7 +60,7 @@ def ata(A, C, alpha=1.0, threshold=DEFAULT_THRESHOLD, ws: StrassenWorkspace | No
         threshold = int(threshold)
         if threshold < 1:
             raise ShapeMismatchError("shape mismatch: threshold must be >= 1")
-    C_ = DeviceOperand(c, writable=True)
+    C_ = DeviceOperand(c, writable=True, lower=True)   # kernels touch only lower(C)
     A_ = DeviceOperand(a, dtype=C_.t.dtype, device=C_.t.device)
     if ws is None:
         ws = workspace_for_ata(m, n, threshold, dtype=C_.t.dtype)
