@@ -24,7 +24,8 @@ Shape of the plan (all windows into A, C and one HBM workspace):
        write updates per node (strassen.py:238-275) and is executed bottom-up.
    Quadrant splits are ceil-first (first half = ceil, the trailing half is
    the zero-extended one), so every node of a level has identical shapes.
-3. Diagonal leaves are SYRK-lower products, one group.
+3. Diagonal leaves are SYRK-lower products; they join the first breadth-
+   first leaf group (they read only A), else form the last group.
 The Strassen trees of one AtA level are planned breadth-first (one leaf group)
 when their workspace fits ``ws_budget_gb``; otherwise depth-first over each
 block's top-level children (one leaf group per subtree).
@@ -66,10 +67,13 @@ class AutoParams:
     ws_budget_gb: float = 40.0     # workspace for breadth-first planning of one AtA level
     fill_waves: int = 2            # split the contraction of groups with fewer tiles than this
     min_chunk: int = 8192          # ... into chunks of at least this many rows
+    tf32_tflops: float = 400.0     # single-pass TF32 leaf-product rate (tcgen05, profiles/)
+    tf32_fill_waves: int = 8       # 128x256 tcgen05 tiles: more chunks to fill 148 SMs
 
 
 TILE = 128        # output tile of the product kernels
 NUM_SMS = 148     # B200
+MAX_BATCH = 48    # products per persistent launch (kMaxBatch, ata_common.cuh)
 
 
 def _ceil2(d: int) -> int:
@@ -98,6 +102,10 @@ class _AutoPlanner:
         self.ws_top = 0          # bump allocator over the workspace (elements)
         self.ws_peak = 0
         self.ws_floor = 0        # persistent prefix (the rounded operand copy)
+        self.rate = params.dmma_tflops
+        self.esize = 8
+        self.fill_waves = params.fill_waves
+        self.tile = (TILE, TILE)
 
     # ---------------------------------------------------------------- workspace
     def alloc(self, rows: int, cols: int) -> Win:
@@ -110,10 +118,10 @@ class _AutoPlanner:
     def worth_split(self, m: int, n: int, k: int, depth_left: int) -> bool:
         if depth_left <= 0 or min(n, k) < 2 * self.p.min_dim or m < 2:
             return False
-        saved_s = 2.0 * m * n * k / 8 / (self.p.dmma_tflops * 1e12)
+        saved_s = 2.0 * m * n * k / 8 / (self.rate * 1e12)
         # pre: read both operands, write 5 + 5 quarter sums; post: write 7 child
         # products (leaf epilogue), read them back, write (or RMW) 4 quadrants
-        moved = 8.0 * (m * n * (1 + 5 / 4) + m * k * (1 + 5 / 4) + n * k * (7 / 4 + 7 / 4 + 2))
+        moved = self.esize * (m * n * (1 + 5 / 4) + m * k * (1 + 5 / 4) + n * k * (7 / 4 + 7 / 4 + 2))
         added_s = moved / (self.p.hbm_gbs * 1e9)
         return saved_s > self.p.gain * added_s
 
@@ -149,8 +157,8 @@ class _AutoPlanner:
             self.tree(S[i], T[i], m1, n1, k1, kids[i], 1.0, False, depth - 1, leaves, posts)
         posts.append((kids, out, sign, n1, k1, accumulate))
 
-    def emit(self, leaves, posts):
-        prods = []
+    def emit(self, leaves, posts, extra=()):
+        prods = list(extra)
         for (m, n, k, a, b, out, sign, accumulate) in leaves:
             if a.rows == 0 or a.cols == 0 or b.rows == 0 or b.cols == 0:
                 if not accumulate:            # an all-zero operand: the product buffer is zero
@@ -161,10 +169,39 @@ class _AutoPlanner:
         for (kids, out, sign, n1, k1, accumulate) in posts:
             self._post(kids, out, sign, n1, k1, accumulate)
 
-    @staticmethod
-    def _tiles(kind, n, k):
-        t = -(-n // TILE)
-        return t * (t + 1) // 2 if kind == "syrk" else t * -(-k // TILE)
+    def _tiles(self, kind, n, k):
+        """Output tiles of one product on the leaf kernel this plan runs on
+        (FP64: 128x128 tiles; single-pass TF32: 128x256 tcgen05 tiles, SYRK
+        strips enumerate only the column tiles touching the lower triangle)."""
+        bm, bn = self.tile
+        tn, tk = -(-n // bm), -(-k // bn)
+        if kind != "syrk":
+            return tn * tk
+        return sum(min(tk, (ti * bm + bm - 1) // bn + 1) for ti in range(tn))
+
+    def _chunks(self, tiles: int, rows: int, nprods: int = 1) -> int:
+        """Contraction split S for a group of `tiles` output tiles: at least
+        fill_waves waves, then the smallest S (up to 3x that) whose tile count fills >= 97% of
+        whole waves of the persistent grid, else the best-filling one (rows/S >= min_chunk)."""
+        target = self.fill_waves * NUM_SMS
+        if tiles >= target:
+            return 1
+        # one persistent launch per group: at most MAX_BATCH products
+        s_hi = min(rows // self.p.min_chunk, max(1, MAX_BATCH // nprods))
+        s_lo = -(-target // tiles)
+        if s_hi <= 1:
+            return 1
+        if s_lo >= s_hi:
+            return s_hi
+        best, best_eff = s_lo, -1.0
+        for S in range(s_lo, min(3 * s_lo, s_hi) + 1):
+            t = tiles * S
+            eff = t / (NUM_SMS * -(-t // NUM_SMS))
+            if eff >= 0.97:
+                return S
+            if eff > best_eff + 1e-9:
+                best, best_eff = S, eff
+        return best
 
     def emit_products(self, prods):
         """One launch group.  When the group's output tiles cannot fill the GPU
@@ -175,10 +212,7 @@ class _AutoPlanner:
         if not prods:
             return
         tiles = sum(self._tiles(p[0], p[2], p[3]) for p in prods)
-        target = self.p.fill_waves * NUM_SMS
-        S = 1
-        if tiles < target:
-            S = min(-(-target // tiles), min(p[1] for p in prods) // self.p.min_chunk)
+        S = self._chunks(tiles, min(p[1] for p in prods), len(prods))
         group = self.pb.new_group()
         if S <= 1:
             for (kind, m, n, k, a, b, out, sign, accumulate) in prods:
@@ -236,6 +270,7 @@ class _AutoPlanner:
 
     def _dry_ws(self, a, b, m, n, k, depth) -> int:
         probe = _AutoPlanner(self.p)
+        probe.rate, probe.esize = self.rate, self.esize
         probe.tree(a, b, m, n, k, Win(nat.BASE_C, 0, max(k, 1), n, k), 1.0, True, depth, [], [])
         return probe.ws_peak
 
@@ -243,6 +278,8 @@ class _AutoPlanner:
         A = Win(nat.BASE_A, 0, lda, m, n)
         C = Win(nat.BASE_C, 0, ldc, n, n)
         if round_tf32:
+            self.rate, self.esize, self.fill_waves = self.p.tf32_tflops, 4, self.p.tf32_fill_waves
+            self.tile = (128, 256)
             # single-pass TF32: products read a TF32-rounded copy of A with a
             # 128-byte-aligned pitch (TMA-legal), written once by ATA_OP_ROUND
             ld = -(-n // 32) * 32
@@ -253,13 +290,24 @@ class _AutoPlanner:
             A = R
             self.ws_floor = self.ws_top
         self.budget = int(self.p.ws_budget_gb * 1e9 / 8)
+        # the diagonal SYRK leaves depend only on A: they join the first
+        # breadth-first leaf group (more tiles per launch), else run last
+        diag, level = [], [(0, n)]
+        while level:
+            nxt = []
+            for (c0, w) in level:
+                if w <= self.p.leaf_cols or w < 2:
+                    diag.append((c0, w))
+                else:
+                    nxt += [(c0, w // 2), (c0 + w // 2, w - w // 2)]
+            level = nxt
+        diag_prods = [("syrk", m, w, w, A.sub(0, c0, m, w), None, C.sub(c0, c0, w, w), 1.0, True)
+                      for (c0, w) in sorted(diag)]
         level = [(0, n)]
-        diag = []
         while level:
             blocks, nxt = [], []
             for (c0, w) in level:
                 if w <= self.p.leaf_cols or w < 2:
-                    diag.append((c0, w))
                     continue
                 n1 = w // 2
                 n2 = w - n1
@@ -276,14 +324,14 @@ class _AutoPlanner:
                     for (a, b, c) in blocks:
                         self.tree(a, b, a.rows, a.cols, b.cols, c, 1.0, True, self.p.max_depth,
                                   leaves, posts)
-                    self.emit(leaves, posts)
+                    self.emit(leaves, posts, diag_prods)
+                    diag_prods = []
                     self.ws_top = self.ws_floor
                 else:
                     for (a, b, c) in blocks:
                         self.node(a, b, a.rows, a.cols, b.cols, c, 1.0, True, self.p.max_depth)
             level = nxt
-        self.emit_products([("syrk", m, w, w, A.sub(0, c0, m, w), None, C.sub(c0, c0, w, w), 1.0,
-                             True) for (c0, w) in sorted(diag)])
+        self.emit_products(diag_prods)
 
 
 def plan_ata_auto(m: int, n: int, lda: int, ldc: int, params: AutoParams = AutoParams(),

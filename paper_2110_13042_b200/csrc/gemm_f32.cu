@@ -298,6 +298,7 @@ static cudaError_t launch_batch_f32_t(BatchArgs<float> a, cudaStream_t s) {
 
 bool tc_eligible(const DProd<float>& p);
 cudaError_t launch_tf32_tc(const DProd<float>* prods, int count, double alpha, cudaStream_t s);
+cudaError_t launch_tf32_2sm(const DProd<float>* prods, int count, double alpha, cudaStream_t s);
 
 cudaError_t launch_batch_f32(const BatchArgs<float>& a, cudaStream_t s, bool split) {
   if (split) return launch_batch_f32_t<true>(a, s);
@@ -318,7 +319,8 @@ cudaError_t launch_batch_f32(const BatchArgs<float>& a, cudaStream_t s, bool spl
     else rest.p[rest.count++] = a.p[i];
   }
   if (ntc > 0) {
-    cudaError_t e = launch_tf32_tc(tcp, ntc, a.alpha, s);
+    // 2 = CTA-pair tcgen05 kernel (cta_group::2), 1 = single-CTA tcgen05 kernel
+    cudaError_t e = use_tc == 2 ? launch_tf32_2sm(tcp, ntc, a.alpha, s) : launch_tf32_tc(tcp, ntc, a.alpha, s);
     if (e != cudaSuccess) return e;
   }
   if (rest.count > 0) return launch_batch_f32_t<false>(rest, s);

@@ -1,0 +1,397 @@
+// TF32 product kernel, CTA-pair version (sm_100a): tcgen05.mma.cta_group::2
+// (M = 256 across the two SMs of a cluster, N = 256), TMA 2SM loads, TMEM
+// accumulators in both CTAs.  Same products as gemm_tf32_tc.cu (single-term
+// operands, one destination, SYRK lower tiles); the pair halves the L2->SM
+// operand traffic per flop (each CTA stages 128 rows of A and 128 columns of B
+// per k-block: 32 KB per 2 x 128x256x32 MACs instead of 48 KB), which is what
+// bounds the single-CTA kernel on the tall-skinny config c5 (~11.6 TB/s of
+// L2->SM traffic measured).
+//
+// Roles per CTA (192 threads): warp 0 TMA producer (both CTAs load their halves,
+// completion counted on the leader's barrier), warp 1 TMEM allocation (both
+// CTAs, cta_group::2) + MMA issue (leader only), warps 2-5 epilogue (each CTA
+// drains its own 128 accumulator rows).  Every wait is bounded: a protocol
+// error traps instead of hanging the GPU.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstdlib>
+#include <cstring>
+
+#include "ata_common.cuh"
+
+namespace ata {
+
+namespace tc2 {
+constexpr int BM = 256, BN = 256, BK = 32, STAGES = 6;   // per pair
+constexpr int HALF = 128;                                 // rows of A / cols of B per CTA
+constexpr int A_BYTES = BK * HALF * 4;                    // 16 KB
+constexpr int B_BYTES = BK * HALF * 4;                    // 16 KB
+constexpr int STAGE_BYTES = A_BYTES + B_BYTES;            // 32 KB per CTA
+constexpr int THREADS = 192;
+constexpr int TMEM_COLS = 512;
+constexpr int kMax = 48;   // = kMaxBatch: one launch per plan group (15 KB of kernel parameters)
+constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (1u << 16) |
+                           (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
+}  // namespace tc2
+
+struct alignas(64) Tc2Prod {
+  CUtensorMap ts;
+  CUtensorMap tt;
+  float* d;
+  long long ld;
+  int drows, dcols;
+  float scale;
+  int kind, m, n, k;
+  int tn, tk, tile_begin, accumulate;
+};
+
+struct Tc2Args {
+  Tc2Prod p[tc2::kMax];
+  int count;
+  int total_tiles;
+};
+static_assert(sizeof(Tc2Args) <= 32000, "kernel parameter space (CUDA 12.1+: 32 KB)");
+
+
+__device__ __forceinline__ uint32_t t2_smem(const void* p) { return smem_u32(p); }
+__device__ __forceinline__ uint64_t t2_now() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+__device__ __forceinline__ void t2_wait(uint64_t* bar, unsigned parity) {
+  uint32_t ok;
+  asm volatile(
+      "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(ok)
+      : "r"(t2_smem(bar)), "r"(parity)
+      : "memory");
+  if (ok) return;
+  const uint64_t t0 = t2_now();
+  while (true) {
+    asm volatile(
+        "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(ok)
+        : "r"(t2_smem(bar)), "r"(parity)
+        : "memory");
+    if (ok) return;
+    if (t2_now() - t0 > 10000000000ull) __trap();  // 10 s: protocol error, fail loudly
+  }
+}
+__device__ __forceinline__ uint32_t t2_rank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+__device__ __forceinline__ uint32_t t2_map(uint32_t saddr, uint32_t rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+  return r;
+}
+__device__ __forceinline__ void t2_cluster_sync() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\nbarrier.cluster.wait.acquire.aligned;\n" ::: "memory");
+}
+__device__ __forceinline__ uint64_t t2_desc(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+  d |= (uint64_t)((4096 >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((512 >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)1 << 61;  // SWIZZLE_128B_BASE32B (MN-major 32-bit)
+  return d;
+}
+
+struct Tc2Tile {
+  int pi, ti, tj;
+};
+
+__device__ __forceinline__ Tc2Tile t2_decode(const Tc2Args& a, int tile) {
+  int pi = 0;
+  while (pi + 1 < a.count && tile >= a.p[pi + 1].tile_begin) ++pi;
+  const Tc2Prod& P = a.p[pi];
+  const int local = tile - P.tile_begin;
+  Tc2Tile t;
+  t.pi = pi;
+  if (P.kind == kSyrk) {  // square 256-tiles, lower triangle, row by row
+    int r = (int)((sqrt(8.0 * (double)local + 1.0) - 1.0) * 0.5);
+    while ((r + 1) * (r + 2) / 2 <= local) ++r;
+    while (r * (r + 1) / 2 > local) --r;
+    t.ti = r;
+    t.tj = local - r * (r + 1) / 2;
+  } else {
+    const int per_group = 8 * P.tk;
+    const int grp = local / per_group;
+    const int first = grp * 8;
+    const int gsz = min(P.tn - first, 8);
+    const int in = local - grp * per_group;
+    t.ti = first + in % gsz;
+    t.tj = in / gsz;
+  }
+  return t;
+}
+
+__global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
+    prod_tf32_2sm_kernel(const __grid_constant__ Tc2Args args) {
+  using namespace tc2;
+  extern __shared__ uint8_t t2_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(t2_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + 2;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t rank = t2_rank();
+  const bool leader = rank == 0;
+  const int cluster = blockIdx.x >> 1, nclusters = gridDim.x >> 1;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(t2_smem(&full[s])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(t2_smem(&empty[s])));
+    }
+    for (int b = 0; b < 2; ++b) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(t2_smem(&tfull[b])));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 8;" ::"r"(t2_smem(&tempty[b])));
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(t2_smem(tmem_slot)),
+                 "n"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  t2_cluster_sync();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    // ================= TMA producer (both CTAs) =================
+    if (lane == 0) {
+      int ks = 0;
+      for (int tile = cluster; tile < args.total_tiles; tile += nclusters) {
+        const Tc2Tile t = t2_decode(args, tile);
+        const Tc2Prod& P = args.p[t.pi];
+        const CUtensorMap* mt = P.kind == kSyrk ? &P.ts : &P.tt;
+        const int i0 = t.ti * BM + rank * HALF, j0 = t.tj * BN + rank * HALF;
+        const int KT = (P.m + BK - 1) / BK;
+        for (int kb = 0; kb < KT; ++kb, ++ks) {
+          const int s = ks % STAGES;
+          t2_wait(&empty[s], ((ks / STAGES) & 1) ^ 1);
+          uint8_t* sa = smem + s * STAGE_BYTES;
+          uint8_t* sb = sa + A_BYTES;
+          const uint32_t bar = t2_smem(&full[s]) & 0xFEFFFFFFu;  // the leader's barrier
+          if (leader)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(t2_smem(&full[s])),
+                         "r"(2 * STAGE_BYTES)
+                         : "memory");
+#pragma unroll
+          for (int g = 0; g < HALF / 32; ++g)
+            asm volatile(
+                "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%3, %4}], [%2];" ::"r"(t2_smem(sa + g * 4096)),
+                "l"(reinterpret_cast<uint64_t>(&P.ts)), "r"(bar), "r"(i0 + g * 32), "r"(kb * BK)
+                : "memory");
+#pragma unroll
+          for (int g = 0; g < HALF / 32; ++g)
+            asm volatile(
+                "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%3, %4}], [%2];" ::"r"(t2_smem(sb + g * 4096)),
+                "l"(reinterpret_cast<uint64_t>(mt)), "r"(bar), "r"(j0 + g * 32), "r"(kb * BK)
+                : "memory");
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ================= MMA issuer (leader CTA only) =================
+    if (leader) {
+      int ks = 0, it = 0;
+      for (int tile = cluster; tile < args.total_tiles; tile += nclusters, ++it) {
+        const Tc2Tile t = t2_decode(args, tile);
+        const Tc2Prod& P = args.p[t.pi];
+        const int KT = (P.m + BK - 1) / BK;
+        const int buf = it & 1;
+        t2_wait(&tempty[buf], ((it >> 1) & 1) ^ 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t dt = tmem + buf * BN;
+        for (int kb = 0; kb < KT; ++kb, ++ks) {
+          const int s = ks % STAGES;
+          t2_wait(&full[s], (ks / STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          if (lane == 0) {
+            const uint32_t sa = t2_smem(smem + s * STAGE_BYTES);
+            const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+            for (int kk = 0; kk < BK / 8; ++kk)
+              asm volatile(
+                  "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+                  "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(dt),
+                  "l"(t2_desc(sa + kk * 1024)), "l"(t2_desc(sb + kk * 1024)), "r"(IDESC),
+                  "r"((uint32_t)((kb | kk) != 0)));
+            asm volatile(
+                "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], "
+                "%1;" ::"r"(t2_smem(&empty[s])),
+                "h"((uint16_t)3)
+                : "memory");
+            if (kb == KT - 1)
+              asm volatile(
+                  "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], "
+                  "%1;" ::"r"(t2_smem(&tfull[buf])),
+                  "h"((uint16_t)3)
+                  : "memory");
+          }
+          __syncwarp();
+        }
+      }
+    }
+  } else {
+    // ================= epilogue (warps 2..5, both CTAs) =================
+    const int q = warp & 3;
+    const uint32_t leader_tempty0 = t2_map(t2_smem(&tempty[0]), 0);
+    const uint32_t leader_tempty1 = t2_map(t2_smem(&tempty[1]), 0);
+    int it = 0;
+    for (int tile = cluster; tile < args.total_tiles; tile += nclusters, ++it) {
+      const Tc2Tile t = t2_decode(args, tile);
+      const Tc2Prod& P = args.p[t.pi];
+      const int buf = it & 1;
+      t2_wait(&tfull[buf], (it >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const int row = t.ti * BM + rank * HALF + q * 32 + lane;
+      const bool syrk = P.kind == kSyrk;
+      float* drow = P.d + (long long)row * P.ld;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t v[32];
+        const uint32_t addr = tmem + ((uint32_t)(q * 32) << 16) + buf * BN + c * 32;
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,"
+            "%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+              "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+              "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+              "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+            : "r"(addr));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        if (row < P.drows) {
+          const int col0 = t.tj * BN + c * 32;
+          int cmax = P.dcols - col0;
+          if (syrk) cmax = min(cmax, row - col0 + 1);
+          if (cmax > 32) cmax = 32;
+          if (cmax > 0) {
+            float* dp = drow + col0;
+            if (cmax == 32 && ((reinterpret_cast<uintptr_t>(dp) & 15) == 0)) {
+#pragma unroll
+              for (int e = 0; e < 32; e += 4) {
+                float4 o = make_float4(P.scale * __uint_as_float(v[e]), P.scale * __uint_as_float(v[e + 1]),
+                                       P.scale * __uint_as_float(v[e + 2]), P.scale * __uint_as_float(v[e + 3]));
+                if (P.accumulate) {
+                  const float4 old = *reinterpret_cast<const float4*>(dp + e);
+                  o.x += old.x;
+                  o.y += old.y;
+                  o.z += old.z;
+                  o.w += old.w;
+                }
+                *reinterpret_cast<float4*>(dp + e) = o;
+              }
+            } else {
+#pragma unroll
+              for (int e = 0; e < 32; ++e) {
+                if (e < cmax) {
+                  const float o = P.scale * __uint_as_float(v[e]);
+                  dp[e] = P.accumulate ? dp[e] + o : o;
+                }
+              }
+            }
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0)
+        asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(buf ? leader_tempty1 : leader_tempty0)
+                     : "memory");
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  t2_cluster_sync();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(TMEM_COLS));
+  }
+}
+
+// ---------------------------------------------------------------- host side
+static bool t2_map_term(CUtensorMap* map, const DTerm<float>& t) {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (enc == nullptr) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return false;
+    enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)t.cols, (cuuint64_t)t.rows};
+  cuuint64_t strides[1] = {(cuuint64_t)t.ld * 4};
+  cuuint32_t box[2] = {32, 32};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(t.p), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+cudaError_t launch_tf32_2sm(const DProd<float>* prods, int count, double alpha, cudaStream_t s) {
+  using namespace tc2;
+  static int sms = 0;
+  if (sms == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  const size_t smem = (size_t)STAGES * STAGE_BYTES + 1024 + 256;
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(prod_tf32_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  for (int base = 0; base < count; base += kMax) {
+    Tc2Args a;
+    std::memset(&a, 0, sizeof(a));
+    long long total = 0;
+    const int n = count - base < kMax ? count - base : kMax;
+    for (int i = 0; i < n; ++i) {
+      const DProd<float>& p = prods[base + i];
+      Tc2Prod& q = a.p[i];
+      if (!t2_map_term(&q.ts, p.s[0])) return cudaErrorInvalidValue;
+      if (p.kind != kSyrk && !t2_map_term(&q.tt, p.t[0])) return cudaErrorInvalidValue;
+      q.d = p.d[0].p;
+      q.ld = p.d[0].ld;
+      q.drows = p.d[0].rows;
+      q.dcols = p.d[0].cols;
+      q.scale = (float)(alpha * p.d[0].sign);
+      q.kind = p.kind;
+      q.m = p.m;
+      q.n = p.n;
+      q.k = p.k;
+      q.accumulate = p.accumulate;
+      q.tn = (p.n + BM - 1) / BM;
+      q.tk = (p.k + BN - 1) / BN;
+      q.tile_begin = (int)total;
+      total += p.kind == kSyrk ? (long long)q.tn * (q.tn + 1) / 2 : (long long)q.tn * q.tk;
+    }
+    a.count = n;
+    a.total_tiles = (int)total;
+    if (total == 0) continue;
+    const int clusters = (int)(total < sms / 2 ? total : sms / 2);
+    prod_tf32_2sm_kernel<<<clusters * 2, THREADS, smem, s>>>(a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace ata

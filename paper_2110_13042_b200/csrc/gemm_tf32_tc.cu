@@ -37,7 +37,7 @@ constexpr int B_BYTES = BK * BN * 4;           // 32 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int THREADS = 192;
 constexpr int TMEM_COLS = 512;
-constexpr int kMax = 16;
+constexpr int kMax = 48;   // = kMaxBatch: one launch per plan group (15 KB of kernel parameters)
 // instruction descriptor: D f32, A/B tf32, both MN-major, N = 256, M = 128
 constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (1u << 16) |
                            (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
@@ -60,6 +60,8 @@ struct TcArgs {
   int total_tiles;
   float* dbg;  // debug dump (ATA_TC_DEBUG): stage-0 smem of the first k-block
 };
+static_assert(sizeof(TcArgs) <= 32000, "kernel parameter space (CUDA 12.1+: 32 KB)");
+
 
 __device__ __forceinline__ uint32_t tc_smem(const void* p) { return smem_u32(p); }
 

@@ -145,7 +145,7 @@ def _tf32_round(x):
     return (((b + 0x1000) & ~np.uint64(0x1FFF)).astype(np.uint32)).view(np.float32)
 
 
-@pytest.mark.parametrize("tc", ["1", "0"])
+@pytest.mark.parametrize("tc", ["2", "1", "0"])
 def test_tf32_products_tcgen05_and_legacy(tc, rng, monkeypatch):
     """Single-pass TF32 plain products through run_plan: the tcgen05/TMA kernel
     (ATA_TF32_TC=1, default) and the mma.sync kernel agree with an fp64 product
