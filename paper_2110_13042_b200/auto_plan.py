@@ -220,15 +220,16 @@ class _AutoPlanner:
                 self.pb.product(kind, m, n, k, [(a, 1.0)], T, [(out, sign)],
                                 accumulate=int(accumulate), group=group)
             return
-        reductions = []
-        for (kind, m, n, k, a, b, out, sign, accumulate) in prods:
-            mc = -(-m // S)
-            parts = []
-            for c in range(S):
+        # chunk-major order: the products of one row chunk are adjacent, so a
+        # wave of the persistent grid runs whole chunks (periodic_workers)
+        parts = [[] for _ in prods]
+        for c in range(S):
+            for pi, (kind, m, n, k, a, b, out, sign, accumulate) in enumerate(prods):
+                mc = -(-m // S)
                 r0 = c * mc
                 rows = min(mc, m - r0)
                 if rows <= 0:
-                    break
+                    continue
                 ac = _clip(a, r0, 0, rows, a.cols)
                 bc = ac if b is None else _clip(b, r0, 0, rows, b.cols)
                 if ac.rows == 0 or bc.rows == 0:
@@ -237,8 +238,9 @@ class _AutoPlanner:
                 T = [] if kind == "syrk" else [(bc, 1.0)]
                 self.pb.product(kind, rows, n, k, [(ac, 1.0)], T, [(P, 1.0)], accumulate=0,
                                 group=group)
-                parts.append(P)
-            reductions.append((kind, out, sign, accumulate, parts))
+                parts[pi].append(P)
+        reductions = [(kind, out, sign, accumulate, parts[pi])
+                      for pi, (kind, m, n, k, a, b, out, sign, accumulate) in enumerate(prods)]
         for (kind, out, sign, accumulate, parts) in reductions:
             srcs = list(parts)
             first = True

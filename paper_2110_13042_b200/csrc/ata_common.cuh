@@ -100,4 +100,26 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N));
 }
 
+// Persistent grid size for a static round-robin tile schedule.  When the
+// launch's products repeat with a period of P tiles (a contraction split into
+// row chunks, each chunk = the same products over new rows) and P fits the
+// machine, use a multiple of P workers so every wave runs whole chunks: the
+// tiles sharing a chunk's operand panels then stream them in lockstep and the
+// panels are read from HBM once (a chunk split across waves is read twice).
+inline int periodic_workers(const int* tiles, const int* kinds, int n, long long total, int slots) {
+  if (total <= slots) return (int)total;
+  for (int q = 1; q <= n / 2; ++q) {
+    if (n % q != 0) continue;
+    bool same = true;
+    for (int i = q; i < n && same; ++i) same = tiles[i] == tiles[i - q] && kinds[i] == kinds[i - q];
+    if (!same) continue;
+    long long period = 0;
+    for (int i = 0; i < q; ++i) period += tiles[i];
+    if (period > slots) break;
+    const long long w = (slots / period) * period;
+    return w * 10 >= (long long)slots * 9 ? (int)w : slots;
+  }
+  return slots;
+}
+
 }  // namespace ata

@@ -362,6 +362,7 @@ cudaError_t launch_tf32_2sm(const DProd<float>* prods, int count, double alpha, 
     Tc2Args a;
     std::memset(&a, 0, sizeof(a));
     long long total = 0;
+    int ptiles[kMax], pkinds[kMax];
     const int n = count - base < kMax ? count - base : kMax;
     for (int i = 0; i < n; ++i) {
       const DProd<float>& p = prods[base + i];
@@ -381,12 +382,14 @@ cudaError_t launch_tf32_2sm(const DProd<float>* prods, int count, double alpha, 
       q.tn = (p.n + BM - 1) / BM;
       q.tk = (p.k + BN - 1) / BN;
       q.tile_begin = (int)total;
-      total += p.kind == kSyrk ? (long long)q.tn * (q.tn + 1) / 2 : (long long)q.tn * q.tk;
+      ptiles[i] = p.kind == kSyrk ? q.tn * (q.tn + 1) / 2 : q.tn * q.tk;
+      pkinds[i] = p.kind;
+      total += ptiles[i];
     }
     a.count = n;
     a.total_tiles = (int)total;
     if (total == 0) continue;
-    const int clusters = (int)(total < sms / 2 ? total : sms / 2);
+    const int clusters = periodic_workers(ptiles, pkinds, n, total, sms / 2);
     prod_tf32_2sm_kernel<<<clusters * 2, THREADS, smem, s>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;

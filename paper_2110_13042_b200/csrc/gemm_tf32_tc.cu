@@ -388,6 +388,7 @@ cudaError_t launch_tf32_tc(const DProd<float>* prods, int count, double alpha, c
     TcArgs a;
     std::memset(&a, 0, sizeof(a));
     long long total = 0;
+    int ptiles[kMax], pkinds[kMax];
     const int n = count - base < kMax ? count - base : kMax;
     for (int i = 0; i < n; ++i) {
       const DProd<float>& p = prods[base + i];
@@ -407,14 +408,17 @@ cudaError_t launch_tf32_tc(const DProd<float>* prods, int count, double alpha, c
       q.tn = (p.n + BM - 1) / BM;
       q.tk = (p.k + BN - 1) / BN;
       q.tile_begin = (int)total;
+      ptiles[i] = 0;
       if (p.kind == kSyrk) {
         for (int ti = 0; ti < q.tn; ++ti) {
           int c = (ti * BM + BM - 1) / BN + 1;
-          total += c < q.tk ? c : q.tk;
+          ptiles[i] += c < q.tk ? c : q.tk;
         }
       } else {
-        total += (long long)q.tn * q.tk;
+        ptiles[i] = q.tn * q.tk;
       }
+      pkinds[i] = p.kind;
+      total += ptiles[i];
     }
     a.count = n;
     a.total_tiles = (int)total;
@@ -433,7 +437,7 @@ cudaError_t launch_tf32_tc(const DProd<float>* prods, int count, double alpha, c
       if (want) std::printf("tc launch: %d products, %lld tiles, dbg %p\n", n, total, (void*)dbg);
     }
     if (total == 0) continue;
-    const int grid = (int)(total < sms ? total : sms);
+    const int grid = periodic_workers(ptiles, pkinds, n, total, sms);
     prod_tf32_tc_kernel<<<grid, THREADS, smem, s>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
