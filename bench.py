@@ -123,14 +123,19 @@ def launch_units(plan):
     while i < len(ops):
         t = int(ops[i]["type"])
         j = i + 1
-        if t in (nat.OP_GEMM, nat.OP_SYRK) and int(ops[i]["group"]) >= 0:
-            g = int(ops[i]["group"])
+        if (t == nat.OP_ROUND and int(ops[i]["group"]) >= 0 and j < len(ops)
+                and int(ops[j]["group"]) == int(ops[i]["group"])):
+            t = int(ops[j]["type"])     # fused rounding: part of the product launch that follows
+        if t in (nat.OP_GEMM, nat.OP_SYRK) and int(ops[j - 1]["group"]) >= 0:
+            g = int(ops[j - 1]["group"])
             while j < len(ops) and int(ops[j]["type"]) in (nat.OP_GEMM, nat.OP_SYRK) \
                     and int(ops[j]["group"]) == g:
                 j += 1
         flops = 0
         for op in ops[i:j]:
             ot = int(op["type"])
+            if ot == nat.OP_ROUND and t in (nat.OP_GEMM, nat.OP_SYRK):
+                continue
             m, n, k = int(op["m"]), int(op["n"]), int(op["k"])
             if ot == nat.OP_GEMM:
                 flops += 2 * m * n * k
@@ -144,8 +149,13 @@ def launch_units(plan):
     # the executor splits groups beyond 48 products into several launches
     launches = 0
     for (i, j, is_prod, _) in units:
-        launches += -(-(j - i) // 48) if is_prod else 1
+        launches += -(-_nprod(ops, i, j) // 48) if is_prod else 1
     return units, launches
+
+
+def _nprod(ops, i, j):
+    from paper_2110_13042_b200 import _native as nat
+    return sum(1 for o in ops[i:j] if int(o["type"]) in (nat.OP_GEMM, nat.OP_SYRK))
 
 
 def cpu_sample_rate(cfg_name, cores):
@@ -333,7 +343,7 @@ def main():
             else:
                 ew_ms += d
                 ew_elems += fl
-    prod_launches = sum(-(-(j - i) // 48) for (i, j, p, _) in units if p) * args.steps
+    prod_launches = sum(-(-_nprod(plan.ops, i, j) // 48) for (i, j, p, _) in units if p) * args.steps
     achieved = prod_flops / (prod_ms * 1e-3) / 1e12 if prod_ms > 0 else 0.0
     peak = FP64_PEAK_TFLOPS if f64 else TF32_PEAK_TFLOPS
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
