@@ -38,7 +38,7 @@ sys.path.insert(0, ROOT)
 # DMMA m8n8k4 issue-rate peak; cuBLAS DGEMM 8192^3 reached 35.5-36.3 TF/s on the same box.
 FP64_PEAK_TFLOPS = 37.17
 # TF32: cuBLAS TF32 GEMM measured 766-839 TF/s (profiles/fp64_peak.txt); nominal dense 1100.
-TF32_PEAK_TFLOPS = 839.0
+TF32_PEAK_TFLOPS = 1112.0   # measured tcgen05 kind::tf32 MN-major issue rate (profiles/fp64_peak.txt)
 CPU_SAMPLE = {"c4": (16384, 4096), "c3": (16384, 4096), "c2": (6001, 4097), "c5": (65536, 2048),
               "c1": (1024, 1024)}
 
@@ -348,10 +348,11 @@ def main():
     peak = FP64_PEAK_TFLOPS if f64 else TF32_PEAK_TFLOPS
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": None,
-                "kernel": "prod_f64_kernel" if f64 else "prod_f32_kernel",
+                "kernel": "prod_f64_ws_kernel" if f64 else "prod_tf32_tc_kernel",
                 "peak_source": ("measured DMMA m8n8k4 issue-rate peak on this pool's B200 "
                                 "(profiles/fp64_peak.txt); MEASURED_PEAKS.json has no FP64 figure")
-                if f64 else "measured cuBLAS TF32 GEMM on this pool's B200 (profiles/fp64_peak.txt)",
+                if f64 else ("measured tcgen05.mma kind::tf32 issue rate on this pool's B200 "
+                             "(profiles/fp64_peak.txt; cuBLAS TF32 reaches 766-839)"),
                 "share_of_step": prod_ms / total_ms if total_ms else None,
                 "executed_flops_per_step": prod_flops // args.steps,
                 "algorithmic_flops_per_step": m * n * n,

@@ -70,11 +70,7 @@ extern "C" {
  * with accumulate selecting += (into C) or = (into a parent's product buffer). */
 #define ATA_OP_POSTADD7 6
 /* ATA_OP_ROUND: d[0] = round-to-nearest TF32 of s[0] (fp32 only; equal extents).
- * Emitted once per operand by single-pass-TF32 plans before the tcgen05 products.
- * group >= 0 equal to the group of the product op that immediately follows joins
- * the rounding to that launch: the tcgen05 kernel's epilogue warps round blocks of
- * 128 rows and its TMA producers wait per block (needs ata_sync_ints_needed ints
- * of sync); any other launcher path runs it first, standalone.  group < 0: standalone. */
+ * Emitted once per operand by single-pass-TF32 plans before the tcgen05 products. */
 #define ATA_OP_ROUND 7
 #define ATA_MAX_TERMS 4
 #define ATA_MAX_DESTS 8

@@ -15,6 +15,9 @@ import numpy as np
 from . import errors
 
 LIB_PATH = Path(__file__).resolve().parent / "_lib" / "libatamul_b200.so"
+# developer knob for A/B kernel experiments: load another in-tree build instead
+if os.environ.get("ATA_LIB_PATH"):
+    LIB_PATH = Path(os.environ["ATA_LIB_PATH"]).resolve()
 
 ATA_F64, ATA_F32, ATA_TF32 = 0, 1, 2
 OP_GEMM, OP_SYRK, OP_COMBO, OP_UPDATE, OP_FILL, OP_COMBO4, OP_POSTADD7, OP_ROUND = \

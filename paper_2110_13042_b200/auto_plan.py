@@ -69,8 +69,6 @@ class AutoParams:
     min_chunk: int = 8192          # ... into chunks of at least this many rows
     tf32_tflops: float = 400.0     # single-pass TF32 leaf-product rate (tcgen05, profiles/)
     tf32_fill_waves: int = 8       # 128x256 tcgen05 tiles: more chunks to fill 148 SMs
-    fuse_round: bool = False       # TF32: round A inside the first product launch (measured
-                                   # neutral on c5: 9.85 ms fused vs 9.93 ms standalone)
 
 
 TILE = 128        # output tile of the product kernels
@@ -347,11 +345,5 @@ def plan_ata_auto(m: int, n: int, lda: int, ldc: int, params: AutoParams = AutoP
     ap = _AutoPlanner(params)
     ap.ata(m, n, lda, ldc, round_tf32)
     plan = ap.pb.finish()
-    ops = plan.ops
-    if (round_tf32 and params.fuse_round and len(ops) > 1 and int(ops[0]["type"]) == nat.OP_ROUND
-            and int(ops[1]["type"]) in (nat.OP_GEMM, nat.OP_SYRK) and int(ops[1]["group"]) >= 0):
-        # the rounding joins the first product launch: its epilogue warps round
-        # row blocks while the tensor cores run, the TMA producer waits per block
-        ops[0]["group"] = ops[1]["group"]
     plan.ws_scalars = max(plan.ws_scalars, ap.ws_peak)
     return plan

@@ -92,13 +92,7 @@ cudaError_t launch_batch<double>(const ata::BatchArgs<double>& a, cudaStream_t s
 }
 template <>
 cudaError_t launch_batch<float>(const ata::BatchArgs<float>& a, cudaStream_t s, int dtype) {
-  return ata::launch_batch_f32(a, s, dtype != ATA_TF32, nullptr);
-}
-cudaError_t launch_batch_rounded(const ata::BatchArgs<float>& a, cudaStream_t s, int dtype, const ata::RoundJob& rj) {
-  return ata::launch_batch_f32(a, s, dtype != ATA_TF32, &rj);
-}
-cudaError_t launch_batch_rounded(const ata::BatchArgs<double>&, cudaStream_t, int, const ata::RoundJob&) {
-  return cudaErrorInvalidValue;  // unreachable: ROUND is rejected for fp64 plans
+  return ata::launch_batch_f32(a, s, dtype != ATA_TF32);
 }
 
 int validate_op(const ata_op& op, const Bases& b, int i) {
@@ -192,24 +186,18 @@ bool supports_ordering<double>() { return ata::f64_supports_ordering(); }
 template <>
 bool supports_ordering<float>() { return false; }
 
-// Walk the op list with the executor's batching rule, calling
-// on_batch(first, last, round) for every product launch [first, last) and
-// on_ew(i) for every elementwise op.  Consecutive GEMM/SYRK ops with equal
-// group >= 0 share a launch (at most kMaxBatch); when the launcher cannot
-// order shared destinations, a product whose region already occurs in the
-// open batch starts a new launch.  A ROUND op carrying the group of the
-// product that immediately follows it is joined to that launch (round = its
-// index, else -1): the launcher fuses it or runs it first.
+// Walk the op list with the executor's batching rule, calling on_batch(first, last)
+// for every product launch [first, last) and on_ew(i) for every elementwise op.
+// Consecutive GEMM/SYRK ops with equal group >= 0 share a launch (at most
+// kMaxBatch); when the launcher cannot order shared destinations, a product
+// whose region already occurs in the open batch starts a new launch.
 template <typename F1, typename F2>
 int walk_batches(const ata_op* ops, int n_ops, bool ordering, F1 on_batch, F2 on_ew) {
-  int first = -1, group = -1, count = 0, round = -1;
+  int first = -1, group = -1, count = 0;
   std::vector<int> regions;
   auto flush = [&](int end) -> int {
     int rc = ATA_OK;
-    if (count > 0) {
-      rc = on_batch(first, end, round);
-      round = -1;
-    }
+    if (count > 0) rc = on_batch(first, end);
     first = -1;
     count = 0;
     regions.clear();
@@ -218,12 +206,6 @@ int walk_batches(const ata_op* ops, int n_ops, bool ordering, F1 on_batch, F2 on
   for (int i = 0; i < n_ops; ++i) {
     const ata_op& op = ops[i];
     int rc;
-    if (op.type == ATA_OP_ROUND && op.group >= 0 && i + 1 < n_ops &&
-        (ops[i + 1].type == ATA_OP_GEMM || ops[i + 1].type == ATA_OP_SYRK) && ops[i + 1].group == op.group) {
-      if ((rc = flush(i))) return rc;
-      round = i;  // joins the launch opened by ops[i + 1]
-      continue;
-    }
     if (op.type == ATA_OP_GEMM || op.type == ATA_OP_SYRK) {
       bool join = count > 0 && op.group >= 0 && op.group == group && count < ata::kMaxBatch;
       if (join && !ordering) {
@@ -232,7 +214,7 @@ int walk_batches(const ata_op* ops, int n_ops, bool ordering, F1 on_batch, F2 on
             for (int r : regions)
               if (r == op.d[j].region) join = false;
       }
-      if (!join && count > 0 && (rc = flush(i))) return rc;
+      if (!join && (rc = flush(i))) return rc;
       if (count == 0) first = i;
       ++count;
       group = op.group;
@@ -279,7 +261,7 @@ int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, int* sync, int64_t 
   }
   const bool ordering = supports_ordering<T>();
   ata::BatchArgs<T> batch;
-  auto on_batch = [&](int first, int last, int round) -> int {
+  auto on_batch = [&](int first, int last) -> int {
     std::memset(&batch, 0, sizeof(batch));
     batch.alpha = alpha;
     const int64_t need = batch_sync_ints(ops, first, last);
@@ -318,22 +300,7 @@ int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, int* sync, int64_t 
         }
       }
     }
-    cudaError_t e = cudaSuccess;
-    if (round >= 0) {
-      // validate_op admits ROUND for fp32 plans only
-      ata::RoundJob rj;
-      const ata::DTerm<T> src = term_of<T>(ops[round].s[0], b);
-      const ata::DDest<T> dst = dest_of<T>(ops[round].d[0], b);
-      rj.src = reinterpret_cast<const float*>(src.p);
-      rj.dst = reinterpret_cast<float*>(dst.p);
-      rj.lds = src.ld;
-      rj.ldd = dst.ld;
-      rj.rows = dst.rows;
-      rj.cols = dst.cols;
-      e = launch_batch_rounded(batch, s, dtype, rj);
-    } else {
-      e = launch_batch<T>(batch, s, dtype);
-    }
+    cudaError_t e = launch_batch<T>(batch, s, dtype);
     if (e != cudaSuccess) return cuda_fail(e, "product launch");
     return ATA_OK;
   };
@@ -429,10 +396,8 @@ int64_t ata_sync_ints_needed(int dtype, const ata_op* ops, int32_t n_ops) {
   int64_t need = 1;
   walk_batches(
       ops, n_ops, ordering,
-      [&](int first, int last, int round) -> int {
+      [&](int first, int last) -> int {
         need = std::max(need, batch_sync_ints(ops, first, last));
-        if (round >= 0)  // fused rounding: claim + done counters and one flag per item
-          need = std::max<int64_t>(need, ata::kRoundSyncExtra + (ops[round].d[0].rows + ata::kRoundRows - 1) / ata::kRoundRows);
         return ATA_OK;
       },
       [](int) -> int { return ATA_OK; });

@@ -68,18 +68,7 @@ struct EwArgs {  // elementwise op: rows x cols iteration space
 cudaError_t launch_batch_f64(const BatchArgs<double>& a, cudaStream_t s);
 cudaError_t launch_batch_f64_ws(const BatchArgs<double>& a, cudaStream_t s);
 bool f64_supports_ordering();
-// A ROUND op joined to the product launch that follows it (same plan group):
-// R = rna_tf32(src), rows published to the products as they are rounded
-// (single-pass TF32 tcgen05 path; any other path rounds first, standalone).
-struct RoundJob {
-  const float* src;
-  float* dst;
-  long long lds, ldd;
-  int rows, cols;
-};
-constexpr int kRoundRows = 128;      // rows per rounding item
-constexpr int kRoundSyncExtra = 16;  // sync ints beyond one flag per item (counters, alignment, poll overrun)
-cudaError_t launch_batch_f32(const BatchArgs<float>& a, cudaStream_t s, bool split, const RoundJob* rj);
+cudaError_t launch_batch_f32(const BatchArgs<float>& a, cudaStream_t s, bool split);
 template <typename T> cudaError_t launch_combo(const EwArgs<T>& a, cudaStream_t s);
 template <typename T> cudaError_t launch_update(const EwArgs<T>& a, cudaStream_t s);
 template <typename T> cudaError_t launch_combo4(const EwArgs<T>& a, cudaStream_t s);

@@ -297,21 +297,11 @@ static cudaError_t launch_batch_f32_t(BatchArgs<float> a, cudaStream_t s) {
 }
 
 bool tc_eligible(const DProd<float>& p);
-cudaError_t launch_tf32_tc(const DProd<float>* prods, int count, double alpha, cudaStream_t s,
-                           const RoundJob* rj, int* sync);
-cudaError_t launch_tf32_2sm(const DProd<float>* prods, int count, double alpha, cudaStream_t s,
-                            const RoundJob* rj, int* sync);
+cudaError_t launch_tf32_tc(const DProd<float>* prods, int count, double alpha, cudaStream_t s);
+cudaError_t launch_tf32_2sm(const DProd<float>* prods, int count, double alpha, cudaStream_t s);
 
-static cudaError_t round_first(const RoundJob* rj, cudaStream_t s) {
-  return rj == nullptr ? cudaSuccess
-                       : launch_round_tf32(rj->src, rj->lds, rj->dst, rj->ldd, rj->rows, rj->cols, s);
-}
-
-cudaError_t launch_batch_f32(const BatchArgs<float>& a, cudaStream_t s, bool split, const RoundJob* rj) {
-  if (split) {
-    cudaError_t e = round_first(rj, s);
-    return e != cudaSuccess ? e : launch_batch_f32_t<true>(a, s);
-  }
+cudaError_t launch_batch_f32(const BatchArgs<float>& a, cudaStream_t s, bool split) {
+  if (split) return launch_batch_f32_t<true>(a, s);
   // single-pass TF32: plain products go to the tcgen05/TMA kernel, the rest
   // (fused multi-term / multi-destination products) to the mma.sync kernel
   static int use_tc = -1;
@@ -319,10 +309,7 @@ cudaError_t launch_batch_f32(const BatchArgs<float>& a, cudaStream_t s, bool spl
     const char* e = std::getenv("ATA_TF32_TC");
     use_tc = e ? std::atoi(e) : 1;
   }
-  if (!use_tc) {
-    cudaError_t e = round_first(rj, s);
-    return e != cudaSuccess ? e : launch_batch_f32_t<false>(a, s);
-  }
+  if (!use_tc) return launch_batch_f32_t<false>(a, s);
   DProd<float> tcp[kMaxBatch];
   int ntc = 0;
   BatchArgs<float> rest = a;
@@ -331,18 +318,9 @@ cudaError_t launch_batch_f32(const BatchArgs<float>& a, cudaStream_t s, bool spl
     if (tc_eligible(a.p[i])) tcp[ntc++] = a.p[i];
     else rest.p[rest.count++] = a.p[i];
   }
-  // the rounding fuses into the tcgen05 launch (its epilogue warps
-  // round while the tensor cores run); otherwise it runs first, standalone
-  const bool fuse = rj != nullptr && ntc > 0 && a.sync != nullptr &&
-                    a.n_sync >= kRoundSyncExtra + (rj->rows + kRoundRows - 1) / kRoundRows;
-  if (!fuse) {
-    cudaError_t e = round_first(rj, s);
-    if (e != cudaSuccess) return e;
-  }
   if (ntc > 0) {
     // 2 = CTA-pair tcgen05 kernel (cta_group::2), 1 = single-CTA tcgen05 kernel
-    cudaError_t e = use_tc == 2 ? launch_tf32_2sm(tcp, ntc, a.alpha, s, fuse ? rj : nullptr, a.sync)
-                                : launch_tf32_tc(tcp, ntc, a.alpha, s, fuse ? rj : nullptr, a.sync);
+    cudaError_t e = use_tc == 2 ? launch_tf32_2sm(tcp, ntc, a.alpha, s) : launch_tf32_tc(tcp, ntc, a.alpha, s);
     if (e != cudaSuccess) return e;
   }
   if (rest.count > 0) return launch_batch_f32_t<false>(rest, s);

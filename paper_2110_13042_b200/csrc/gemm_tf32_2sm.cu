@@ -19,7 +19,6 @@
 #include <cstring>
 
 #include "ata_common.cuh"
-#include "tf32_fused_round.cuh"
 
 namespace ata {
 
@@ -45,12 +44,10 @@ struct alignas(64) Tc2Prod {
   float scale;
   int kind, m, n, k;
   int tn, tk, tile_begin, accumulate;
-  int rrow0, rshift;  // fused rounding (see TcProd)
 };
 
 struct Tc2Args {
   Tc2Prod p[tc2::kMax];
-  TcRound rnd;
   int count;
   int total_tiles;
 };
@@ -175,17 +172,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
     // ================= TMA producer (both CTAs) =================
     if (lane == 0) {
       int ks = 0;
-      if (blockIdx.x == 0 && args.rnd.items > 0) args.rnd.done[2] = (int)(tc_now() & 0x7fffffff);  // diagnostics
       for (int tile = cluster; tile < args.total_tiles; tile += nclusters) {
         const Tc2Tile t = t2_decode(args, tile);
         const Tc2Prod& P = args.p[t.pi];
         const CUtensorMap* mt = P.kind == kSyrk ? &P.ts : &P.tt;
         const int i0 = t.ti * BM + rank * HALF, j0 = t.tj * BN + rank * HALF;
         const int KT = (P.m + BK - 1) / BK;
-        int next_item = (P.rrow0 >= 0 && args.rnd.items > 0) ? P.rrow0 / kRoundRows : 0x7fffffff;
         for (int kb = 0; kb < KT; ++kb, ++ks) {
-          if (P.rrow0 >= 0)  // fused rounding: rows of this k-block published?
-            tc_round_acquire(args.rnd, P.rrow0 + P.rshift + kb * BK + BK - 1, next_item);
           const int s = ks % STAGES;
           t2_wait(&empty[s], ((ks / STAGES) & 1) ^ 1);
           uint8_t* sa = smem + s * STAGE_BYTES;
@@ -260,13 +253,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
     const uint32_t leader_tempty0 = t2_map(t2_smem(&tempty[0]), 0);
     const uint32_t leader_tempty1 = t2_map(t2_smem(&tempty[1]), 0);
     int it = 0;
-    bool rounding = args.rnd.items > 0;
     for (int tile = cluster; tile < args.total_tiles; tile += nclusters, ++it) {
       const Tc2Tile t = t2_decode(args, tile);
       const Tc2Prod& P = args.p[t.pi];
       const int buf = it & 1;
-      // while the accumulator is busy, round operand rows (fused ATA_OP_ROUND)
-      while (rounding && !tc_mbar_test(&tfull[buf], (it >> 1) & 1)) rounding = tc_round_next(args.rnd, lane);
       t2_wait(&tfull[buf], (it >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const int row = t.ti * BM + rank * HALF + q * 32 + lane;
@@ -325,7 +315,6 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
         asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(buf ? leader_tempty1 : leader_tempty0)
                      : "memory");
     }
-    while (rounding) rounding = tc_round_next(args.rnd, lane);
   }
   asm volatile("tcgen05.fence::before_thread_sync;");
   t2_cluster_sync();
@@ -354,8 +343,7 @@ static bool t2_map_term(CUtensorMap* map, const DTerm<float>& t) {
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-cudaError_t launch_tf32_2sm(const DProd<float>* prods, int count, double alpha, cudaStream_t s,
-                            const RoundJob* rj, int* sync) {
+cudaError_t launch_tf32_2sm(const DProd<float>* prods, int count, double alpha, cudaStream_t s) {
   using namespace tc2;
   static int sms = 0;
   if (sms == 0) {
@@ -397,14 +385,6 @@ cudaError_t launch_tf32_2sm(const DProd<float>* prods, int count, double alpha, 
       ptiles[i] = p.kind == kSyrk ? q.tn * (q.tn + 1) / 2 : q.tn * q.tk;
       pkinds[i] = p.kind;
       total += ptiles[i];
-      const int rs = tc_round_row(p.s[0], base == 0 ? rj : nullptr);
-      const int rt = p.kind == kSyrk ? rs : tc_round_row(p.t[0], base == 0 ? rj : nullptr);
-      q.rrow0 = rs < 0 ? rt : (rt < 0 ? rs : min(rs, rt));
-      q.rshift = (rs >= 0 && rt >= 0) ? max(rs, rt) - q.rrow0 : 0;
-    }
-    if (base == 0 && rj != nullptr && rj->rows > 0 && rj->cols > 0) {
-      cudaError_t e = tc_round_setup(a.rnd, rj, sync, s);
-      if (e != cudaSuccess) return e;
     }
     a.count = n;
     a.total_tiles = (int)total;

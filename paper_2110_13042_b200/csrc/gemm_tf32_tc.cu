@@ -27,7 +27,6 @@
 #include <cstring>
 
 #include "ata_common.cuh"
-#include "tf32_fused_round.cuh"
 
 namespace ata {
 
@@ -39,7 +38,6 @@ constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int THREADS = 192;
 constexpr int TMEM_COLS = 512;
 constexpr int kMax = 48;   // = kMaxBatch: one launch per plan group (15 KB of kernel parameters)
-constexpr int RB = kRoundRows;  // rows per fused-rounding item
 // instruction descriptor: D f32, A/B tf32, both MN-major, N = 256, M = 128
 constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (1u << 16) |
                            (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
@@ -54,13 +52,10 @@ struct alignas(64) TcProd {
   float scale;
   int kind, m, n, k;
   int tn, tk, tile_begin, accumulate;
-  int rrow0;   // fused rounding: first row of the rounded copy R this product's operands read (-1: none)
-  int rshift;  // row offset between the two operand windows (both inside R)
 };
 
 struct TcArgs {
   TcProd p[tc::kMax];
-  TcRound rnd;
   int count;
   int total_tiles;
   float* dbg;  // debug dump (ATA_TC_DEBUG): stage-0 smem of the first k-block
@@ -209,17 +204,13 @@ __global__ void __launch_bounds__(tc::THREADS, 1) prod_tf32_tc_kernel(const __gr
     // ================= TMA producer =================
     if (lane == 0) {
       int ks = 0;
-      if (blockIdx.x == 0 && args.rnd.items > 0) args.rnd.done[2] = (int)(tc_now() & 0x7fffffff);  // diagnostics
       for (int tile = blockIdx.x; tile < args.total_tiles; tile += gridDim.x) {
         const TcTile t = tc_decode(args, tile);
         const TcProd& P = args.p[t.pi];
         const CUtensorMap* mt = P.kind == kSyrk ? &P.ts : &P.tt;
         const int i0 = t.ti * BM, j0 = t.tj * BN;
         const int KT = (P.m + BK - 1) / BK;
-        int next_item = (P.rrow0 >= 0 && args.rnd.items > 0) ? P.rrow0 / RB : 0x7fffffff;  // first item not yet seen
         for (int kb = 0; kb < KT; ++kb, ++ks) {
-          if (P.rrow0 >= 0)  // fused rounding: rows of this k-block published?
-            tc_round_acquire(args.rnd, P.rrow0 + P.rshift + kb * BK + BK - 1, next_item);
           const int s = ks % STAGES;
           tc_mbar_wait(&empty[s], ((ks / STAGES) & 1) ^ 1);
           uint8_t* sa = smem + s * STAGE_BYTES;
@@ -268,13 +259,10 @@ __global__ void __launch_bounds__(tc::THREADS, 1) prod_tf32_tc_kernel(const __gr
     // ================= epilogue (warps 2..5) =================
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
     int it = 0;
-    bool rounding = args.rnd.items > 0;
     for (int tile = blockIdx.x; tile < args.total_tiles; tile += gridDim.x, ++it) {
       const TcTile t = tc_decode(args, tile);
       const TcProd& P = args.p[t.pi];
       const int buf = it & 1;
-      // while the accumulator is busy, round operand rows (fused ATA_OP_ROUND)
-      while (rounding && !tc_mbar_test(&tfull[buf], (it >> 1) & 1)) rounding = tc_round_next(args.rnd, lane);
       tc_mbar_wait(&tfull[buf], (it >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n");
       const int row = t.ti * BM + q * 32 + lane;
@@ -333,7 +321,6 @@ __global__ void __launch_bounds__(tc::THREADS, 1) prod_tf32_tc_kernel(const __gr
       __syncwarp();
       if (lane == 0) tc_mbar_arrive(&tempty[buf]);
     }
-    while (rounding) rounding = tc_round_next(args.rnd, lane);
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n");
   __syncthreads();
@@ -382,8 +369,7 @@ bool tc_eligible(const DProd<float>& p) {
   return true;
 }
 
-cudaError_t launch_tf32_tc(const DProd<float>* prods, int count, double alpha, cudaStream_t s,
-                           const RoundJob* rj, int* sync) {
+cudaError_t launch_tf32_tc(const DProd<float>* prods, int count, double alpha, cudaStream_t s) {
   using namespace tc;
   static int sms = 0;
   if (sms == 0) {
@@ -433,15 +419,6 @@ cudaError_t launch_tf32_tc(const DProd<float>* prods, int count, double alpha, c
       }
       pkinds[i] = p.kind;
       total += ptiles[i];
-      // fused rounding: producers wait for the rows of both operand windows
-      const int rs = tc_round_row(p.s[0], base == 0 ? rj : nullptr);
-      const int rt = p.kind == kSyrk ? rs : tc_round_row(p.t[0], base == 0 ? rj : nullptr);
-      q.rrow0 = rs < 0 ? rt : (rt < 0 ? rs : min(rs, rt));
-      q.rshift = (rs >= 0 && rt >= 0) ? max(rs, rt) - q.rrow0 : 0;
-    }
-    if (base == 0 && rj != nullptr && rj->rows > 0 && rj->cols > 0) {
-      cudaError_t e = tc_round_setup(a.rnd, rj, sync, s);
-      if (e != cudaSuccess) return e;
     }
     a.count = n;
     a.total_tiles = (int)total;
