@@ -131,6 +131,10 @@ def launch_units(plan):
             while j < len(ops) and int(ops[j]["type"]) in (nat.OP_GEMM, nat.OP_SYRK) \
                     and int(ops[j]["group"]) == g:
                 j += 1
+        elif t in (nat.OP_COMBO4, nat.OP_POSTADD7) and int(ops[i]["group"]) >= 0:
+            g = int(ops[i]["group"])     # multi-node elementwise launch
+            while j < len(ops) and int(ops[j]["type"]) == t and int(ops[j]["group"]) == g:
+                j += 1
         flops = 0
         for op in ops[i:j]:
             ot = int(op["type"])
@@ -225,7 +229,7 @@ def main():
         else:
             dist.init_process_group(backend)
     import paper_2110_13042_b200 as P
-    from paper_2110_13042_b200 import _native as nat, auto_plan, dist as pdist, engine, planner
+    from paper_2110_13042_b200 import _native as nat, auto_plan, dist as pdist, engine, planner, ref_bfs
     from paper_2110_13042_b200.measure import CONFIGS
 
     cfg = CONFIGS[args.config]
@@ -255,8 +259,12 @@ def main():
             if plan.ws_scalars else None
     else:
         ws = P.workspace_for_ata(mloc, n, threshold, dtype=np_dt)
-        plan = planner.plan_ata_reference(mloc, n, n, n, threshold, ws.level_offsets())
-        wsbuf = ws.ensure(dev)
+        if engine.reference_dfs():
+            plan = planner.plan_ata_reference(mloc, n, n, n, threshold, ws.level_offsets())
+            wsbuf = ws.ensure(dev)
+        else:   # the reference recursion tree executed breadth first
+            plan = ref_bfs.plan_ata_reference_bfs(mloc, n, n, n, threshold)
+            wsbuf = ws.ensure(dev, extra=plan.ws_scalars)
     units, n_launch = launch_units(plan)
     code = nat.dtype_code(A.dtype, precision)
     a_elems, c_elems = A.numel(), C.numel()

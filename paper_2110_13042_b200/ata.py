@@ -5,8 +5,9 @@
 triangle of C is never read or written by any kernel (ata.py:121-123).
 
 ``threshold`` keeps the reference's element-count meaning (ata.py:23-26,
-strassen.py:38-41) and then reproduces the reference recursion exactly (same
-leaves, same exact multiplication count).  ``threshold="auto"`` selects the
+strassen.py:38-41) and then reproduces the reference recursion tree exactly
+(same leaves, same exact multiplication count), executed breadth first
+(ref_bfs.py; ATA_REF_DFS=1 selects the depth-first executor).  ``threshold="auto"`` selects the
 GPU plan (auto_plan.plan_ata_auto).  Inputs are torch CUDA tensors (zero copy)
 or anything the reference accepts (staged through the device).
 """
@@ -15,7 +16,7 @@ from __future__ import annotations
 import numpy as np
 
 from . import _native as nat
-from . import auto_plan, engine, planner
+from . import auto_plan, engine, planner, ref_bfs
 from .errors import ShapeMismatchError, UnsupportedSizeError
 from .matrix import (DenseMatrix, DeviceOperand, MultCounter, as_array, mirror_lower_to_upper)
 from .workspace import (DEFAULT_THRESHOLD, StrassenWorkspace, ata_calls, check_ata_workspace,
@@ -40,10 +41,14 @@ def _plan_for(m, n, lda, ldc, threshold, ws, auto_params=None, round_tf32=False)
         key = ("ata-auto", m, n, lda, ldc, params, round_tf32)
         return engine.cached_plan(
             key, lambda: auto_plan.plan_ata_auto(m, n, lda, ldc, params, round_tf32=round_tf32))
-    offs = tuple(ws.level_offsets())
-    key = ("ata-ref", m, n, lda, ldc, int(threshold), offs)
-    return engine.cached_plan(
-        key, lambda: planner.plan_ata_reference(m, n, lda, ldc, int(threshold), list(offs)))
+    if engine.reference_dfs():
+        offs = tuple(ws.level_offsets())
+        key = ("ata-ref", m, n, lda, ldc, int(threshold), offs)
+        return engine.cached_plan(
+            key, lambda: planner.plan_ata_reference(m, n, lda, ldc, int(threshold), list(offs)))
+    # the reference recursion tree, executed breadth first (ref_bfs.py)
+    key = ("ata-ref-bfs", m, n, lda, ldc, int(threshold))
+    return engine.cached_plan(key, lambda: ref_bfs.plan_ata_reference_bfs(m, n, lda, ldc, int(threshold)))
 
 
 def ata(A, C, alpha=1.0, threshold=DEFAULT_THRESHOLD, ws: StrassenWorkspace | None = None,
@@ -69,8 +74,8 @@ def ata(A, C, alpha=1.0, threshold=DEFAULT_THRESHOLD, ws: StrassenWorkspace | No
     import torch
     plan = _plan_for(m, n, A_.ld, C_.ld, threshold, ws, auto_params,
                      round_tf32=(precision == "tf32" and C_.t.dtype == torch.float32))
-    wbuf = ws.ensure(C_.t.device, extra=plan.ws_scalars if threshold == AUTO else 0) \
-        if plan.ws_scalars > 0 else None
+    extra = plan.ws_scalars if (threshold == AUTO or not engine.reference_dfs()) else 0
+    wbuf = ws.ensure(C_.t.device, extra=extra) if plan.ws_scalars > 0 else None
     engine.run_plan(plan, nat.dtype_code(C_.t.dtype, precision), A_.ptr, A_.elems, C_.ptr, C_.elems, alpha,
                     ws=int(wbuf.data_ptr()) if wbuf is not None else 0,
                     ws_elems=int(wbuf.numel()) if wbuf is not None else 0)

@@ -187,12 +187,14 @@ template <>
 bool supports_ordering<float>() { return false; }
 
 // Walk the op list with the executor's batching rule, calling on_batch(first, last)
-// for every product launch [first, last) and on_ew(i) for every elementwise op.
+// for every product launch [first, last), on_ew_run(first, last) for every run of
+// COMBO4 / POSTADD7 ops sharing a group >= 0 (one multi-node launch) and on_ew(i)
+// for every other elementwise op.
 // Consecutive GEMM/SYRK ops with equal group >= 0 share a launch (at most
 // kMaxBatch); when the launcher cannot order shared destinations, a product
 // whose region already occurs in the open batch starts a new launch.
-template <typename F1, typename F2>
-int walk_batches(const ata_op* ops, int n_ops, bool ordering, F1 on_batch, F2 on_ew) {
+template <typename F1, typename F2, typename F3>
+int walk_batches(const ata_op* ops, int n_ops, bool ordering, F1 on_batch, F2 on_ew, F3 on_ew_run) {
   int first = -1, group = -1, count = 0;
   std::vector<int> regions;
   auto flush = [&](int end) -> int {
@@ -224,6 +226,14 @@ int walk_batches(const ata_op* ops, int n_ops, bool ordering, F1 on_batch, F2 on
       continue;
     }
     if ((rc = flush(i))) return rc;
+    if ((op.type == ATA_OP_COMBO4 || op.type == ATA_OP_POSTADD7) && op.group >= 0) {
+      // consecutive combo4 / postadd7 ops of one group: independent nodes, one launch
+      int j = i + 1;
+      while (j < n_ops && ops[j].type == op.type && ops[j].group == op.group) ++j;
+      if ((rc = on_ew_run(i, j))) return rc;
+      i = j - 1;
+      continue;
+    }
     if ((rc = on_ew(i))) return rc;
   }
   return flush(n_ops);
@@ -250,6 +260,38 @@ int64_t batch_sync_ints(const ata_op* ops, int first, int last) {
     }
   for (auto& e : reg) total += (int64_t)e.second.first * e.second.second;
   return total;
+}
+
+template <typename T>
+ata::EwArgs<T> combo4_args(const ata_op& op, const Bases& b) {
+  ata::EwArgs<T> a;
+  std::memset(&a, 0, sizeof(a));
+  a.nsrc = op.ns;
+  a.ndst = op.nd;
+  a.lower = op.accumulate;  // COMBO4: accumulate field = lower-triangular outputs
+  for (int j = 0; j < op.ns; ++j) a.src[j] = term_of<T>(op.s[j], b);
+  for (int j = 0; j < op.nd; ++j) {
+    a.dst[j] = dest_of<T>(op.d[j], b);
+    a.dst[j].coef = op.d[j].region;
+    a.rows = a.rows > op.d[j].rows ? a.rows : op.d[j].rows;
+    a.cols = a.cols > op.d[j].cols ? a.cols : op.d[j].cols;
+  }
+  return a;
+}
+
+template <typename T>
+ata::EwArgs<T> postadd7_args(const ata_op& op, const Bases& b) {
+  ata::EwArgs<T> a;
+  std::memset(&a, 0, sizeof(a));
+  a.nsrc = 7;
+  a.ndst = 4;
+  for (int q = 0; q < 7; ++q) {
+    a.src[q] = term_of<T>(q < 4 ? op.s[q] : op.t[q - 4], b);
+    a.rows = a.rows > a.src[q].rows ? a.rows : a.src[q].rows;
+    a.cols = a.cols > a.src[q].cols ? a.cols : a.src[q].cols;
+  }
+  for (int j = 0; j < 4; ++j) a.dst[j] = dest_of<T>(op.d[j], b);
+  return a;
 }
 
 template <typename T>
@@ -330,41 +372,44 @@ int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, int* sync, int64_t 
       ata::DDest<T> d = dest_of<T>(op.d[0], b);
       e = ata::launch_fill<T>(d.p, d.ld, d.rows, d.cols, s);
     } else if (op.type == ATA_OP_COMBO4) {
-      ata::EwArgs<T> a;
-      std::memset(&a, 0, sizeof(a));
-      a.nsrc = op.ns;
-      a.ndst = op.nd;
-      a.lower = op.accumulate;  // COMBO4: accumulate field = lower-triangular outputs
-      for (int j = 0; j < op.ns; ++j) a.src[j] = term_of<T>(op.s[j], b);
-      for (int j = 0; j < op.nd; ++j) {
-        a.dst[j] = dest_of<T>(op.d[j], b);
-        a.dst[j].coef = op.d[j].region;
-        a.rows = a.rows > op.d[j].rows ? a.rows : op.d[j].rows;
-        a.cols = a.cols > op.d[j].cols ? a.cols : op.d[j].cols;
-      }
-      e = ata::launch_combo4<T>(a, s);
+      e = ata::launch_combo4<T>(combo4_args<T>(op, b), s);
     } else if (op.type == ATA_OP_ROUND) {
       const ata::DTerm<T> src = term_of<T>(op.s[0], b);
       const ata::DDest<T> dst = dest_of<T>(op.d[0], b);
       e = ata::launch_round_tf32(reinterpret_cast<const float*>(src.p), src.ld, reinterpret_cast<float*>(dst.p),
                                  dst.ld, dst.rows, dst.cols, s);
     } else if (op.type == ATA_OP_POSTADD7) {
-      ata::EwArgs<T> a;
-      std::memset(&a, 0, sizeof(a));
-      a.nsrc = 7;
-      a.ndst = 4;
-      for (int q = 0; q < 7; ++q) {
-        a.src[q] = term_of<T>(q < 4 ? op.s[q] : op.t[q - 4], b);
-        a.rows = a.rows > a.src[q].rows ? a.rows : a.src[q].rows;
-        a.cols = a.cols > a.src[q].cols ? a.cols : a.src[q].cols;
-      }
-      for (int j = 0; j < 4; ++j) a.dst[j] = dest_of<T>(op.d[j], b);
-      e = ata::launch_postadd7<T>(a, op.accumulate, s);
+      e = ata::launch_postadd7<T>(postadd7_args<T>(op, b), op.accumulate, s);
     }
     if (e != cudaSuccess) return cuda_fail(e, "elementwise launch");
     return ATA_OK;
   };
-  return walk_batches(ops, n_ops, ordering, on_batch, on_ew);
+  auto on_ew_run = [&](int first, int last) -> int {
+    std::vector<ata::EwArgs<T>> args;
+    std::vector<int> acc;
+    args.reserve(last - first);
+    cudaError_t e = cudaSuccess;
+    if (ops[first].type == ATA_OP_COMBO4) {
+      bool small = true;
+      for (int i = first; i < last; ++i) small = small && ops[i].nd <= 5;
+      if (!small) {  // nodes with > 5 outputs: one launch each
+        for (int i = first; i < last; ++i)
+          if (int rc = on_ew(i)) return rc;
+        return ATA_OK;
+      }
+      for (int i = first; i < last; ++i) args.push_back(combo4_args<T>(ops[i], b));
+      e = ata::launch_combo4_multi<T>(args.data(), (int)args.size(), s);
+    } else {
+      for (int i = first; i < last; ++i) {
+        args.push_back(postadd7_args<T>(ops[i], b));
+        acc.push_back(ops[i].accumulate);
+      }
+      e = ata::launch_postadd7_multi<T>(args.data(), acc.data(), (int)args.size(), s);
+    }
+    if (e != cudaSuccess) return cuda_fail(e, "elementwise launch");
+    return ATA_OK;
+  };
+  return walk_batches(ops, n_ops, ordering, on_batch, on_ew, on_ew_run);
 }
 
 }  // namespace
@@ -400,7 +445,7 @@ int64_t ata_sync_ints_needed(int dtype, const ata_op* ops, int32_t n_ops) {
         need = std::max(need, batch_sync_ints(ops, first, last));
         return ATA_OK;
       },
-      [](int) -> int { return ATA_OK; });
+      [](int) -> int { return ATA_OK; }, [](int, int) -> int { return ATA_OK; });
   return need;
 }
 

@@ -75,6 +75,10 @@ template <typename T> cudaError_t launch_combo4(const EwArgs<T>& a, cudaStream_t
 cudaError_t launch_round_tf32(const float* src, long long lds, float* dst, long long ldd, int rows, int cols,
                               cudaStream_t s);
 template <typename T> cudaError_t launch_postadd7(const EwArgs<T>& a, int accumulate, cudaStream_t s);
+// many independent nodes per launch (elementwise_multi.cu); combo4 nodes: <= 5 outputs
+template <typename T> cudaError_t launch_combo4_multi(const EwArgs<T>* nodes, int count, cudaStream_t s);
+template <typename T>
+cudaError_t launch_postadd7_multi(const EwArgs<T>* nodes, const int* accumulate, int count, cudaStream_t s);
 template <typename T> cudaError_t launch_fill(T* p, long long ld, int rows, int cols, cudaStream_t s);
 template <typename T> cudaError_t launch_mirror(T* C, long long ldc, int n, cudaStream_t s);
 template <typename T> cudaError_t launch_pack(const T* C, long long ldc, int n, T* packed, cudaStream_t s);

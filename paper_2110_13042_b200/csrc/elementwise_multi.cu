@@ -1,0 +1,240 @@
+// Multi-node Strassen additions (sm_100a): one launch runs the combo4 (operand
+// sums) or postadd7 (post-additions) passes of many independent nodes of one
+// recursion level -- the breadth-first executions of reference-threshold
+// recursions (ref_bfs.py) have thousands of small nodes per level, where one
+// launch per node would be launch-latency bound.
+//
+// Node descriptors are compact windows packed into the kernel parameters
+// (<= 30 KB per launch); blockIdx.z selects the node, (x, y) tile its
+// rows x cols extent with the same per-element arithmetic as the single-node
+// kernels in elementwise.cu (zero-extended sources, truncated outputs).
+#include <cstring>
+
+#include "ata_common.cuh"
+
+namespace ata {
+
+namespace {
+
+constexpr int kMtX = 128, kMtY = 2;
+
+template <typename T>
+struct Win {
+  T* p;
+  long long ld;
+  int rows, cols;
+};
+
+template <typename T>
+struct C4Node {
+  Win<T> src[4];
+  Win<T> dst[5];
+  int code[5];
+  int nsrc, ndst, rows, cols, lower;
+};
+
+template <typename T>
+struct P7Node {
+  Win<T> src[7];
+  Win<T> dst[4];
+  T sign[4];
+  int rows, cols, accumulate, _pad;
+};
+
+constexpr int kC4Max = 104;
+constexpr int kP7Max = 96;
+
+template <typename T>
+struct C4Batch {
+  int count, maxrows;
+  C4Node<T> n[kC4Max];
+};
+template <typename T>
+struct P7Batch {
+  int count, maxrows;
+  P7Node<T> n[kP7Max];
+};
+static_assert(sizeof(C4Batch<double>) <= 30000 && sizeof(P7Batch<double>) <= 30000, "kernel parameter space");
+
+template <typename T>
+__global__ void combo4_multi_kernel(const __grid_constant__ C4Batch<T> b) {
+  const C4Node<T>& a = b.n[blockIdx.z];
+  const int c0 = (blockIdx.x * blockDim.x + threadIdx.x) * 2;
+  if (c0 >= a.cols) return;
+  for (int r = blockIdx.y * blockDim.y + threadIdx.y; r < a.rows; r += gridDim.y * blockDim.y) {
+    T v[4][2];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      v[q][0] = v[q][1] = T(0);
+      if (q < a.nsrc) {
+        const Win<T>& S = a.src[q];
+        if (r < S.rows) {
+          const T* p = S.p + (long long)r * S.ld + c0;
+          if (c0 < S.cols) v[q][0] = __ldcs(p);
+          if (c0 + 1 < S.cols) v[q][1] = __ldcs(p + 1);
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      if (j >= a.ndst) break;
+      const Win<T>& D = a.dst[j];
+      if (r >= D.rows) continue;
+      T o0 = T(0), o1 = T(0);
+      int code = a.code[j];
+#pragma unroll
+      for (int q = 0; q < 4; ++q, code >>= 2) {
+        const int cq = code & 3;
+        if (cq == 1) o0 += v[q][0], o1 += v[q][1];
+        else if (cq == 2) o0 -= v[q][0], o1 -= v[q][1];
+      }
+      T* p = D.p + (long long)r * D.ld + c0;
+      const int cmax = a.lower ? min(D.cols, r + 1) : D.cols;
+      if (c0 < cmax) __stcs(p, o0);
+      if (c0 + 1 < cmax) __stcs(p + 1, o1);
+    }
+  }
+}
+
+template <typename T>
+__global__ void postadd7_multi_kernel(const __grid_constant__ P7Batch<T> b) {
+  const P7Node<T>& a = b.n[blockIdx.z];
+  const int c0 = (blockIdx.x * blockDim.x + threadIdx.x) * 2;
+  if (c0 >= a.cols) return;
+  for (int r = blockIdx.y * blockDim.y + threadIdx.y; r < a.rows; r += gridDim.y * blockDim.y) {
+    T p[7][2];
+#pragma unroll
+    for (int i = 0; i < 7; ++i) {
+      p[i][0] = p[i][1] = T(0);
+      const Win<T>& S = a.src[i];
+      if (r < S.rows) {
+        const T* q = S.p + (long long)r * S.ld + c0;
+        if (c0 < S.cols) p[i][0] = __ldcs(q);
+        if (c0 + 1 < S.cols) p[i][1] = __ldcs(q + 1);
+      }
+    }
+    T o[4][2];
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      o[0][e] = p[0][e] + p[3][e] - p[4][e] + p[6][e];
+      o[1][e] = p[2][e] + p[4][e];
+      o[2][e] = p[1][e] + p[3][e];
+      o[3][e] = p[0][e] - p[1][e] + p[2][e] + p[5][e];
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const Win<T>& D = a.dst[j];
+      if (r >= D.rows) continue;
+      T* q = D.p + (long long)r * D.ld + c0;
+      const T sg = a.sign[j];
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        if (c0 + e < D.cols) {
+          const T v = sg * o[j][e];
+          q[e] = a.accumulate ? q[e] + v : v;
+        }
+      }
+    }
+  }
+}
+
+template <typename T>
+Win<T> win_of(const DTerm<T>& t) {
+  Win<T> w;
+  w.p = const_cast<T*>(t.p);
+  w.ld = t.ld;
+  w.rows = t.rows;
+  w.cols = t.cols;
+  return w;
+}
+template <typename T>
+Win<T> win_of(const DDest<T>& d) {
+  Win<T> w;
+  w.p = d.p;
+  w.ld = d.ld;
+  w.rows = d.rows;
+  w.cols = d.cols;
+  return w;
+}
+
+// grid for `count` nodes of at most maxcols x maxrows: ~32 blocks per SM in total
+static dim3 multi_grid(int count, int maxrows, int maxcols) {
+  const int gx = (maxcols + 2 * kMtX - 1) / (2 * kMtX);
+  long long gy = 148LL * 32 / ((long long)gx * count);
+  const long long need = (maxrows + kMtY - 1) / kMtY;
+  if (gy > need) gy = need;
+  if (gy < 1) gy = 1;
+  return dim3(gx, (unsigned)gy, count);
+}
+
+}  // namespace
+
+template <typename T>
+cudaError_t launch_combo4_multi(const EwArgs<T>* nodes, int count, cudaStream_t s) {
+  for (int i = 0; i < count;) {
+    C4Batch<T> b;
+    std::memset(&b, 0, sizeof(b));
+    int maxcols = 0;
+    for (; i < count && b.count < kC4Max; ++i) {
+      const EwArgs<T>& a = nodes[i];
+      if (a.ndst > 5 || a.rows <= 0 || a.cols <= 0) {
+        if (a.ndst > 5) return cudaErrorInvalidValue;  // the caller batches <= 5 outputs only
+        continue;
+      }
+      C4Node<T>& n = b.n[b.count++];
+      for (int q = 0; q < a.nsrc; ++q) n.src[q] = win_of(a.src[q]);
+      for (int j = 0; j < a.ndst; ++j) {
+        n.dst[j] = win_of(a.dst[j]);
+        n.code[j] = a.dst[j].coef;
+      }
+      n.nsrc = a.nsrc;
+      n.ndst = a.ndst;
+      n.rows = a.rows;
+      n.cols = a.cols;
+      n.lower = a.lower;
+      b.maxrows = b.maxrows > a.rows ? b.maxrows : a.rows;
+      maxcols = maxcols > a.cols ? maxcols : a.cols;
+    }
+    if (b.count == 0) continue;
+    combo4_multi_kernel<T><<<multi_grid(b.count, b.maxrows, maxcols), dim3(kMtX, kMtY), 0, s>>>(b);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+template <typename T>
+cudaError_t launch_postadd7_multi(const EwArgs<T>* nodes, const int* accumulate, int count, cudaStream_t s) {
+  for (int i = 0; i < count;) {
+    P7Batch<T> b;
+    std::memset(&b, 0, sizeof(b));
+    int maxcols = 0;
+    for (; i < count && b.count < kP7Max; ++i) {
+      const EwArgs<T>& a = nodes[i];
+      if (a.rows <= 0 || a.cols <= 0) continue;
+      P7Node<T>& n = b.n[b.count++];
+      for (int q = 0; q < 7; ++q) n.src[q] = win_of(a.src[q]);
+      for (int j = 0; j < 4; ++j) {
+        n.dst[j] = win_of(a.dst[j]);
+        n.sign[j] = T(a.dst[j].sign);
+      }
+      n.rows = a.rows;
+      n.cols = a.cols;
+      n.accumulate = accumulate[i];
+      b.maxrows = b.maxrows > a.rows ? b.maxrows : a.rows;
+      maxcols = maxcols > a.cols ? maxcols : a.cols;
+    }
+    if (b.count == 0) continue;
+    postadd7_multi_kernel<T><<<multi_grid(b.count, b.maxrows, maxcols), dim3(kMtX, kMtY), 0, s>>>(b);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
+template cudaError_t launch_combo4_multi<double>(const EwArgs<double>*, int, cudaStream_t);
+template cudaError_t launch_combo4_multi<float>(const EwArgs<float>*, int, cudaStream_t);
+template cudaError_t launch_postadd7_multi<double>(const EwArgs<double>*, const int*, int, cudaStream_t);
+template cudaError_t launch_postadd7_multi<float>(const EwArgs<float>*, const int*, int, cudaStream_t);
+
+}  // namespace ata

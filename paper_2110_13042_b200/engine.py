@@ -7,6 +7,8 @@ their work counter and destination turn counters.
 """
 from __future__ import annotations
 
+import os
+
 import ctypes
 from collections import OrderedDict
 
@@ -29,6 +31,13 @@ def cached_plan(key, builder):
     else:
         _PLAN_CACHE.move_to_end(key)
     return p
+
+
+def reference_dfs() -> bool:
+    """ATA_REF_DFS=1: run integer-threshold recursions with the depth-first
+    executor (planner._ReferencePlanner, the reference's per-depth scratch)
+    instead of the breadth-first one (ref_bfs.py)."""
+    return os.environ.get("ATA_REF_DFS", "0") == "1"
 
 
 def sync_ints_needed(plan, dtype_code) -> int:

@@ -110,6 +110,7 @@ class PlanBuilder:
         if group < 0 or group != self._last_group:
             self.launches += 1
         self._last_group = group if group >= 0 else None
+        self._last_ew = None
         if count:
             self.mults += m * n * (n + 1) // 2 if kind == "syrk" else m * n * k
 
@@ -121,6 +122,7 @@ class PlanBuilder:
         self.rows.append((op, 0, 0, 0, len(S), 0, len(D), 0, -1, 0, s, [_EMPTY] * nat.MAX_TERMS, d))
         self.launches += 1
         self._last_group = None
+        self._last_ew = None
 
     def combo(self, dst: Win, terms):
         self._ew(nat.OP_COMBO, [(w.clip(dst.rows, dst.cols), sg) for w, sg in terms], [(dst, 1.0)])
@@ -132,10 +134,20 @@ class PlanBuilder:
     def fill(self, dst: Win):
         self._ew(nat.OP_FILL, [], [(dst, 1.0)])
 
-    def combo4(self, sources, outputs, lower: bool = False):
+    def _ew_launch(self, op, group):
+        # consecutive COMBO4 / POSTADD7 ops of one group >= 0 share a launch
+        key = (op, group)
+        if group < 0 or key != getattr(self, "_last_ew", None):
+            self.launches += 1
+        self._last_ew = key if group >= 0 else None
+        self._last_group = None
+
+    def combo4(self, sources, outputs, lower: bool = False, group: int = -1):
         """One pass over up to 4 source windows writing up to 8 sums:
         outputs = [(dst Win, (c_0, .., c_{ns-1}))] with c_q in {0, +1, -1};
-        lower=True writes only the lower triangle of each output window."""
+        lower=True writes only the lower triangle of each output window.
+        group >= 0: consecutive combo4 ops of the group (independent nodes)
+        run as one multi-node launch."""
         if len(sources) > nat.MAX_TERMS or len(outputs) > nat.MAX_DESTS:
             raise ValueError("combo4: too many sources/outputs")
         for w in list(sources) + [o[0] for o in outputs]:
@@ -148,26 +160,25 @@ class PlanBuilder:
                 code |= (1 if cq > 0 else 2 if cq < 0 else 0) << (2 * q)
             d.append(_ref(w, 1.0, code))
         d += [_EMPTY] * (nat.MAX_DESTS - len(outputs))
-        self.rows.append((nat.OP_COMBO4, 0, 0, 0, len(sources), 0, len(outputs), int(lower), -1, 0, s,
+        self.rows.append((nat.OP_COMBO4, 0, 0, 0, len(sources), 0, len(outputs), int(lower), group, 0, s,
                           [_EMPTY] * nat.MAX_TERMS, d))
-        self.launches += 1
-        self._last_group = None
+        self._ew_launch(nat.OP_COMBO4, group)
 
     def round_tf32(self, src: Win, dst: Win):
         """dst = round-to-nearest TF32(src) (ATA_OP_ROUND)."""
         self._ew(nat.OP_ROUND, [(src, 1.0)], [(dst, 1.0)])
 
-    def postadd7(self, children, outputs, accumulate: bool):
+    def postadd7(self, children, outputs, accumulate: bool, group: int = -1):
         """Strassen post-addition of one node: children = 7 product windows
-        (P1..P7), outputs = [(C11 win, sign), (C12..), (C21..), (C22..)]."""
+        (P1..P7), outputs = [(C11 win, sign), (C12..), (C21..), (C22..)].
+        group >= 0: consecutive postadd7 ops of the group share one launch."""
         for w in list(children) + [o[0] for o in outputs]:
             self._touch(w)
         s = [_ref(w) for w in children[:4]]
         t = [_ref(w) for w in children[4:]] + [_EMPTY]
         d = [_ref(w, sg) for (w, sg) in outputs] + [_EMPTY] * (nat.MAX_DESTS - 4)
-        self.rows.append((nat.OP_POSTADD7, 0, 0, 0, 4, 3, 4, int(accumulate), -1, 0, s, t, d))
-        self.launches += 1
-        self._last_group = None
+        self.rows.append((nat.OP_POSTADD7, 0, 0, 0, 4, 3, 4, int(accumulate), group, 0, s, t, d))
+        self._ew_launch(nat.OP_POSTADD7, group)
 
     def finish(self) -> Plan:
         ops = np.array(self.rows, dtype=nat.OP_DTYPE) if self.rows else np.zeros(0, nat.OP_DTYPE)

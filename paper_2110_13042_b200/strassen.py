@@ -10,7 +10,7 @@ from __future__ import annotations
 
 import numpy as np
 
-from . import _native as nat
+from . import ref_bfs, _native as nat
 from . import engine, planner
 from .errors import ShapeMismatchError, UnsupportedSizeError, WorkspaceUndersizedError
 from .matrix import DeviceOperand, MultCounter, as_array
@@ -45,11 +45,18 @@ def fast_strassen(A, B, C, alpha=1.0, ws: StrassenWorkspace | None = None,
     elif not ws.covers(m, n, k, threshold):
         raise WorkspaceUndersizedError(
             f"workspace undersized for ({m},{n},{k}) at threshold {threshold}")
-    offs = tuple(ws.level_offsets())
-    key = ("strassen-ref", m, n, k, A_.ld, B_.ld, C_.ld, threshold, offs)
-    plan = engine.cached_plan(key, lambda: planner.plan_strassen_reference(
-        m, n, k, A_.ld, B_.ld, C_.ld, threshold, list(offs)))
-    wbuf = ws.ensure(C_.t.device) if plan.ws_scalars > 0 else None
+    if engine.reference_dfs():
+        offs = tuple(ws.level_offsets())
+        key = ("strassen-ref", m, n, k, A_.ld, B_.ld, C_.ld, threshold, offs)
+        plan = engine.cached_plan(key, lambda: planner.plan_strassen_reference(
+            m, n, k, A_.ld, B_.ld, C_.ld, threshold, list(offs)))
+        extra = 0
+    else:   # same recursion tree, executed breadth first (ref_bfs.py)
+        key = ("strassen-ref-bfs", m, n, k, A_.ld, B_.ld, C_.ld, threshold)
+        plan = engine.cached_plan(key, lambda: ref_bfs.plan_strassen_reference_bfs(
+            m, n, k, A_.ld, B_.ld, C_.ld, threshold))
+        extra = plan.ws_scalars
+    wbuf = ws.ensure(C_.t.device, extra=extra) if plan.ws_scalars > 0 else None
     engine.run_plan(plan, nat.dtype_code(C_.t.dtype), A_.ptr, A_.elems, C_.ptr, C_.elems, alpha,
                     ws=int(wbuf.data_ptr()) if wbuf is not None else 0,
                     ws_elems=int(wbuf.numel()) if wbuf is not None else 0,

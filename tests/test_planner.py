@@ -8,7 +8,7 @@ from hypothesis import strategies as st
 
 import plan_interp
 from oracle import atamul_oracle as O
-from paper_2110_13042_b200 import auto_plan, planner
+from paper_2110_13042_b200 import auto_plan, planner, ref_bfs
 from paper_2110_13042_b200.workspace import ata_calls, calls_sizes, workspace_for_calls
 from paper_2110_13042_b200.strassen import workspace_for
 from paper_2110_13042_b200.ata import workspace_for_ata
@@ -176,3 +176,86 @@ def test_auto_plan_tf32_round_and_split_contraction():
     plan_interp.run(p.ops, a, c, 1.0, WS=np.full(max(1, p.ws_scalars), np.nan, dtype=np.float32))
     assert np.all(c[np.triu_indices(n, 1)] == 5.0)
     assert O.rel_frobenius_lower(c, O.gram_blas(a)) <= 1e-4
+
+
+# ---------------------------------------------------------- breadth-first reference plans
+
+def _bfs_plan(m, n, t, budget=ref_bfs.DEFAULT_BUDGET):
+    return ref_bfs.plan_ata_reference_bfs(m, n, n, n, t, budget)
+
+
+def test_bfs_reference_plan_counts(golden):
+    """Same recursion tree as the reference: the exact MultCounter totals."""
+    meta, _ = golden
+    for key, want in meta["counts"].items():
+        parts = key.split("_")
+        if parts[0] == "ata" and parts[1] == "square":
+            n, t = int(parts[2]), int(parts[3][1:])
+            m = n
+        elif parts[0] == "ata":
+            m, n = map(int, parts[1].split("x"))
+            t = int(parts[2][1:])
+        else:
+            n = int(parts[2])
+            p = ref_bfs.plan_strassen_reference_bfs(n, n, n, n, n, n, 1)
+            assert p.mults == want, key
+            continue
+        assert _bfs_plan(m, n, t).mults == want, key
+        # a tiny scratch budget forces the depth-first fallback: same tree
+        assert _bfs_plan(m, n, t, budget=64).mults == want, key
+
+
+@pytest.mark.parametrize("budget", [ref_bfs.DEFAULT_BUDGET, 200])
+def test_bfs_reference_plan_semantics(golden, budget):
+    """Every golden AtA / Strassen case through the interpreter: reference
+    results (1e-12 / 1e-5), strict upper triangle untouched."""
+    meta, arrays = golden
+    for case in meta["cases"]:
+        key = case["key"]
+        if case["kind"] == "ata":
+            a = arrays[key + "_A"]
+            m, n = a.shape
+            p = _bfs_plan(m, n, case["threshold"], budget)
+            c = np.zeros((n, n), dtype=a.dtype)
+            c[np.triu_indices(n, 1)] = 1.0e30
+            plan_interp.run(p.ops, a, c, case["alpha"],
+                            WS=np.full(max(1, p.ws_scalars), np.nan, dtype=a.dtype))
+            tol = 1e-12 if a.dtype == np.float64 else 1e-5
+            assert O.rel_frobenius_lower(c, arrays[key + "_C"]) <= tol, key
+            assert np.all(c[np.triu_indices(n, 1)] == 1.0e30), key
+        else:
+            a, b, c0 = arrays[key + "_A"], arrays[key + "_B"], arrays[key + "_C0"]
+            m, n = a.shape
+            k = b.shape[1]
+            p = ref_bfs.plan_strassen_reference_bfs(m, n, k, n, k, k, case["threshold"], budget)
+            c = c0.copy()
+            plan_interp.run(p.ops, a, c, 1.0, WS=np.full(max(1, p.ws_scalars), np.nan), B=b)
+            assert np.abs(c - arrays[key + "_C"]).max() <= 1e-12 * m, key
+
+
+@pytest.mark.parametrize("shape", [(97, 83, 64), (50, 37, 1), (50, 37, 64), (33, 17, 2), (9, 40, 3)])
+def test_bfs_reference_plan_groups_write_disjoint(shape):
+    """Within one launch group no two ops write the same element (rounds),
+    including nested diagonal leaves of uneven splits (threshold 1)."""
+    p = _bfs_plan(*shape)
+    groups = {}
+    for op in p.ops:
+        g = int(op["group"])
+        if g >= 0:
+            groups.setdefault(g, []).append(op)
+    assert len(groups) >= 1
+    for g, ops in groups.items():
+        seen = set()
+        for op in ops:
+            cells = set(_dest_cells(op, shape[1]))
+            assert not (cells & seen), f"group {g}: two writers"
+            seen |= cells
+
+
+def test_bfs_reference_plan_launches():
+    """c2-shaped recursion: far fewer launches than the depth-first executor."""
+    m, n, t = 6001, 4097, 256 * 256
+    p = _bfs_plan(m, n, t)
+    d = planner.plan_ata_reference(m, n, n, n, t, workspace_for_ata(m, n, t).level_offsets())
+    assert p.mults == d.mults
+    assert p.launches * 10 < d.launches
