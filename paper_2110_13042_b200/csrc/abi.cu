@@ -10,6 +10,7 @@
 #include <cstring>
 #include <string>
 #include <algorithm>
+#include <map>
 #include <vector>
 
 #include "../../include/atamul_b200.h"
@@ -193,13 +194,16 @@ bool supports_ordering<float>() { return false; }
 // Consecutive GEMM/SYRK ops with equal group >= 0 share a launch (at most
 // kMaxBatch); when the launcher cannot order shared destinations, a product
 // whose region already occurs in the open batch starts a new launch.
+// on_batch(first, last, cont): cont = the group continues in the next launch
+// (the batch was cut at kMaxBatch products), so the two may run concurrently
+// when neither orders shared destinations.
 template <typename F1, typename F2, typename F3>
 int walk_batches(const ata_op* ops, int n_ops, bool ordering, F1 on_batch, F2 on_ew, F3 on_ew_run) {
   int first = -1, group = -1, count = 0;
   std::vector<int> regions;
-  auto flush = [&](int end) -> int {
+  auto flush = [&](int end, bool cont = false) -> int {
     int rc = ATA_OK;
-    if (count > 0) rc = on_batch(first, end);
+    if (count > 0) rc = on_batch(first, end, cont);
     first = -1;
     count = 0;
     regions.clear();
@@ -209,14 +213,17 @@ int walk_batches(const ata_op* ops, int n_ops, bool ordering, F1 on_batch, F2 on
     const ata_op& op = ops[i];
     int rc;
     if (op.type == ATA_OP_GEMM || op.type == ATA_OP_SYRK) {
-      bool join = count > 0 && op.group >= 0 && op.group == group && count < ata::kMaxBatch;
+      const bool same = count > 0 && op.group >= 0 && op.group == group;
+      bool join = same && count < ata::kMaxBatch;
+      bool conflict = false;
       if (join && !ordering) {
-        for (int j = 0; j < op.nd && join; ++j)
+        for (int j = 0; j < op.nd && !conflict; ++j)
           if (op.d[j].region > 0)
             for (int r : regions)
-              if (r == op.d[j].region) join = false;
+              if (r == op.d[j].region) conflict = true;
+        join = !conflict;
       }
-      if (!join && (rc = flush(i))) return rc;
+      if (!join && (rc = flush(i, same && !conflict))) return rc;
       if (count == 0) first = i;
       ++count;
       group = op.group;
@@ -262,6 +269,30 @@ int64_t batch_sync_ints(const ata_op* ops, int first, int last) {
   return total;
 }
 
+// Auxiliary streams + events of the current device for concurrent product
+// launches (created once; the first plan runs before any graph capture).
+struct ForkJoin {
+  static constexpr int K = 4;
+  cudaStream_t aux[K];
+  cudaEvent_t fork, done[K];
+  bool ok = false;
+  static ForkJoin& get() {
+    static std::map<int, ForkJoin> per_device;
+    int dev = 0;
+    cudaGetDevice(&dev);
+    auto it = per_device.find(dev);
+    if (it != per_device.end()) return it->second;
+    ForkJoin& f = per_device[dev];
+    bool ok = cudaEventCreateWithFlags(&f.fork, cudaEventDisableTiming) == cudaSuccess;
+    for (int k = 0; k < K && ok; ++k)
+      ok = cudaStreamCreateWithFlags(&f.aux[k], cudaStreamNonBlocking) == cudaSuccess &&
+           cudaEventCreateWithFlags(&f.done[k], cudaEventDisableTiming) == cudaSuccess;
+    f.ok = ok;
+    if (!ok) cudaGetLastError();  // fall back to one stream
+    return f;
+  }
+};
+
 template <typename T>
 ata::EwArgs<T> combo4_args(const ata_op& op, const Bases& b) {
   ata::EwArgs<T> a;
@@ -303,7 +334,7 @@ int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, int* sync, int64_t 
   }
   const bool ordering = supports_ordering<T>();
   ata::BatchArgs<T> batch;
-  auto on_batch = [&](int first, int last) -> int {
+  auto launch_one = [&](int first, int last, cudaStream_t s) -> int {
     std::memset(&batch, 0, sizeof(batch));
     batch.alpha = alpha;
     const int64_t need = batch_sync_ints(ops, first, last);
@@ -346,7 +377,56 @@ int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, int* sync, int64_t 
     if (e != cudaSuccess) return cuda_fail(e, "product launch");
     return ATA_OK;
   };
+  // Launches of one product group cut at kMaxBatch are independent: unless they
+  // order shared destinations (turn counters in the sync buffer), they run
+  // concurrently on auxiliary streams forked from / joined back into `s`, so
+  // groups of many small products fill the machine (graph-capturable).
+  ForkJoin& fj = ForkJoin::get();
+  bool prev_cont = false;
+  int aux_next = 0;
+  bool forked = false, aux_used[ForkJoin::K] = {false};
+  auto join_all = [&]() -> int {
+    if (!forked) return ATA_OK;
+    for (int k = 0; k < ForkJoin::K; ++k)
+      if (aux_used[k]) {
+        if (cudaEventRecord(fj.done[k], fj.aux[k]) != cudaSuccess ||
+            cudaStreamWaitEvent(s, fj.done[k], 0) != cudaSuccess)
+          return cuda_fail(cudaGetLastError(), "stream join");
+        aux_used[k] = false;
+      }
+    forked = false;
+    return ATA_OK;
+  };
+  auto on_batch = [&](int first, int last, bool cont) -> int {
+    bool regions = false;
+    for (int i = first; i < last && !regions; ++i)
+      for (int j = 0; j < ops[i].nd; ++j) regions = regions || ops[i].d[j].region > 0;
+    const bool concurrent = (cont || prev_cont) && !regions && fj.ok;
+    if (!prev_cont || !concurrent) {  // a new group (or an ordered batch): serialise behind all prior work
+      if (int rc = join_all()) return rc;
+    }
+    prev_cont = cont;
+    cudaStream_t ls = s;
+    if (concurrent) {
+      if (!forked) {
+        if (cudaEventRecord(fj.fork, s) != cudaSuccess) return cuda_fail(cudaGetLastError(), "stream fork");
+        forked = true;
+        aux_next = 0;
+      }
+      const int k = aux_next++ % ForkJoin::K;
+      if (!aux_used[k]) {
+        if (cudaStreamWaitEvent(fj.aux[k], fj.fork, 0) != cudaSuccess)
+          return cuda_fail(cudaGetLastError(), "stream fork");
+        aux_used[k] = true;
+      }
+      ls = fj.aux[k];
+    }
+    if (int rc = launch_one(first, last, ls)) return rc;
+    if (!cont) return join_all();
+    return ATA_OK;
+  };
   auto on_ew = [&](int i) -> int {
+    if (int rc = join_all()) return rc;
     const ata_op& op = ops[i];
     cudaError_t e = cudaSuccess;
     if (op.type == ATA_OP_COMBO || op.type == ATA_OP_UPDATE) {
@@ -385,6 +465,7 @@ int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, int* sync, int64_t 
     return ATA_OK;
   };
   auto on_ew_run = [&](int first, int last) -> int {
+    if (int rc = join_all()) return rc;
     std::vector<ata::EwArgs<T>> args;
     std::vector<int> acc;
     args.reserve(last - first);
@@ -409,7 +490,9 @@ int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, int* sync, int64_t 
     if (e != cudaSuccess) return cuda_fail(e, "elementwise launch");
     return ATA_OK;
   };
-  return walk_batches(ops, n_ops, ordering, on_batch, on_ew, on_ew_run);
+  int rc = walk_batches(ops, n_ops, ordering, on_batch, on_ew, on_ew_run);
+  int rj = join_all();
+  return rc ? rc : rj;
 }
 
 }  // namespace
@@ -441,7 +524,7 @@ int64_t ata_sync_ints_needed(int dtype, const ata_op* ops, int32_t n_ops) {
   int64_t need = 1;
   walk_batches(
       ops, n_ops, ordering,
-      [&](int first, int last) -> int {
+      [&](int first, int last, bool) -> int {
         need = std::max(need, batch_sync_ints(ops, first, last));
         return ATA_OK;
       },
