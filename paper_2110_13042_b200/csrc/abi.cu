@@ -11,6 +11,7 @@
 #include <string>
 #include <algorithm>
 #include <map>
+#include <type_traits>
 #include <vector>
 
 #include "../../include/atamul_b200.h"
@@ -198,8 +199,10 @@ bool supports_ordering<float>() { return false; }
 // (the batch was cut at kMaxBatch products), so the two may run concurrently
 // when neither orders shared destinations.
 template <typename F1, typename F2, typename F3>
-int walk_batches(const ata_op* ops, int n_ops, bool ordering, F1 on_batch, F2 on_ew, F3 on_ew_run) {
+int walk_batches(const ata_op* ops, int n_ops, bool ordering, bool narrow, F1 on_batch, F2 on_ew,
+                 F3 on_ew_run) {
   int first = -1, group = -1, count = 0;
+  bool all_narrow = true;  // every product of the open batch has <= kNarrowDests destinations
   std::vector<int> regions;
   auto flush = [&](int end, bool cont = false) -> int {
     int rc = ATA_OK;
@@ -214,7 +217,8 @@ int walk_batches(const ata_op* ops, int n_ops, bool ordering, F1 on_batch, F2 on
     int rc;
     if (op.type == ATA_OP_GEMM || op.type == ATA_OP_SYRK) {
       const bool same = count > 0 && op.group >= 0 && op.group == group;
-      bool join = same && count < ata::kMaxBatch;
+      const int cap = (narrow && all_narrow && op.nd <= ata::kNarrowDests) ? ata::kMaxBatchNarrow : ata::kMaxBatch;
+      bool join = same && count < cap;
       bool conflict = false;
       if (join && !ordering) {
         for (int j = 0; j < op.nd && !conflict; ++j)
@@ -224,7 +228,11 @@ int walk_batches(const ata_op* ops, int n_ops, bool ordering, F1 on_batch, F2 on
         join = !conflict;
       }
       if (!join && (rc = flush(i, same && !conflict))) return rc;
-      if (count == 0) first = i;
+      if (count == 0) {
+        first = i;
+        all_narrow = true;
+      }
+      all_narrow = all_narrow && op.nd <= ata::kNarrowDests;
       ++count;
       group = op.group;
       for (int j = 0; j < op.nd; ++j)
@@ -272,7 +280,7 @@ int64_t batch_sync_ints(const ata_op* ops, int first, int last) {
 // Auxiliary streams + events of the current device for concurrent product
 // launches (created once; the first plan runs before any graph capture).
 struct ForkJoin {
-  static constexpr int K = 4;
+  static constexpr int K = 8;
   cudaStream_t aux[K];
   cudaEvent_t fork, done[K];
   bool ok = false;
@@ -334,20 +342,16 @@ int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, int* sync, int64_t 
   }
   const bool ordering = supports_ordering<T>();
   ata::BatchArgs<T> batch;
-  auto launch_one = [&](int first, int last, cudaStream_t s) -> int {
-    std::memset(&batch, 0, sizeof(batch));
+  static ata::BatchArgsNarrow64 nbatch;  // 28 KB: not on the stack
+  const bool narrow = std::is_same<T, double>::value && ata::f64_narrow_supported();
+  auto fill_batch = [&](auto& batch, int first, int last) {
     batch.alpha = alpha;
-    const int64_t need = batch_sync_ints(ops, first, last);
-    if (ordering && need > 1 && (sync == nullptr || need > sync_ints))
-      return fail(ATA_E_WORKSPACE, "workspace undersized: sync buffer needs " +
-                                       std::to_string(need) + " ints, have " +
-                                       std::to_string(sync_ints));
     batch.sync = sync;
     batch.n_sync = (int)(sync_ints < 0x7fffffff ? sync_ints : 0x7fffffff);
     std::vector<int> ids;  // batch-local region numbering (1-based)
     for (int i = first; i < last; ++i) {
       const ata_op& op = ops[i];
-      ata::DProd<T>& p = batch.p[batch.count++];
+      auto& p = batch.p[batch.count++];
       p.kind = op.type == ATA_OP_SYRK ? ata::kSyrk : ata::kGemm;
       p.m = op.m;
       p.n = op.n;
@@ -373,6 +377,27 @@ int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, int* sync, int64_t 
         }
       }
     }
+  };
+  auto launch_one = [&](int first, int last, cudaStream_t s) -> int {
+    const int64_t need = batch_sync_ints(ops, first, last);
+    if (ordering && need > 1 && (sync == nullptr || need > sync_ints))
+      return fail(ATA_E_WORKSPACE, "workspace undersized: sync buffer needs " +
+                                       std::to_string(need) + " ints, have " +
+                                       std::to_string(sync_ints));
+    bool nb = narrow;
+    for (int i = first; i < last && nb; ++i) nb = ops[i].nd <= ata::kNarrowDests;
+    if (!nb && last - first > ata::kMaxBatch) return fail(ATA_E_ARG, "internal: oversized product batch");
+    if (nb) {
+      if constexpr (std::is_same<T, double>::value) {
+        std::memset(&nbatch, 0, sizeof(nbatch));
+        fill_batch(nbatch, first, last);
+        cudaError_t e = ata::launch_batch_f64_narrow(nbatch, s);
+        if (e != cudaSuccess) return cuda_fail(e, "product launch");
+        return ATA_OK;
+      }
+    }
+    std::memset(&batch, 0, sizeof(batch));
+    fill_batch(batch, first, last);
     cudaError_t e = launch_batch<T>(batch, s, dtype);
     if (e != cudaSuccess) return cuda_fail(e, "product launch");
     return ATA_OK;
@@ -490,7 +515,7 @@ int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, int* sync, int64_t 
     if (e != cudaSuccess) return cuda_fail(e, "elementwise launch");
     return ATA_OK;
   };
-  int rc = walk_batches(ops, n_ops, ordering, on_batch, on_ew, on_ew_run);
+  int rc = walk_batches(ops, n_ops, ordering, narrow, on_batch, on_ew, on_ew_run);
   int rj = join_all();
   return rc ? rc : rj;
 }
@@ -521,9 +546,10 @@ int ata_abi_op_size(void) { return (int)sizeof(ata_op); }
 int64_t ata_sync_ints_needed(int dtype, const ata_op* ops, int32_t n_ops) {
   if (n_ops <= 0 || ops == nullptr) return 1;
   const bool ordering = dtype == ATA_F64 ? ata::f64_supports_ordering() : false;
+  const bool narrow = dtype == ATA_F64 && ata::f64_narrow_supported();
   int64_t need = 1;
   walk_batches(
-      ops, n_ops, ordering,
+      ops, n_ops, ordering, narrow,
       [&](int first, int last, bool) -> int {
         need = std::max(need, batch_sync_ints(ops, first, last));
         return ATA_OK;

@@ -30,8 +30,8 @@ struct DDest {  // truncated write window
 
 enum : int { kGemm = 0, kSyrk = 1 };
 
-template <typename T>
-struct DProd {
+template <typename T, int MAXD>
+struct DProdT {
   int kind;        // kGemm / kSyrk
   int m, n, k;     // contraction, output rows, output cols
   int ns, nt, nd;  // term / dest counts
@@ -40,11 +40,13 @@ struct DProd {
   int tile_begin;  // prefix offset of this product in the launch's tile space
   int _pad;
   DTerm<T> s[2], t[2];
-  DDest<T> d[kMaxDests];
+  DDest<T> d[MAXD];
 };
-
 template <typename T>
-struct BatchArgs {
+using DProd = DProdT<T, kMaxDests>;
+
+template <typename T, int MAXD, int MAXB>
+struct BatchArgsT {
   int count;
   int total_tiles;
   double alpha;
@@ -52,8 +54,17 @@ struct BatchArgs {
   int n_sync;  // ints available at sync
   int dynamic; // 1: tiles handed out by the work counter (needed for ordered destinations)
   int dbg;     // experiment flags (ATA_DBG): 1 = skip ordering waits, 2 = skip epilogue
-  DProd<T> p[kMaxBatch];
+  DProdT<T, MAXD> p[MAXB];
 };
+template <typename T>
+using BatchArgs = BatchArgsT<T, kMaxDests, kMaxBatch>;
+
+// Narrow FP64 batches: products with <= 2 destinations (every planner's leaves)
+// fit 104 to a launch (28 KB of parameters) instead of 48 -- groups of many
+// small leaf products then give each persistent CTA several tiles.
+constexpr int kNarrowDests = 2;
+constexpr int kMaxBatchNarrow = 104;
+using BatchArgsNarrow64 = BatchArgsT<double, kNarrowDests, kMaxBatchNarrow>;
 
 template <typename T>
 struct EwArgs {  // elementwise op: rows x cols iteration space
@@ -67,6 +78,8 @@ struct EwArgs {  // elementwise op: rows x cols iteration space
 // ---- host launchers (defined in gemm_*.cu / elementwise.cu) ----
 cudaError_t launch_batch_f64(const BatchArgs<double>& a, cudaStream_t s);
 cudaError_t launch_batch_f64_ws(const BatchArgs<double>& a, cudaStream_t s);
+cudaError_t launch_batch_f64_narrow(const BatchArgsNarrow64& a, cudaStream_t s);
+bool f64_narrow_supported();
 bool f64_supports_ordering();
 cudaError_t launch_batch_f32(const BatchArgs<float>& a, cudaStream_t s, bool split);
 template <typename T> cudaError_t launch_combo(const EwArgs<T>& a, cudaStream_t s);

@@ -308,6 +308,8 @@ static int pick_cfg() {
 }
 
 bool f64_supports_ordering() { return pick_cfg() == 4; }
+bool f64_narrow_supported() { return pick_cfg() == 4; }
+cudaError_t launch_batch_f64_ws_narrow(const BatchArgsNarrow64& a, cudaStream_t s);
 
 template <int NS, int NT>
 static cudaError_t launch_terms(const BatchArgs<double>& a, cudaStream_t s) {
@@ -318,6 +320,12 @@ static cudaError_t launch_terms(const BatchArgs<double>& a, cudaStream_t s) {
     case 4: return launch_batch_f64_ws(a, s);
     default: return launch_cfg<CfgB, NS, NT>(a, s);
   }
+}
+
+// Narrow batches go to the persistent warp-specialised kernel in one launch
+// (the executor forms them only when f64_narrow_supported()).
+cudaError_t launch_batch_f64_narrow(const BatchArgsNarrow64& a, cudaStream_t s) {
+  return launch_batch_f64_ws_narrow(a, s);
 }
 
 cudaError_t launch_batch_f64(const BatchArgs<double>& a, cudaStream_t s) {

@@ -148,10 +148,11 @@ struct TileInfo {
   int pi, ti, tj;
 };
 
-__device__ __forceinline__ TileInfo decode_tile(const BatchArgs<double>& args, int tile) {
+template <typename Args>
+__device__ __forceinline__ TileInfo decode_tile(const Args& args, int tile) {
   int pi = 0;
   while (pi + 1 < args.count && tile >= args.p[pi + 1].tile_begin) ++pi;
-  const DProd<double>& P = args.p[pi];
+  const auto& P = args.p[pi];
   const int local = tile - P.tile_begin;
   TileInfo t;
   t.pi = pi;
@@ -174,9 +175,9 @@ __device__ __forceinline__ TileInfo decode_tile(const BatchArgs<double>& args, i
   return t;
 }
 
-template <int BK, int NS, int NT, int STAGES>
+template <int BK, int NS, int NT, int STAGES, typename Args>
 __global__ void __launch_bounds__(ws64::THREADS, 1)
-    prod_f64_ws_kernel(const __grid_constant__ BatchArgs<double> args) {
+    prod_f64_ws_kernel(const __grid_constant__ Args args) {
   using namespace ws64;
   constexpr int BUF = BK * LD;  // doubles per operand buffer
   constexpr int STAGE = (NS + NT) * BUF;
@@ -222,7 +223,7 @@ __global__ void __launch_bounds__(ws64::THREADS, 1)
       }
       if (tile >= args.total_tiles) break;
       const TileInfo tl = decode_tile(args, tile);
-      const DProd<double>& P = args.p[tl.pi];
+      const auto& P = args.p[tl.pi];
       const bool syrk = P.kind == kSyrk;
       const bool same = syrk && tl.ti == tl.tj;
       const int ns = P.ns, nt = syrk ? 1 : P.nt;
@@ -306,7 +307,7 @@ __global__ void __launch_bounds__(ws64::THREADS, 1)
     if (lane == 0) mbar_arrive(&tempty[slot]);
     if (tile >= args.total_tiles) break;
     const TileInfo tl = decode_tile(args, tile);
-    const DProd<double>& P = args.p[tl.pi];
+    const auto& P = args.p[tl.pi];
     const bool syrk = P.kind == kSyrk;
     const bool same = syrk && tl.ti == tl.tj;
     const int i0 = tl.ti * BM, j0 = tl.tj * BN;
@@ -421,12 +422,12 @@ static int num_sms() {
   return n;
 }
 
-template <int BK, int NS, int NT>
-static cudaError_t launch_ws(BatchArgs<double> a, cudaStream_t s) {
+template <int BK, int NS, int NT, typename Args>
+static cudaError_t launch_ws(Args a, cudaStream_t s) {
   using namespace ws64;
   long long total = 0;
   for (int i = 0; i < a.count; ++i) {
-    DProd<double>& p = a.p[i];
+    auto& p = a.p[i];
     p.tn = (p.n + BM - 1) / BM;
     p.tk = (p.k + BN - 1) / BN;
     p.tile_begin = (int)total;
@@ -482,7 +483,7 @@ static cudaError_t launch_ws(BatchArgs<double> a, cudaStream_t s) {
   static_assert(STAGES >= 2, "smem");
   const size_t smem = (size_t)STAGES * STAGE_BYTES + (2 * STAGES + 2 * TSLOTS) * sizeof(uint64_t) +
                       (TSLOTS + 2) * sizeof(int);
-  auto kern = prod_f64_ws_kernel<BK, NS, NT, STAGES>;
+  auto kern = prod_f64_ws_kernel<BK, NS, NT, STAGES, Args>;
   static bool attr_set = false;
   if (!attr_set) {
     e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -494,7 +495,8 @@ static cudaError_t launch_ws(BatchArgs<double> a, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_batch_f64_ws(const BatchArgs<double>& a, cudaStream_t s) {
+template <typename Args>
+static cudaError_t launch_ws_any(const Args& a, cudaStream_t s) {
   int ns = 1, nt = 1;
   for (int i = 0; i < a.count; ++i) {
     ns = max(ns, a.p[i].ns);
@@ -516,5 +518,8 @@ cudaError_t launch_batch_f64_ws(const BatchArgs<double>& a, cudaStream_t s) {
   if (ns == 1 && nt == 2) return launch_ws<16, 1, 2>(a, s);
   return launch_ws<16, 2, 2>(a, s);
 }
+
+cudaError_t launch_batch_f64_ws(const BatchArgs<double>& a, cudaStream_t s) { return launch_ws_any(a, s); }
+cudaError_t launch_batch_f64_ws_narrow(const BatchArgsNarrow64& a, cudaStream_t s) { return launch_ws_any(a, s); }
 
 }  // namespace ata

@@ -14,9 +14,9 @@ first with one scratch buffer per depth, so on a GPU every tiny node becomes
 its own launch (config c2: 16586 ops, 8006 launches).  Here all Strassen calls
 are expanded breadth first with private buffers per node:
 
-  1. operand sums, top-down, one multi-node ``combo4`` launch per level (a
-     node's children that are leaves take their two-term operands fused into
-     the product's tile load instead -- strassen.py:195-203 without a buffer);
+  1. operand sums, top-down, one multi-node ``combo4`` launch per level
+     (strassen.py:195-203; ``fused_leaves=True`` instead lets leaf children
+     take their two-term operands fused into the product's tile load);
   2. all leaf products into private product buffers in few persistent
      launches (up to 48 products each);
   3. post-additions bottom-up, one multi-node ``postadd7`` launch per level
@@ -47,7 +47,7 @@ DEFAULT_BUDGET = 2_000_000_000      # scratch scalars per wave (16 GB of fp64)
 
 
 class _Node:
-    __slots__ = ("S", "T", "m", "n", "k", "out", "acc", "sign", "level", "kids", "sums")
+    __slots__ = ("S", "T", "m", "n", "k", "out", "acc", "sign", "level", "kids", "sums", "merged")
 
     def __init__(self, S, T, m, n, k, out, acc, sign, level):
         self.S, self.T = S, T            # operand terms [(Win, sign)] (internal nodes: one view)
@@ -56,6 +56,7 @@ class _Node:
         self.level = level
         self.kids = None
         self.sums = None                 # (A quadrants, [(Win, coefs)], B quadrants, [(Win, coefs)])
+        self.merged = False              # merged reference leaves: a leaf whatever its size
 
 
 def _quads(w: Win, r1: int, c1: int):
@@ -64,9 +65,14 @@ def _quads(w: Win, r1: int, c1: int):
 
 
 class _RefBFS:
-    def __init__(self, threshold: int, budget: int = DEFAULT_BUDGET):
+    def __init__(self, threshold: int, budget: int = DEFAULT_BUDGET, fused_leaves: bool = False):
         self.t = int(threshold)
         self.budget = int(budget)
+        # False: leaf children read materialized operand sums (one multi-node
+        # combo4 pass per level; 1-term products run ~1.6x faster than the
+        # 2-term fused loads at these small sizes -- tools/prof_small.py)
+        self.fused_leaves = fused_leaves
+        self.extra = []          # C writers joining the next leaf group (diagonal SYRKs)
         self.pb = PlanBuilder("reference")
         self.ws_top = 0
         self.ws_peak = 0
@@ -80,7 +86,7 @@ class _RefBFS:
 
     # ------------------------------------------------------------ expansion
     def _leaf(self, node: _Node) -> bool:
-        return is_base_case(node.m, node.n, node.k, self.t)
+        return node.merged or is_base_case(node.m, node.n, node.k, self.t)
 
     def split(self, node: _Node, materialize_all: bool = False):
         """Children of an internal node (its S and T are single windows)."""
@@ -92,7 +98,7 @@ class _RefBFS:
         for i, (s_shape, s_terms, t_shape, t_terms, _) in enumerate(_strassen_products(a, b, node.out)):
             ms, ns = s_shape if s_shape else (s_terms[0][0].rows, s_terms[0][0].cols)
             _, kt = t_shape if t_shape else (t_terms[0][0].rows, t_terms[0][0].cols)
-            leaf = is_base_case(ms, ns, kt, self.t) and not materialize_all
+            leaf = is_base_case(ms, ns, kt, self.t) and not materialize_all and self.fused_leaves
             if leaf or not s_shape:
                 S = [(w, sg) for (w, sg) in s_terms]
             else:
@@ -161,17 +167,33 @@ class _RefBFS:
             q = _quads(nd.out, n1, k1)
             self.pb.postadd7([kid.out for kid in nd.kids], [(w, nd.sign) for w in q], accumulate, group=g)
 
-    def _products(self, leaves):
+    def _emit_item(self, it, group, private):
+        if isinstance(it, tuple):                      # ("syrk", a, c): diagonal leaf
+            _, a, c = it
+            self.pb.product("syrk", a.rows, a.cols, a.cols, [(a, 1.0)], [], [(c, 1.0)],
+                            accumulate=1, group=group)
+        else:
+            self.pb.product("gemm", it.m, it.n, it.k, it.S, it.T, [(it.out, it.sign)],
+                            accumulate=0 if private else 1, group=group)
+
+    def _products(self, leaves, extra=()):
+        """Leaf products: one group holding every private leaf plus the first
+        round of C writers (diagonal SYRKs, Strassen calls that are leaves --
+        the long ones, issued first), then one group per further round."""
         private = [l for l in leaves if not l.acc]
-        shared = [l for l in leaves if l.acc]
-        if private:
+        shared = list(extra) + [l for l in leaves if l.acc]
+        rounds = self._rounds_rect(shared, lambda it: it[2] if isinstance(it, tuple) else it.out)
+        first = rounds[0] if rounds else []
+        if private or first:
             g = self.pb.new_group()
+            for it in first:
+                self._emit_item(it, g, False)
             for l in private:
-                self.pb.product("gemm", l.m, l.n, l.k, l.S, l.T, [(l.out, l.sign)], accumulate=0, group=g)
-        for rnd in self._rounds_rect(shared, lambda l: l.out):
+                self._emit_item(l, g, True)
+        for rnd in rounds[1:]:
             g = self.pb.new_group()
-            for l in rnd:
-                self.pb.product("gemm", l.m, l.n, l.k, l.S, l.T, [(l.out, l.sign)], accumulate=1, group=g)
+            for it in rnd:
+                self._emit_item(it, g, False)
 
     def emit_wave(self, roots):
         """Breadth-first execution of independent Strassen calls."""
@@ -180,7 +202,8 @@ class _RefBFS:
             self.expand(r, levels, leaves)
         for lv in sorted(levels):
             self._combo([nd for nd in levels[lv] if nd.sums[1] or nd.sums[3]])
-        self._products(leaves)
+        extra, self.extra = self.extra, []
+        self._products(leaves, extra)
         for lv in sorted(levels, reverse=True):
             inner = [nd for nd in levels[lv] if not nd.acc]
             if inner:
@@ -189,13 +212,50 @@ class _RefBFS:
                 self._post(rnd, True)
 
     def need(self, node: _Node) -> int:
-        probe = _RefBFS(self.t, self.budget)
-        probe.expand(_Node(node.S, node.T, node.m, node.n, node.k, node.out, node.acc, node.sign, 0),
-                     defaultdict(list), [])
+        probe = _RefBFS(self.t, self.budget, self.fused_leaves)
+        copy = _Node(node.S, node.T, node.m, node.n, node.k, node.out, node.acc, node.sign, 0)
+        copy.merged = node.merged
+        probe.expand(copy, defaultdict(list), [])
         return probe.ws_peak
+
+    def _merge_leaf_roots(self, roots):
+        """Strassen calls that are leaves themselves (strassen.py:38-41) and add
+        into the same C block from vertically adjacent row blocks (the two
+        calls of an AtA node, ata.py:114-115, and the nodes of every row block
+        of one column block) are one classical product over the union of
+        their rows: the same scalar multiplications, one launch slot."""
+        out, runs, order = [], {}, []
+        for r in roots:
+            if not (r.acc and self._leaf(r) and len(r.S) == 1 and len(r.T) == 1):
+                out.append(r)
+                continue
+            (x, sx), (y, sy) = r.S[0], r.T[0]
+            key = (r.out, r.sign, sx, sy, x.base, x.ld, x.off % x.ld, x.cols, y.base, y.ld, y.off % y.ld, y.cols)
+            if key not in runs:
+                runs[key] = []
+                order.append(key)
+            runs[key].append(r)
+        for key in order:
+            rs = sorted(runs[key], key=lambda r: r.S[0][0].off)
+            cur = rs[0]
+            for r in rs[1:]:
+                x, y = cur.S[0][0], cur.T[0][0]
+                x2, y2 = r.S[0][0], r.T[0][0]
+                if x2.off == x.off + x.rows * x.ld and y2.off == y.off + y.rows * y.ld and x2.rows == y2.rows:
+                    X = Win(x.base, x.off, x.ld, x.rows + x2.rows, x.cols)
+                    Y = Win(y.base, y.off, y.ld, y.rows + y2.rows, y.cols)
+                    cur = _Node([(X, cur.S[0][1])], [(Y, cur.T[0][1])], X.rows, cur.n, cur.k, cur.out, True,
+                                cur.sign, 0)
+                    cur.merged = True
+                else:
+                    out.append(cur)
+                    cur = r
+            out.append(cur)
+        return out
 
     def calls(self, roots):
         """Waves of calls whose breadth-first scratch fits the budget."""
+        roots = self._merge_leaf_roots(roots)
         wave, wave_need = [], 0
         for r in roots:
             need = self.need(r)
@@ -258,12 +318,39 @@ class _RefBFS:
                 roots.append(_Node([(x, 1.0)], [(y, 1.0)], x.rows, x.cols, y.cols, c21, True, 1.0, 0))
 
         rec(A, C)
-        for rnd in self._rounds_rect(syrk, lambda ac: ac[1]):
-            g = self.pb.new_group()
-            for (a, c) in rnd:
-                self.pb.product("syrk", a.rows, a.cols, a.cols, [(a, 1.0)], [], [(c, 1.0)],
-                                accumulate=1, group=g)
+        self.extra = [("syrk", a, c) for (a, c) in self._merge_syrk(syrk)]
         self.calls(roots)
+        if self.extra:                                 # no Strassen call took them
+            extra, self.extra = self.extra, []
+            self._products([], extra)
+
+    @staticmethod
+    def _merge_syrk(leaves):
+        """Diagonal leaves that accumulate into the same C block from vertically
+        adjacent row blocks of the same columns (ata.py:110-113 sends every row
+        block of a column block to the same C block) are one SYRK over the
+        union of their rows: the same scalar multiplications (sum over the row
+        blocks of m_r * n(n+1)/2), one product instead of one per row block."""
+        runs = {}
+        order = []
+        for (a, c) in leaves:
+            key = (c, a.base, a.ld, a.off % a.ld, a.cols)
+            if key not in runs:
+                runs[key] = []
+                order.append(key)
+            runs[key].append(a)
+        out = []
+        for key in order:
+            blocks = sorted(runs[key], key=lambda w: w.off)
+            cur = blocks[0]
+            for w in blocks[1:]:
+                if w.off == cur.off + cur.rows * cur.ld:      # the next rows of the same columns
+                    cur = Win(cur.base, cur.off, cur.ld, cur.rows + w.rows, cur.cols)
+                else:
+                    out.append((cur, key[0]))
+                    cur = w
+            out.append((cur, key[0]))
+        return out
 
     def strassen(self, A: Win, B: Win, C: Win):
         self.calls([_Node([(A, 1.0)], [(B, 1.0)], A.rows, A.cols, B.cols, C, True, 1.0, 0)])
@@ -274,13 +361,15 @@ class _RefBFS:
         return plan
 
 
-def plan_ata_reference_bfs(m, n, lda, ldc, threshold, budget: int = DEFAULT_BUDGET) -> Plan:
-    p = _RefBFS(threshold, budget)
+def plan_ata_reference_bfs(m, n, lda, ldc, threshold, budget: int = DEFAULT_BUDGET,
+                           fused_leaves: bool = False) -> Plan:
+    p = _RefBFS(threshold, budget, fused_leaves)
     p.ata(Win(nat.BASE_A, 0, lda, m, n), Win(nat.BASE_C, 0, ldc, n, n))
     return p.finish()
 
 
-def plan_strassen_reference_bfs(m, n, k, lda, ldb, ldc, threshold, budget: int = DEFAULT_BUDGET) -> Plan:
-    p = _RefBFS(threshold, budget)
+def plan_strassen_reference_bfs(m, n, k, lda, ldb, ldc, threshold, budget: int = DEFAULT_BUDGET,
+                                fused_leaves: bool = False) -> Plan:
+    p = _RefBFS(threshold, budget, fused_leaves)
     p.strassen(Win(nat.BASE_A, 0, lda, m, n), Win(nat.BASE_B, 0, ldb, m, k), Win(nat.BASE_C, 0, ldc, n, k))
     return p.finish()
