@@ -69,11 +69,15 @@ class AutoParams:
     min_chunk: int = 8192          # ... into chunks of at least this many rows
     tf32_tflops: float = 400.0     # single-pass TF32 leaf-product rate (tcgen05, profiles/)
     tf32_fill_waves: int = 8       # 128x256 tcgen05 tiles: more chunks to fill 148 SMs
+    tail_split: bool = True        # FP64: K-split a group's trailing products (partial last wave)
+    min_tail_rows: int = 1024      # ... only when every chunk keeps this many rows
 
 
 TILE = 128        # output tile of the product kernels
 NUM_SMS = 148     # B200
 MAX_BATCH = 48    # products per persistent launch (kMaxBatch, ata_common.cuh)
+MAX_BATCH_NARROW = 104   # FP64 products with <= 2 destinations (kMaxBatchNarrow)
+TAIL_CHUNKS = 4          # K split of a leaf group's trailing products
 
 
 def _ceil2(d: int) -> int:
@@ -179,6 +183,27 @@ class _AutoPlanner:
             return tn * tk
         return sum(min(tk, (ti * bm + bm - 1) // bn + 1) for ti in range(tn))
 
+    def _tail_split(self, prods) -> int:
+        """Index of the first product whose contraction is split for the tail
+        (FP64 groups only: ordered accumulation needs the FP64 kernel's turn
+        counters).  The trailing products covering one wave of tiles are split
+        when the group ends in a partial wave and stays within one launch."""
+        if self.esize != 8 or not self.p.tail_split:
+            return len(prods)
+        tl = [self._tiles(p[0], p[2], p[3]) for p in prods]
+        total = sum(tl)
+        if total <= NUM_SMS or total % NUM_SMS == 0:
+            return len(prods)
+        j, acc = len(prods), 0
+        while j > 0 and acc < NUM_SMS:
+            j -= 1
+            acc += tl[j]
+        if any(prods[q][1] < TAIL_CHUNKS * self.p.min_tail_rows for q in range(j, len(prods))):
+            return len(prods)
+        if j + (len(prods) - j) * TAIL_CHUNKS > MAX_BATCH_NARROW:
+            return len(prods)
+        return j
+
     def _chunks(self, tiles: int, rows: int, nprods: int = 1) -> int:
         """Contraction split S for a group of `tiles` output tiles: at least
         fill_waves waves, then the smallest S (up to 3x that) whose tile count fills >= 97% of
@@ -215,10 +240,27 @@ class _AutoPlanner:
         S = self._chunks(tiles, min(p[1] for p in prods), len(prods))
         group = self.pb.new_group()
         if S <= 1:
-            for (kind, m, n, k, a, b, out, sign, accumulate) in prods:
+            split_from = self._tail_split(prods)
+            for (kind, m, n, k, a, b, out, sign, accumulate) in prods[:split_from]:
                 T = [] if kind == "syrk" else [(b, 1.0)]
                 self.pb.product(kind, m, n, k, [(a, 1.0)], T, [(out, sign)],
                                 accumulate=int(accumulate), group=group)
+            # tail products: K split into TAIL_CHUNKS ordered partial products
+            # (chunk 0 writes, the rest accumulate in turn through the FP64
+            # kernel's per-tile turn counters), issued last so the dynamic tile
+            # queue ends with short tiles instead of a partial wave of full ones
+            for (kind, m, n, k, a, b, out, sign, accumulate) in prods[split_from:]:
+                region = self.pb.new_region()
+                mc = -(-m // TAIL_CHUNKS)
+                for c in range(TAIL_CHUNKS):
+                    r0 = c * mc
+                    rows = min(mc, m - r0)
+                    if rows <= 0:
+                        break
+                    ac = _clip(a, r0, 0, rows, a.cols)
+                    T = [] if kind == "syrk" else [(_clip(b, r0, 0, rows, b.cols), 1.0)]
+                    self.pb.product(kind, rows, n, k, [(ac, 1.0)], T, [(out, sign, region)],
+                                    accumulate=int(accumulate or c > 0), group=group)
             return
         # chunk-major order: the products of one row chunk are adjacent, so a
         # wave of the persistent grid runs whole chunks (periodic_workers)
