@@ -18,7 +18,8 @@ import numpy as np
 from . import _native as nat
 from . import auto_plan, engine, planner, ref_bfs
 from .errors import ShapeMismatchError, UnsupportedSizeError
-from .matrix import (DenseMatrix, DeviceOperand, MultCounter, as_array, mirror_lower_to_upper)
+from .matrix import (DenseMatrix, DeviceOperand, MultCounter, _copy_lower, as_array,
+                     mirror_lower_to_upper)
 from .workspace import (DEFAULT_THRESHOLD, StrassenWorkspace, ata_calls, check_ata_workspace,
                         workspace_for_calls)
 
@@ -65,6 +66,8 @@ def ata(A, C, alpha=1.0, threshold=DEFAULT_THRESHOLD, ws: StrassenWorkspace | No
         threshold = int(threshold)
         if threshold < 1:
             raise ShapeMismatchError("shape mismatch: threshold must be >= 1")
+    if threshold == AUTO and _pipelined_host_ata(a, c, m, n, alpha, ws, counter, auto_params, precision):
+        return
     C_ = DeviceOperand(c, writable=True, lower=True)   # kernels touch only lower(C)
     A_ = DeviceOperand(a, dtype=C_.t.dtype, device=C_.t.device)
     if ws is None:
@@ -82,6 +85,105 @@ def ata(A, C, alpha=1.0, threshold=DEFAULT_THRESHOLD, ws: StrassenWorkspace | No
     C_.commit()
     if counter is not None:
         counter.add(plan.mults)
+
+
+PIPELINE_MIN_BYTES = 1 << 30      # host A at least this large: copy/compute pipeline
+PIPELINE_BLOCK_BYTES = 4 << 30    # ~ bytes of A per row block
+
+
+def _first_c_writer(ops) -> int:
+    """Index of the first op with a destination in C (ops before it only touch A / scratch)."""
+    d = ops["d"]
+    hits = np.nonzero(((d["base"] == nat.BASE_C) & (d["rows"] > 0)).any(axis=1))[0]
+    return int(hits[0]) if len(hits) else len(ops)
+
+
+class _SubPlan:
+    def __init__(self, ops):
+        self.ops = np.ascontiguousarray(ops)
+
+
+def _pipelined_host_ata(a, c, m, n, alpha, ws, counter, auto_params, precision) -> bool:
+    """Host A and C (pinned torch tensors): A^T A = sum over row blocks A_r^T A_r,
+    so A crosses PCIe in R row blocks on a copy stream while the GPU runs the
+    auto plan of the blocks already resident; C's lower block-trapezoids are
+    uploaded behind the first block and awaited only by the first op that
+    writes C.  Returns False (caller takes the plain path) when not applicable."""
+    import torch
+    if not (isinstance(a, torch.Tensor) and isinstance(c, torch.Tensor)) or a.is_cuda or c.is_cuda:
+        return False
+    if a.dtype != c.dtype or a.dtype not in (torch.float32, torch.float64):
+        return False
+    if not (a.is_contiguous() and c.is_contiguous() and a.is_pinned() and c.is_pinned()):
+        return False
+    es = a.element_size()
+    if m * n * es < PIPELINE_MIN_BYTES or m < 2:
+        return False
+    R = max(2, min(8, -(-m * n * es // PIPELINE_BLOCK_BYTES)))
+    rb = -(-m // R)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    main = torch.cuda.current_stream(dev)
+    copy = _copy_stream(dev)
+    dA = torch.empty((m, n), dtype=a.dtype, device=dev)
+    dC = torch.empty((n, n), dtype=c.dtype, device=dev)
+    code = nat.dtype_code(c.dtype, precision)
+    round_tf32 = precision == "tf32" and c.dtype == torch.float32
+    params = auto_params or auto_plan.AutoParams()
+    blocks = []
+    for r0 in range(0, m, rb):
+        rows = min(rb, m - r0)
+        key = ("ata-auto", rows, n, n, n, params, round_tf32)
+        blocks.append((r0, rows, engine.cached_plan(
+            key, lambda rows=rows: auto_plan.plan_ata_auto(rows, n, n, n, params, round_tf32=round_tf32))))
+    need = max(p.ws_scalars for (_, _, p) in blocks)
+    if ws is None:
+        ws = workspace_for_ata(m, n, AUTO, dtype=c.dtype)
+    wbuf = ws.ensure(dev, extra=need) if need > 0 else None
+    wptr = int(wbuf.data_ptr()) if wbuf is not None else 0
+    wel = int(wbuf.numel()) if wbuf is not None else 0
+    copy.wait_stream(main)                 # dA / dC / scratch are free to overwrite
+    events = []
+    c_ready = torch.cuda.Event()
+    with torch.cuda.stream(copy):
+        for i, (r0, rows, _) in enumerate(blocks):
+            dA[r0:r0 + rows].copy_(a[r0:r0 + rows], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(copy)
+            events.append(ev)
+            if i == 0:
+                _copy_lower(dC, c, to_device=True)
+                c_ready.record(copy)
+    mults = 0
+    for i, (r0, rows, plan) in enumerate(blocks):
+        main.wait_event(events[i])
+        ops = plan.ops
+        cut = _first_c_writer(ops) if i == 0 else 0
+        A_ptr = int(dA.data_ptr()) + r0 * n * es
+        parts = [ops[:cut], ops[cut:]] if i == 0 else [ops]
+        for j, part in enumerate(parts):
+            if i == 0 and j == 1:
+                main.wait_event(c_ready)
+            if len(part):
+                engine.run_plan(_SubPlan(part), code, A_ptr, rows * n, int(dC.data_ptr()), dC.numel(), alpha,
+                                ws=wptr, ws_elems=wel)
+        mults += plan.mults
+    if len(blocks) and _first_c_writer(blocks[0][2].ops) == len(blocks[0][2].ops):
+        main.wait_event(c_ready)          # no op wrote C: still order the download after the upload
+    _copy_lower(c, dC, to_device=False)
+    if counter is not None:
+        counter.add(mults)
+    return True
+
+
+_COPY_STREAMS = {}
+
+
+def _copy_stream(dev):
+    import torch
+    s = _COPY_STREAMS.get(dev.index)
+    if s is None:
+        s = _COPY_STREAMS[dev.index] = torch.cuda.Stream(dev)
+    return s
 
 
 def ata_full(A, threshold=DEFAULT_THRESHOLD, counter: MultCounter | None = None) -> DenseMatrix:

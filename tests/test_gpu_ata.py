@@ -134,3 +134,34 @@ def test_config_c2_full_parity():
     c = np.zeros((4097, 4097))
     P.ata(a, c, 1.0, threshold=256 * 256)
     assert O.rel_frobenius_lower(c, O.gram_blas(a)) <= 1e-10
+
+
+@pytest.mark.parametrize("dtype,precision", [("f64", "fp32"), ("f32", "tf32")])
+def test_pipelined_host_ata(monkeypatch, dtype, precision):
+    """Pinned host A and C: A crosses PCIe in row blocks on a copy stream while
+    the GPU runs the blocks already resident (ata._pipelined_host_ata).  Same
+    result as the device path within the dtype tolerance, upper triangle of C
+    untouched, C accumulated into (not overwritten)."""
+    import torch
+    import paper_2110_13042_b200 as P
+    import importlib
+    ata_mod = importlib.import_module("paper_2110_13042_b200.ata")
+    monkeypatch.setattr(ata_mod, "PIPELINE_MIN_BYTES", 1 << 20)
+    monkeypatch.setattr(ata_mod, "PIPELINE_BLOCK_BYTES", 3 << 20)
+    tdt = torch.float64 if dtype == "f64" else torch.float32
+    rng = np.random.default_rng(21)
+    a = rng.standard_normal((20011, 300))
+    hA = torch.from_numpy(a).to(tdt).pin_memory()
+    c0 = rng.standard_normal((300, 300))
+    hC = torch.from_numpy(c0).to(tdt).pin_memory()
+    called = []
+    orig = ata_mod._pipelined_host_ata
+    monkeypatch.setattr(ata_mod, "_pipelined_host_ata", lambda *x: called.append(1) or orig(*x))
+    P.ata(hA, hC, 0.5, threshold="auto", precision=precision)
+    assert called
+    got = hC.numpy().astype(np.float64)
+    ref = c0 + 0.5 * O.gram_blas(hA.numpy().astype(np.float64))
+    tol = 1e-12 if dtype == "f64" else 1e-4
+    assert O.rel_frobenius_lower(got, ref) <= tol
+    iu = np.triu_indices(300, 1)
+    assert np.array_equal(hC.numpy()[iu], torch.from_numpy(c0).to(tdt).numpy()[iu])
