@@ -162,13 +162,18 @@ class _AutoPlanner:
         posts.append((kids, out, sign, n1, k1, accumulate))
 
     def emit(self, leaves, posts, extra=()):
-        prods = list(extra)
+        prods = []
         for (m, n, k, a, b, out, sign, accumulate) in leaves:
             if a.rows == 0 or a.cols == 0 or b.rows == 0 or b.cols == 0:
                 if not accumulate:            # an all-zero operand: the product buffer is zero
                     self.pb.fill(out)
                 continue
             prods.append(("gemm", m, n, k, a, b, out, sign, accumulate))
+        # products writing C go last in the group: everything before the first
+        # C writer only needs A and scratch (ata._pipelined_host_ata uploads C
+        # behind the first block of A and waits for it at the first C writer)
+        prods = [p for p in prods if p[6].base != nat.BASE_C] + list(extra) + \
+            [p for p in prods if p[6].base == nat.BASE_C]
         self.emit_products(prods)
         for (kids, out, sign, n1, k1, accumulate) in posts:
             self._post(kids, out, sign, n1, k1, accumulate)
