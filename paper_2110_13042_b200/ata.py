@@ -98,6 +98,76 @@ def _first_c_writer(ops) -> int:
     return int(hits[0]) if len(hits) else len(ops)
 
 
+_TILES = 64   # C download tiles per side (the same row bands as matrix._copy_lower)
+
+
+def _download_schedule(plan, n, remaining: bool = False, parts: int = 6):
+    """C tiles (block row, block col) of the lower triangle grouped by the op
+    after which their last writer in `plan` has run: [(cut, tiles)] with cut <
+    len(plan.ops), a few groups of similar size.  remaining=True: the tiles
+    written by the plan's last group of ops (or never written)."""
+    cache = plan.__dict__.setdefault("_dl", {})
+    if n not in cache:
+        step = max(1, -(-n // _TILES))
+        nb = -(-n // step)
+        last = np.full((nb, nb), -1, dtype=np.int64)
+        d = plan.ops["d"]
+        ii, jj = np.nonzero((d["base"] == nat.BASE_C) & (d["rows"] > 0) & (d["cols"] > 0))
+        for i, j in zip(ii.tolist(), jj.tolist()):
+            w = d[i, j]
+            r0, c0 = divmod(int(w["off"]), int(w["ld"]))
+            r1, c1 = r0 + int(w["rows"]), c0 + int(w["cols"])
+            last[r0 // step:(r1 - 1) // step + 1, c0 // step:(c1 - 1) // step + 1] = i
+        low = [(bi, bj) for bi in range(nb) for bj in range(bi + 1)]
+        order = sorted((int(last[t]), t) for t in low if last[t] >= 0)
+        groups, cur, target = [], [], len(order) / parts
+        for k, (li, t) in enumerate(order):
+            cur.append(t)
+            if (k + 1 == len(order) or order[k + 1][0] != li) and len(cur) >= target:
+                groups.append((li + 1, cur))
+                cur = []
+        if cur:
+            groups.append((order[-1][0] + 1, cur))
+        n_ops = len(plan.ops)
+        early = [(cut, ts) for (cut, ts) in groups if cut < n_ops]
+        rest = [t for (cut, ts) in groups if cut >= n_ops for t in ts] + [t for t in low if last[t] < 0]
+        cache[n] = (early, rest, step)
+    early, rest, step = cache[n]
+    if remaining:
+        return [(bi, bj, step) for (bi, bj) in rest]
+    return [(cut, [(bi, bj, step) for (bi, bj) in tiles]) for (cut, tiles) in early]
+
+
+def _copy_tiles(host, dev, tiles):
+    """D2H of C tiles (block row, block col, step) on the current stream; runs
+    of adjacent tiles in one block row are one 2D copy.  Diagonal tiles are
+    whole squares: their upper part holds the values uploaded by _copy_lower."""
+    from .matrix import _cudart, _stream_ptr
+    lib = _cudart()
+    stream = _stream_ptr()
+    n = int(dev.shape[0])
+    es = dev.element_size()
+    rows = {}
+    for (bi, bj, step) in tiles:
+        rows.setdefault((bi, step), []).append(bj)
+    for (bi, step), cols in rows.items():
+        cols.sort()
+        r0, r1 = bi * step, min(n, (bi + 1) * step)
+        k = 0
+        while k < len(cols):
+            j0 = cols[k]
+            while k + 1 < len(cols) and cols[k + 1] == cols[k] + 1:
+                k += 1
+            c0, c1 = j0 * step, min(n, (cols[k] + 1) * step)
+            k += 1
+            d = host.data_ptr() + (r0 * host.stride(0) + c0) * es
+            s = dev.data_ptr() + (r0 * dev.stride(0) + c0) * es
+            rc = lib.cudaMemcpy2DAsync(d, host.stride(0) * es, s, dev.stride(0) * es, (c1 - c0) * es, r1 - r0,
+                                       2, stream)
+            if rc != 0:
+                raise RuntimeError(f"cudaMemcpy2DAsync failed ({rc})")
+
+
 class _SubPlan:
     def __init__(self, ops):
         self.ops = np.ascontiguousarray(ops)
@@ -154,22 +224,40 @@ def _pipelined_host_ata(a, c, m, n, alpha, ws, counter, auto_params, precision) 
                 _copy_lower(dC, c, to_device=True)
                 c_ready.record(copy)
     mults = 0
+    last = len(blocks) - 1
     for i, (r0, rows, plan) in enumerate(blocks):
         main.wait_event(events[i])
         ops = plan.ops
-        cut = _first_c_writer(ops) if i == 0 else 0
         A_ptr = int(dA.data_ptr()) + r0 * n * es
-        parts = [ops[:cut], ops[cut:]] if i == 0 else [ops]
-        for j, part in enumerate(parts):
-            if i == 0 and j == 1:
+        # segment boundaries: the first C writer of block 0 waits for C's upload;
+        # in the last block, C tiles whose last writer has run go home early
+        cuts, downloads = [], {}
+        if i == 0:
+            cuts.append(_first_c_writer(ops))
+        if i == last:
+            sched = _download_schedule(plan, n)
+            for cut, tiles in sched:
+                cuts.append(cut)
+                downloads[cut] = tiles
+        prev = 0
+        for cut in sorted(set(cuts)) + [len(ops)]:
+            if cut > prev:
+                engine.run_plan(_SubPlan(ops[prev:cut]), code, A_ptr, rows * n, int(dC.data_ptr()), dC.numel(),
+                                alpha, ws=wptr, ws_elems=wel)
+                prev = cut
+            if i == 0 and cut == cuts[0]:
                 main.wait_event(c_ready)
-            if len(part):
-                engine.run_plan(_SubPlan(part), code, A_ptr, rows * n, int(dC.data_ptr()), dC.numel(), alpha,
-                                ws=wptr, ws_elems=wel)
+            if cut in downloads:
+                ev = torch.cuda.Event()
+                ev.record(main)
+                copy.wait_event(ev)
+                with torch.cuda.stream(copy):
+                    _copy_tiles(c, dC, downloads[cut])
         mults += plan.mults
-    if len(blocks) and _first_c_writer(blocks[0][2].ops) == len(blocks[0][2].ops):
-        main.wait_event(c_ready)          # no op wrote C: still order the download after the upload
-    _copy_lower(c, dC, to_device=False)
+    main.wait_event(c_ready)               # (a plan with no C writer: download after the upload)
+    _copy_tiles(c, dC, _download_schedule(blocks[last][2], n, remaining=True))
+    main.wait_stream(copy)                 # the early downloads
+    main.synchronize()
     if counter is not None:
         counter.add(mults)
     return True
