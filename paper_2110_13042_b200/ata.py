@@ -71,7 +71,7 @@ def ata(A, C, alpha=1.0, threshold=DEFAULT_THRESHOLD, ws: StrassenWorkspace | No
     C_ = DeviceOperand(c, writable=True, lower=True)   # kernels touch only lower(C)
     A_ = DeviceOperand(a, dtype=C_.t.dtype, device=C_.t.device)
     if ws is None:
-        ws = workspace_for_ata(m, n, threshold, dtype=C_.t.dtype)
+        ws = _default_workspace(m, n, threshold, C_.t.dtype)
     elif threshold != AUTO:
         check_ata_workspace(ws, m, n, threshold)
     import torch
@@ -79,12 +79,34 @@ def ata(A, C, alpha=1.0, threshold=DEFAULT_THRESHOLD, ws: StrassenWorkspace | No
                      round_tf32=(precision == "tf32" and C_.t.dtype == torch.float32))
     extra = plan.ws_scalars if (threshold == AUTO or not engine.reference_dfs()) else 0
     wbuf = ws.ensure(C_.t.device, extra=extra) if plan.ws_scalars > 0 else None
-    engine.run_plan(plan, nat.dtype_code(C_.t.dtype, precision), A_.ptr, A_.elems, C_.ptr, C_.elems, alpha,
-                    ws=int(wbuf.data_ptr()) if wbuf is not None else 0,
-                    ws_elems=int(wbuf.numel()) if wbuf is not None else 0)
+    args = (plan, nat.dtype_code(C_.t.dtype, precision), A_.ptr, A_.elems, C_.ptr, C_.elems, alpha)
+    kw = dict(ws=int(wbuf.data_ptr()) if wbuf is not None else 0,
+              ws_elems=int(wbuf.numel()) if wbuf is not None else 0)
+    if threshold != AUTO and not engine.reference_dfs():
+        # launch-bound breadth-first reference plans: replay a CUDA graph on repeat calls
+        engine.run_plan_graphed(("ata-ref-bfs", m, n, A_.ld, C_.ld, threshold), *args, **kw)
+    else:
+        engine.run_plan(*args, **kw)
     C_.commit()
     if counter is not None:
         counter.add(plan.mults)
+
+
+_WS_CACHE: dict = {}
+
+
+def _default_workspace(m, n, threshold, dtype):
+    """ws=None: one arena per (shape, threshold, dtype), kept for the next call
+    (the two most recent) -- repeated calls allocate nothing and keep their
+    pointers, which lets launch-bound plans replay a captured graph."""
+    key = (m, n, threshold, str(dtype))
+    ws = _WS_CACHE.pop(key, None)
+    if ws is None:
+        ws = workspace_for_ata(m, n, threshold, dtype=dtype)
+    _WS_CACHE[key] = ws
+    while len(_WS_CACHE) > 2:
+        _WS_CACHE.pop(next(iter(_WS_CACHE)))
+    return ws
 
 
 PIPELINE_MIN_BYTES = 1 << 30      # host A at least this large: copy/compute pipeline

@@ -109,3 +109,39 @@ class PlanGraph:
 
     def replay(self):
         self.graph.replay()
+
+
+_GRAPHS: "OrderedDict" = OrderedDict()
+_GRAPH_SEEN: dict = {}
+_GRAPHS_MAX = 8
+
+
+def run_plan_graphed(key, plan, dtype_code, A, a_elems, C, c_elems, alpha, ws=None, ws_elems=0,
+                     B=None, b_elems=0):
+    """run_plan for launch-bound plans (breadth-first reference recursions:
+    ~1000 small launches): the second call with identical plan, pointers and
+    alpha captures a CUDA graph, later calls replay it on the current stream.
+    `key` identifies the plan (its cache key)."""
+    import torch
+    dev = torch.cuda.current_device()
+    gkey = (key, dtype_code, dev, int(torch.cuda.current_stream().cuda_stream), A, a_elems, C, c_elems,
+            float(alpha), ws or 0, ws_elems, B or 0, b_elems)
+    g = _GRAPHS.get(gkey)
+    if g is None:
+        seen = _GRAPH_SEEN.get(gkey, 0) + 1
+        _GRAPH_SEEN[gkey] = seen
+        if len(_GRAPH_SEEN) > 64:
+            _GRAPH_SEEN.clear()
+        if seen < 2:
+            run_plan(plan, dtype_code, A, a_elems, C, c_elems, alpha, ws=ws, ws_elems=ws_elems,
+                     B=B, b_elems=b_elems)
+            return
+        g = PlanGraph(plan, dtype_code, A, a_elems, C, c_elems, alpha, ws=ws, ws_elems=ws_elems,
+                      B=B, b_elems=b_elems)
+        _GRAPHS[gkey] = g
+        if len(_GRAPHS) > _GRAPHS_MAX:
+            _GRAPHS.popitem(last=False)
+    else:
+        _GRAPHS.move_to_end(gkey)
+    g.replay()
+

@@ -165,3 +165,27 @@ def test_pipelined_host_ata(monkeypatch, dtype, precision):
     assert O.rel_frobenius_lower(got, ref) <= tol
     iu = np.triu_indices(300, 1)
     assert np.array_equal(hC.numpy()[iu], torch.from_numpy(c0).to(tdt).numpy()[iu])
+
+
+def test_reference_plan_graph_replay():
+    """Integer thresholds: the second identical call captures a CUDA graph and
+    later calls replay it -- every call gives the bitwise-same result and the
+    exact reference multiplication count."""
+    import torch
+    import paper_2110_13042_b200 as P
+    from paper_2110_13042_b200 import engine
+    a = torch.from_numpy(np.random.default_rng(3).standard_normal((700, 300))).cuda()
+    C = torch.zeros(300, 300, dtype=torch.float64, device="cuda")
+    outs, counts = [], []
+    before = len(engine._GRAPHS)
+    for _ in range(4):
+        C.zero_()
+        cnt = P.MultCounter()
+        P.ata(a, C, 1.0, threshold=64 * 64, counter=cnt)
+        outs.append(C.cpu().numpy().copy())
+        counts.append(cnt.scalar_mults)
+    assert len(engine._GRAPHS) == before + 1
+    assert all(np.array_equal(o, outs[0]) for o in outs[1:])
+    assert len(set(counts)) == 1
+    ref = O.gram_blas(a.cpu().numpy())
+    assert O.rel_frobenius_lower(outs[-1], ref) <= 1e-12
