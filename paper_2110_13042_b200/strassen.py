@@ -57,10 +57,13 @@ def fast_strassen(A, B, C, alpha=1.0, ws: StrassenWorkspace | None = None,
             m, n, k, A_.ld, B_.ld, C_.ld, threshold))
         extra = plan.ws_scalars
     wbuf = ws.ensure(C_.t.device, extra=extra) if plan.ws_scalars > 0 else None
-    engine.run_plan(plan, nat.dtype_code(C_.t.dtype), A_.ptr, A_.elems, C_.ptr, C_.elems, alpha,
-                    ws=int(wbuf.data_ptr()) if wbuf is not None else 0,
-                    ws_elems=int(wbuf.numel()) if wbuf is not None else 0,
-                    B=B_.ptr, b_elems=B_.elems)
+    args = (plan, nat.dtype_code(C_.t.dtype), A_.ptr, A_.elems, C_.ptr, C_.elems, alpha)
+    kw = dict(ws=int(wbuf.data_ptr()) if wbuf is not None else 0,
+              ws_elems=int(wbuf.numel()) if wbuf is not None else 0, B=B_.ptr, b_elems=B_.elems)
+    if engine.reference_dfs():
+        engine.run_plan(*args, **kw)
+    else:   # launch-bound breadth-first plan: graph replay on repeat calls
+        engine.run_plan_graphed(key, *args, **kw)
     C_.commit()
     if counter is not None:
         counter.add(plan.mults)
