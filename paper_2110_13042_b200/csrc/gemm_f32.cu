@@ -157,13 +157,18 @@ __global__ void __launch_bounds__(f32cfg::THREADS, 1)
     }
   };
 
-  float acc[4][4][4];
+  // The tensor core's fp32 accumulation drops low-order bits (a negative bias
+  // ~ additions x 2^-25 on sums of positive terms: -2.3e-4 on a 2^20-row Gram
+  // diagonal, tools/acc_bias.py).  `acc` therefore only spans FLUSH k-tiles and
+  // is added into `tot` on the CUDA cores (fp32, round to nearest).
+  constexpr int FLUSH = SPLIT ? 1 : 8;
+  float acc[4][4][4], tot[4][4][4];
 #pragma unroll
   for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b)
 #pragma unroll
-      for (int e = 0; e < 4; ++e) acc[a][b][e] = 0.f;
+      for (int e = 0; e < 4; ++e) acc[a][b][e] = tot[a][b][e] = 0.f;
 
   const int KT = (P.m + BK - 1) / BK;
 #pragma unroll
@@ -225,6 +230,17 @@ __global__ void __launch_bounds__(f32cfg::THREADS, 1)
           mma_tf32(acc[mt][nt2], a[mt], b[nt2]);
         }
     }
+    if ((kt + 1) % FLUSH == 0 || kt == KT - 1) {
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b)
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            tot[a][b][e] += acc[a][b][e];
+            acc[a][b][e] = 0.f;
+          }
+    }
   }
   cp_async_wait<0>();
 
@@ -247,7 +263,7 @@ __global__ void __launch_bounds__(f32cfg::THREADS, 1)
           for (int e = 0; e < 2; ++e) {
             const int cc = col + e;
             if (cc < D.cols && (!syrk || cc <= row)) {
-              const float v = scale * acc[mt][nt2][h * 2 + e];
+              const float v = scale * tot[mt][nt2][h * 2 + e];
               drow[cc] = accumulate ? drow[cc] + v : v;
             }
           }
@@ -307,7 +323,7 @@ cudaError_t launch_batch_f32(const BatchArgs<float>& a, cudaStream_t s, bool spl
   static int use_tc = -1;
   if (use_tc < 0) {
     const char* e = std::getenv("ATA_TF32_TC");
-    use_tc = e ? std::atoi(e) : 1;
+    use_tc = e ? std::atoi(e) : 2;   // CTA pair by default (measured faster on c5 with KSUB flushes)
   }
   if (!use_tc) return launch_batch_f32_t<false>(a, s);
   DProd<float> tcp[kMaxBatch];

@@ -24,6 +24,7 @@ namespace ata {
 
 namespace tc2 {
 constexpr int BM = 256, BN = 256, BK = 32, STAGES = 6;   // per pair
+constexpr int KSUB = 256;  // k-blocks per TMEM accumulator (see gemm_tf32_tc.cu: fp32 accumulation bias)
 constexpr int HALF = 128;                                 // rows of A / cols of B per CTA
 constexpr int A_BYTES = BK * HALF * 4;                    // 16 KB
 constexpr int B_BYTES = BK * HALF * 4;                    // 16 KB
@@ -209,15 +210,17 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
     // ================= MMA issuer (leader CTA only) =================
     if (leader) {
       int ks = 0, it = 0;
-      for (int tile = cluster; tile < args.total_tiles; tile += nclusters, ++it) {
+      for (int tile = cluster; tile < args.total_tiles; tile += nclusters) {
         const Tc2Tile t = t2_decode(args, tile);
         const Tc2Prod& P = args.p[t.pi];
         const int KT = (P.m + BK - 1) / BK;
+       for (int k0 = 0; k0 < KT; k0 += KSUB, ++it) {
+        const int k1 = min(KT, k0 + KSUB);
         const int buf = it & 1;
         t2_wait(&tempty[buf], ((it >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;");
         const uint32_t dt = tmem + buf * BN;
-        for (int kb = 0; kb < KT; ++kb, ++ks) {
+        for (int kb = k0; kb < k1; ++kb, ++ks) {
           const int s = ks % STAGES;
           t2_wait(&full[s], (ks / STAGES) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;");
@@ -230,13 +233,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
                   "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
                   "tcgen05.mma.cta_group::2.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(dt),
                   "l"(t2_desc(sa + kk * 1024)), "l"(t2_desc(sb + kk * 1024)), "r"(IDESC),
-                  "r"((uint32_t)((kb | kk) != 0)));
+                  "r"((uint32_t)((kb != k0) || (kk != 0))));
             asm volatile(
                 "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], "
                 "%1;" ::"r"(t2_smem(&empty[s])),
                 "h"((uint16_t)3)
                 : "memory");
-            if (kb == KT - 1)
+            if (kb == k1 - 1)
               asm volatile(
                   "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], "
                   "%1;" ::"r"(t2_smem(&tfull[buf])),
@@ -245,6 +248,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
           }
           __syncwarp();
         }
+       }
       }
     }
   } else {
@@ -253,9 +257,12 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
     const uint32_t leader_tempty0 = t2_map(t2_smem(&tempty[0]), 0);
     const uint32_t leader_tempty1 = t2_map(t2_smem(&tempty[1]), 0);
     int it = 0;
-    for (int tile = cluster; tile < args.total_tiles; tile += nclusters, ++it) {
+    for (int tile = cluster; tile < args.total_tiles; tile += nclusters) {
       const Tc2Tile t = t2_decode(args, tile);
       const Tc2Prod& P = args.p[t.pi];
+      const int KT = (P.m + BK - 1) / BK;
+     for (int k0 = 0; k0 < KT; k0 += KSUB, ++it) {
+      const bool accumulate = P.accumulate || k0 > 0;
       const int buf = it & 1;
       t2_wait(&tfull[buf], (it >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;");
@@ -288,7 +295,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
               for (int e = 0; e < 32; e += 4) {
                 float4 o = make_float4(P.scale * __uint_as_float(v[e]), P.scale * __uint_as_float(v[e + 1]),
                                        P.scale * __uint_as_float(v[e + 2]), P.scale * __uint_as_float(v[e + 3]));
-                if (P.accumulate) {
+                if (accumulate) {
                   const float4 old = *reinterpret_cast<const float4*>(dp + e);
                   o.x += old.x;
                   o.y += old.y;
@@ -302,7 +309,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
               for (int e = 0; e < 32; ++e) {
                 if (e < cmax) {
                   const float o = P.scale * __uint_as_float(v[e]);
-                  dp[e] = P.accumulate ? dp[e] + o : o;
+                  dp[e] = accumulate ? dp[e] + o : o;
                 }
               }
             }
@@ -314,6 +321,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
       if (lane == 0)
         asm volatile("mbarrier.arrive.shared::cluster.b64 _, [%0];" ::"r"(buf ? leader_tempty1 : leader_tempty0)
                      : "memory");
+     }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;");

@@ -38,6 +38,12 @@ constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
 constexpr int THREADS = 192;
 constexpr int TMEM_COLS = 512;
 constexpr int kMax = 48;   // = kMaxBatch: one launch per plan group (15 KB of kernel parameters)
+// k-blocks accumulated in TMEM before the epilogue adds the partial into the
+// destination in fp32 on the CUDA cores (round to nearest).  The tensor core's
+// fp32 accumulation drops low-order bits (measured: a -4.2e-4 relative bias on
+// the Gram diagonal after 2^16 rows, ~ K/8 additions x 2^-24), so one TMEM
+// accumulator covers at most KSUB*BK = 8192 rows (~5e-5).
+constexpr int KSUB = 256;
 // instruction descriptor: D f32, A/B tf32, both MN-major, N = 256, M = 128
 constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (1u << 16) |
                            (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
@@ -226,42 +232,48 @@ __global__ void __launch_bounds__(tc::THREADS, 1) prod_tf32_tc_kernel(const __gr
   } else if (warp == 1) {
     // ================= MMA issuer =================
     int ks = 0, it = 0;
-    for (int tile = blockIdx.x; tile < args.total_tiles; tile += gridDim.x, ++it) {
+    for (int tile = blockIdx.x; tile < args.total_tiles; tile += gridDim.x) {
       const TcTile t = tc_decode(args, tile);
       const TcProd& P = args.p[t.pi];
       const int KT = (P.m + BK - 1) / BK;
-      const int buf = it & 1;
-      tc_mbar_wait(&tempty[buf], ((it >> 1) & 1) ^ 1);
-      asm volatile("tcgen05.fence::after_thread_sync;\n");
-      const uint32_t dt = tmem + buf * BN;
-      for (int kb = 0; kb < KT; ++kb, ++ks) {
-        const int s = ks % STAGES;
-        tc_mbar_wait(&full[s], (ks / STAGES) & 1);
+      for (int k0 = 0; k0 < KT; k0 += KSUB, ++it) {  // one TMEM accumulator per KSUB k-blocks
+        const int k1 = min(KT, k0 + KSUB);
+        const int buf = it & 1;
+        tc_mbar_wait(&tempty[buf], ((it >> 1) & 1) ^ 1);
         asm volatile("tcgen05.fence::after_thread_sync;\n");
-        if (args.dbg != nullptr && ks == 0 && blockIdx.x == 0) {
-          const float* src = reinterpret_cast<const float*>(smem);
-          for (int e = lane; e < STAGE_BYTES / 4; e += 32) args.dbg[e] = src[e];
+        const uint32_t dt = tmem + buf * BN;
+        for (int kb = k0; kb < k1; ++kb, ++ks) {
+          const int s = ks % STAGES;
+          tc_mbar_wait(&full[s], (ks / STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;\n");
+          if (args.dbg != nullptr && ks == 0 && blockIdx.x == 0) {
+            const float* src = reinterpret_cast<const float*>(smem);
+            for (int e = lane; e < STAGE_BYTES / 4; e += 32) args.dbg[e] = src[e];
+            __syncwarp();
+          }
+          if (lane == 0) {
+            const uint32_t sa = tc_smem(smem + s * STAGE_BYTES);
+            const uint32_t sb = sa + A_BYTES;
+#pragma unroll
+            for (int kk = 0; kk < BK / 8; ++kk)
+              tc_mma(dt, tc_desc(sa + kk * 1024), tc_desc(sb + kk * 1024), (kb != k0) || (kk != 0));
+            tc_commit(&empty[s]);
+            if (kb == k1 - 1) tc_commit(&tfull[buf]);
+          }
           __syncwarp();
         }
-        if (lane == 0) {
-          const uint32_t sa = tc_smem(smem + s * STAGE_BYTES);
-          const uint32_t sb = sa + A_BYTES;
-#pragma unroll
-          for (int kk = 0; kk < BK / 8; ++kk)
-            tc_mma(dt, tc_desc(sa + kk * 1024), tc_desc(sb + kk * 1024), (kb | kk) != 0);
-          tc_commit(&empty[s]);
-          if (kb == KT - 1) tc_commit(&tfull[buf]);
-        }
-        __syncwarp();
       }
     }
   } else {
     // ================= epilogue (warps 2..5) =================
     const int q = warp & 3;  // TMEM lane quadrant this warp may access
     int it = 0;
-    for (int tile = blockIdx.x; tile < args.total_tiles; tile += gridDim.x, ++it) {
+    for (int tile = blockIdx.x; tile < args.total_tiles; tile += gridDim.x) {
       const TcTile t = tc_decode(args, tile);
       const TcProd& P = args.p[t.pi];
+      const int KT = (P.m + BK - 1) / BK;
+     for (int k0 = 0; k0 < KT; k0 += KSUB, ++it) {
+      const bool accumulate = P.accumulate || k0 > 0;   // later partials add (fp32, round to nearest)
       const int buf = it & 1;
       tc_mbar_wait(&tfull[buf], (it >> 1) & 1);
       asm volatile("tcgen05.fence::after_thread_sync;\n");
@@ -282,7 +294,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) prod_tf32_tc_kernel(const __gr
               "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
             : "r"(addr));
         asm volatile("tcgen05.wait::ld.sync.aligned;\n" ::: "memory");
-        if (args.dbg != nullptr && blockIdx.x == 0 && it == 0 && c == 0) {
+        if (args.dbg != nullptr && blockIdx.x == 0 && it == 0 && c == 0) {  // (first partial)
           // raw TMEM values of the first accumulator chunk: row-major [128][32]
           for (int e = 0; e < 32; ++e) args.dbg[STAGE_BYTES / 4 + (q * 32 + lane) * 32 + e] = __uint_as_float(v[e]);
         }
@@ -299,7 +311,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) prod_tf32_tc_kernel(const __gr
               for (int e = 0; e < 32; e += 4) {
                 float4 o = make_float4(P.scale * __uint_as_float(v[e]), P.scale * __uint_as_float(v[e + 1]),
                                        P.scale * __uint_as_float(v[e + 2]), P.scale * __uint_as_float(v[e + 3]));
-                if (P.accumulate) {
+                if (accumulate) {
                   const float4 old = *reinterpret_cast<const float4*>(dp + e);
                   o.x += old.x;
                   o.y += old.y;
@@ -311,7 +323,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) prod_tf32_tc_kernel(const __gr
             } else {
               for (int e = 0; e < cmax; ++e) {
                 const float o = P.scale * __uint_as_float(v[e]);
-                dp[e] = P.accumulate ? dp[e] + o : o;
+                dp[e] = accumulate ? dp[e] + o : o;
               }
             }
           }
@@ -320,6 +332,7 @@ __global__ void __launch_bounds__(tc::THREADS, 1) prod_tf32_tc_kernel(const __gr
       asm volatile("tcgen05.fence::before_thread_sync;\n");
       __syncwarp();
       if (lane == 0) tc_mbar_arrive(&tempty[buf]);
+     }
     }
   }
   asm volatile("tcgen05.fence::before_thread_sync;\n");
