@@ -7,6 +7,7 @@
 // grouped launch, and issues everything on one stream.  It never allocates and
 // never synchronises, so a whole plan can be captured in a CUDA graph.
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <algorithm>
@@ -204,6 +205,11 @@ int walk_batches(const ata_op* ops, int n_ops, bool ordering, bool narrow, F1 on
   int first = -1, group = -1, count = 0;
   bool all_narrow = true;  // every product of the open batch has <= kNarrowDests destinations
   std::vector<int> regions;
+  auto has_region = [](const ata_op& op) {
+    for (int j = 0; j < op.nd; ++j)
+      if (op.d[j].region > 0) return true;
+    return false;
+  };
   auto flush = [&](int end, bool cont = false) -> int {
     int rc = ATA_OK;
     if (count > 0) rc = on_batch(first, end, cont);
@@ -217,7 +223,10 @@ int walk_batches(const ata_op* ops, int n_ops, bool ordering, bool narrow, F1 on
     int rc;
     if (op.type == ATA_OP_GEMM || op.type == ATA_OP_SYRK) {
       const bool same = count > 0 && op.group >= 0 && op.group == group;
-      const int cap = (narrow && all_narrow && op.nd <= ata::kNarrowDests) ? ata::kMaxBatchNarrow : ata::kMaxBatch;
+      // region-free narrow FP64 batches are unbounded (device-resident descriptors)
+      const bool nar = narrow && all_narrow && op.nd <= ata::kNarrowDests;
+      const int cap = (nar && regions.empty() && !has_region(op)) ? ata::kMaxBatchGlobal
+                      : nar ? ata::kMaxBatchNarrow : ata::kMaxBatch;
       bool join = same && count < cap;
       bool conflict = false;
       if (join && !ordering) {
@@ -389,10 +398,39 @@ int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, int* sync, int64_t 
     if (!nb && last - first > ata::kMaxBatch) return fail(ATA_E_ARG, "internal: oversized product batch");
     if (nb) {
       if constexpr (std::is_same<T, double>::value) {
-        std::memset(&nbatch, 0, sizeof(nbatch));
-        fill_batch(nbatch, first, last);
-        cudaError_t e = ata::launch_batch_f64_narrow(nbatch, s);
-        if (e != cudaSuccess) return cuda_fail(e, "product launch");
+        static const bool no_global = std::getenv("ATA_NO_GLOBAL_BATCH") != nullptr;  // A/B knob
+        if (last - first > ata::kMaxBatchNarrow && !no_global) {
+          // unbounded region-free batch: device-resident descriptors, one launch
+          struct {
+            int count;
+            double alpha;
+            int* sync;
+            int n_sync;
+            ata::DProdT<double, ata::kNarrowDests>* p;
+          } vb;
+          std::vector<ata::DProdT<double, ata::kNarrowDests>> prods(last - first);
+          std::memset(prods.data(), 0, sizeof(prods[0]) * prods.size());
+          vb.count = 0;
+          vb.p = prods.data();
+          fill_batch(vb, first, last);
+          cudaError_t e = ata::launch_batch_f64_global(prods.data(), vb.count, alpha, sync, s);
+          if (e == cudaSuccess) return ATA_OK;
+          if (e != cudaErrorNotReady) return cuda_fail(e, "product launch");
+          // capturing a graph with descriptors not yet resident: narrow batches instead
+          for (int c0 = first; c0 < last; c0 += ata::kMaxBatchNarrow) {
+            std::memset(&nbatch, 0, sizeof(nbatch));
+            fill_batch(nbatch, c0, std::min(last, c0 + ata::kMaxBatchNarrow));
+            e = ata::launch_batch_f64_narrow(nbatch, s);
+            if (e != cudaSuccess) return cuda_fail(e, "product launch");
+          }
+          return ATA_OK;
+        }
+        for (int c0 = first; c0 < last; c0 += ata::kMaxBatchNarrow) {
+          std::memset(&nbatch, 0, sizeof(nbatch));
+          fill_batch(nbatch, c0, std::min(last, c0 + ata::kMaxBatchNarrow));
+          cudaError_t e = ata::launch_batch_f64_narrow(nbatch, s);
+          if (e != cudaSuccess) return cuda_fail(e, "product launch");
+        }
         return ATA_OK;
       }
     }

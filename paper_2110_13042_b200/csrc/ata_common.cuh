@@ -66,6 +66,26 @@ constexpr int kNarrowDests = 2;
 constexpr int kMaxBatchNarrow = 104;
 using BatchArgsNarrow64 = BatchArgsT<double, kNarrowDests, kMaxBatchNarrow>;
 
+// Unbounded FP64 batches of region-free narrow products: descriptors live in
+// device memory (uploaded once per distinct batch, cached by content), with a
+// tile -> product table; one persistent launch runs thousands of small
+// products (breadth-first reference plans) with every CTA pipelining across
+// many tiles.
+template <typename T, int MAXD>
+struct BatchArgsG {
+  int count;
+  int total_tiles;
+  double alpha;
+  int* sync;
+  int n_sync;
+  int dynamic;
+  int dbg;
+  const DProdT<T, MAXD>* gp;   // device array [count]
+  const int* tile_prod;        // device array [total_tiles]: product of each tile
+};
+using BatchArgsGlobal64 = BatchArgsG<double, kNarrowDests>;
+constexpr int kMaxBatchGlobal = 1 << 20;
+
 template <typename T>
 struct EwArgs {  // elementwise op: rows x cols iteration space
   int rows, cols, nsrc, ndst;
@@ -79,6 +99,11 @@ struct EwArgs {  // elementwise op: rows x cols iteration space
 cudaError_t launch_batch_f64(const BatchArgs<double>& a, cudaStream_t s);
 cudaError_t launch_batch_f64_ws(const BatchArgs<double>& a, cudaStream_t s);
 cudaError_t launch_batch_f64_narrow(const BatchArgsNarrow64& a, cudaStream_t s);
+// count narrow region-free products with descriptors in host memory; returns
+// cudaErrorNotReady when the descriptors are not resident and the stream is
+// capturing a graph (the caller then launches them in narrow batches)
+cudaError_t launch_batch_f64_global(DProdT<double, kNarrowDests>* prods, int count, double alpha, int* sync,
+                                    cudaStream_t s);
 bool f64_narrow_supported();
 bool f64_supports_ordering();
 cudaError_t launch_batch_f32(const BatchArgs<float>& a, cudaStream_t s, bool split);

@@ -28,6 +28,10 @@
 // waits for turns of strictly earlier tiles, which are already running.
 #include <cstdlib>
 
+#include <unordered_map>
+#include <map>
+#include <vector>
+#include <cstring>
 #include "ata_common.cuh"
 
 namespace ata {
@@ -148,11 +152,47 @@ struct TileInfo {
   int pi, ti, tj;
 };
 
+// product descriptors: in the kernel parameters (BatchArgsT) or in device memory (BatchArgsG)
+template <typename T, int D, int B>
+__device__ __forceinline__ const DProdT<T, D>& prod_of(const BatchArgsT<T, D, B>& a, int i) {
+  return a.p[i];
+}
+template <typename T, int D>
+__device__ __forceinline__ const DProdT<T, D>& prod_of(const BatchArgsG<T, D>& a, int i) {
+  return a.gp[i];
+}
+template <typename T, int D, int B>
+__device__ __forceinline__ int prod_index(const BatchArgsT<T, D, B>& a, int tile) {
+  int pi = 0;
+  while (pi + 1 < a.count && tile >= a.p[pi + 1].tile_begin) ++pi;
+  return pi;
+}
+template <typename T, int D>
+__device__ __forceinline__ int prod_index(const BatchArgsG<T, D>& a, int tile) {
+  return __ldg(a.tile_prod + tile);
+}
+
+// How a role holds its tile's descriptor: parameter-space descriptors by
+// reference (constant bank), device-memory descriptors by value (registers /
+// local memory) -- global loads could not be hoisted across the epilogue's
+// stores and would be re-issued per element.
+template <typename Args>
+struct ProdHold {
+  using type = const DProdT<double, kMaxDests>&;
+};
+template <int B>
+struct ProdHold<BatchArgsT<double, kNarrowDests, B>> {
+  using type = const DProdT<double, kNarrowDests>&;
+};
+template <>
+struct ProdHold<BatchArgsGlobal64> {
+  using type = const DProdT<double, kNarrowDests>;
+};
+
 template <typename Args>
 __device__ __forceinline__ TileInfo decode_tile(const Args& args, int tile) {
-  int pi = 0;
-  while (pi + 1 < args.count && tile >= args.p[pi + 1].tile_begin) ++pi;
-  const auto& P = args.p[pi];
+  const int pi = prod_index(args, tile);
+  const auto& P = prod_of(args, pi);
   const int local = tile - P.tile_begin;
   TileInfo t;
   t.pi = pi;
@@ -223,7 +263,7 @@ __global__ void __launch_bounds__(ws64::THREADS, 1)
       }
       if (tile >= args.total_tiles) break;
       const TileInfo tl = decode_tile(args, tile);
-      const auto& P = args.p[tl.pi];
+      typename ProdHold<Args>::type P = prod_of(args, tl.pi);
       const bool syrk = P.kind == kSyrk;
       const bool same = syrk && tl.ti == tl.tj;
       const int ns = P.ns, nt = syrk ? 1 : P.nt;
@@ -307,7 +347,7 @@ __global__ void __launch_bounds__(ws64::THREADS, 1)
     if (lane == 0) mbar_arrive(&tempty[slot]);
     if (tile >= args.total_tiles) break;
     const TileInfo tl = decode_tile(args, tile);
-    const auto& P = args.p[tl.pi];
+    typename ProdHold<Args>::type P = prod_of(args, tl.pi);
     const bool syrk = P.kind == kSyrk;
     const bool same = syrk && tl.ti == tl.tj;
     const int i0 = tl.ti * BM, j0 = tl.tj * BN;
@@ -354,8 +394,8 @@ __global__ void __launch_bounds__(ws64::THREADS, 1)
       if (D.sem >= 0 && !(args.dbg & 1)) {
         // turn = earlier products of the launch whose window in this region covers the tile
         for (int q = 0; q < tl.pi; ++q)
-          for (int e = 0; e < args.p[q].nd; ++e) {
-            const DDest<double>& E = args.p[q].d[e];
+          for (int e = 0; e < prod_of(args, q).nd; ++e) {
+            const DDest<double>& E = prod_of(args, q).d[e];
             if (E.sem == D.sem && i0 < E.rows && j0 < E.cols) ++turn;
           }
         sem = args.sync + D.sem + tl.ti * D.sem_ld + tl.tj;
@@ -411,6 +451,7 @@ __global__ void __launch_bounds__(ws64::THREADS, 1)
   }
 }
 
+
 static int num_sms() {
   static int n = 0;
   if (n == 0) {
@@ -420,6 +461,27 @@ static int num_sms() {
     if (n <= 0) n = 148;
   }
   return n;
+}
+
+template <int BK, int NS, int NT, typename Args>
+static cudaError_t ws_kernel_launch(const Args& a, long long total, cudaStream_t s) {
+  using namespace ws64;
+  constexpr int STAGE_BYTES = (NS + NT) * BK * LD * 8;
+  constexpr int STAGES =
+      (SMEM_BUDGET - 1024) / STAGE_BYTES > 8 ? 8 : (SMEM_BUDGET - 1024) / STAGE_BYTES;
+  static_assert(STAGES >= 2, "smem");
+  const size_t smem = (size_t)STAGES * STAGE_BYTES + (2 * STAGES + 2 * TSLOTS) * sizeof(uint64_t) +
+                      (TSLOTS + 2) * sizeof(int);
+  auto kern = prod_f64_ws_kernel<BK, NS, NT, STAGES, Args>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    attr_set = true;
+  }
+  const int grid = (int)(total < num_sms() ? total : num_sms());
+  kern<<<grid, THREADS, smem, s>>>(a);
+  return cudaGetLastError();
 }
 
 template <int BK, int NS, int NT, typename Args>
@@ -477,22 +539,7 @@ static cudaError_t launch_ws(Args a, cudaStream_t s) {
     e = cudaMemsetAsync(a.sync, 0, (size_t)n_sync * sizeof(int), s);
     if (e != cudaSuccess) return e;
   }
-  constexpr int STAGE_BYTES = (NS + NT) * BK * LD * 8;
-  constexpr int STAGES =
-      (SMEM_BUDGET - 1024) / STAGE_BYTES > 8 ? 8 : (SMEM_BUDGET - 1024) / STAGE_BYTES;
-  static_assert(STAGES >= 2, "smem");
-  const size_t smem = (size_t)STAGES * STAGE_BYTES + (2 * STAGES + 2 * TSLOTS) * sizeof(uint64_t) +
-                      (TSLOTS + 2) * sizeof(int);
-  auto kern = prod_f64_ws_kernel<BK, NS, NT, STAGES, Args>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
-  const int grid = (int)(total < num_sms() ? total : num_sms());
-  kern<<<grid, THREADS, smem, s>>>(a);
-  return cudaGetLastError();
+  return ws_kernel_launch<BK, NS, NT>(a, total, s);
 }
 
 template <typename Args>
@@ -520,6 +567,115 @@ static cudaError_t launch_ws_any(const Args& a, cudaStream_t s) {
 }
 
 cudaError_t launch_batch_f64_ws(const BatchArgs<double>& a, cudaStream_t s) { return launch_ws_any(a, s); }
+
+// ---- device-resident descriptors (BatchArgsG) ----
+namespace {
+struct DescEntry {
+  std::vector<unsigned char> host;  // exact bytes (descriptors + tile table) for hit checks
+  void* dev = nullptr;
+  uint64_t last_use = 0;
+};
+struct DescCache {
+  std::unordered_map<uint64_t, DescEntry> map;
+  size_t bytes = 0;
+  uint64_t clock = 0;
+};
+DescCache& desc_cache() {
+  static std::map<int, DescCache> per_device;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  return per_device[dev];
+}
+uint64_t blob_hash(const unsigned char* p, size_t n) {  // 64-bit words (blobs are 8-byte multiples)
+  uint64_t h = 1469598103934665603ull ^ n;
+  const uint64_t* w = reinterpret_cast<const uint64_t*>(p);
+  for (size_t i = 0; i < n / 8; ++i) {
+    h ^= w[i] + 0x9e3779b97f4a7c15ull + (h << 6) + (h >> 2);
+    h *= 1099511628211ull;
+  }
+  return h;
+}
+}  // namespace
+
+cudaError_t launch_batch_f64_global(DProdT<double, kNarrowDests>* prods, int count, double alpha, int* sync,
+                                    cudaStream_t s) {
+  using namespace ws64;
+  long long total = 0;
+  int ns = 1, nt = 1;
+  for (int i = 0; i < count; ++i) {
+    auto& p = prods[i];
+    p.tn = (p.n + BM - 1) / BM;
+    p.tk = (p.k + BN - 1) / BN;
+    p.tile_begin = (int)total;
+    total += p.kind == kSyrk ? (long long)p.tn * (p.tn + 1) / 2 : (long long)p.tn * p.tk;
+    ns = max(ns, p.ns);
+    if (p.kind != kSyrk) nt = max(nt, p.nt);
+    for (int d = 0; d < p.nd; ++d) p.d[d].sem = -1;  // region-free by contract
+  }
+  if (total <= 0) return cudaSuccess;
+  if (total > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  const size_t dbytes = sizeof(DProdT<double, kNarrowDests>) * (size_t)count;
+  std::vector<unsigned char> blob(dbytes + ((sizeof(int) * (size_t)total + 7) & ~size_t(7)), 0);
+  std::memcpy(blob.data(), prods, dbytes);
+  int* tp = reinterpret_cast<int*>(blob.data() + dbytes);
+  for (int i = 0; i < count; ++i) {
+    const auto& p = prods[i];
+    const long long nt_i = p.kind == kSyrk ? (long long)p.tn * (p.tn + 1) / 2 : (long long)p.tn * p.tk;
+    for (long long t = 0; t < nt_i; ++t) tp[p.tile_begin + t] = i;
+  }
+  DescCache& cache = desc_cache();
+  const uint64_t key = blob_hash(blob.data(), blob.size());
+  auto it = cache.map.find(key);
+  if (it == cache.map.end() || it->second.host != blob) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    cudaStreamIsCapturing(s, &cs);
+    if (cs != cudaStreamCaptureStatusNone) return cudaErrorNotReady;  // no uploads inside a capture
+    if (it != cache.map.end()) {  // hash collision: replace
+      cudaFree(it->second.dev);
+      cache.bytes -= it->second.host.size();
+      cache.map.erase(it);
+    }
+    // evict least recently used entries beyond 256 MB
+    while (cache.bytes + blob.size() > (256u << 20) && !cache.map.empty()) {
+      auto lru = cache.map.begin();
+      for (auto j = cache.map.begin(); j != cache.map.end(); ++j)
+        if (j->second.last_use < lru->second.last_use) lru = j;
+      cudaStreamSynchronize(s);  // the evicted buffer may be in use by queued work
+      cudaFree(lru->second.dev);
+      cache.bytes -= lru->second.host.size();
+      cache.map.erase(lru);
+    }
+    DescEntry ent;
+    cudaError_t e = cudaMalloc(&ent.dev, blob.size());
+    if (e != cudaSuccess) return e;
+    e = cudaMemcpy(ent.dev, blob.data(), blob.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return e;
+    ent.host = std::move(blob);
+    cache.bytes += ent.host.size();
+    it = cache.map.emplace(key, std::move(ent)).first;
+  }
+  it->second.last_use = ++cache.clock;
+  BatchArgsGlobal64 a;
+  std::memset(&a, 0, sizeof(a));
+  a.count = count;
+  a.total_tiles = (int)total;
+  a.alpha = alpha;
+  // dynamic tile queue: the group mixes long (diagonal / merged) and short products
+  a.dynamic = sync != nullptr;
+  a.sync = sync;
+  a.n_sync = 1;
+  if (a.dynamic) {
+    cudaError_t e = cudaMemsetAsync(sync, 0, sizeof(int), s);
+    if (e != cudaSuccess) return e;
+  }
+  { const char* e = std::getenv("ATA_DBG"); a.dbg = e ? std::atoi(e) : 0; }
+  a.gp = reinterpret_cast<const DProdT<double, kNarrowDests>*>(it->second.dev);
+  a.tile_prod = reinterpret_cast<const int*>(reinterpret_cast<const unsigned char*>(it->second.dev) + dbytes);
+  if (ns == 1 && nt == 1) return ws_kernel_launch<16, 1, 1>(a, total, s);
+  if (ns == 2 && nt == 1) return ws_kernel_launch<16, 2, 1>(a, total, s);
+  if (ns == 1 && nt == 2) return ws_kernel_launch<16, 1, 2>(a, total, s);
+  return ws_kernel_launch<16, 2, 2>(a, total, s);
+}
 cudaError_t launch_batch_f64_ws_narrow(const BatchArgsNarrow64& a, cudaStream_t s) { return launch_ws_any(a, s); }
 
 }  // namespace ata
