@@ -156,6 +156,10 @@ int ata_run_plan(int dtype, const ata_op* ops, int32_t n_ops, const void* A, int
 /* int32 entries of `sync` that ata_run_plan needs for this op list (host-only query). */
 int64_t ata_sync_ints_needed(int dtype, const ata_op* ops, int32_t n_ops);
 
+/* Kernel launches the executor has issued since the library was loaded
+ * (benchmark accounting; a captured graph replays without new calls). */
+int64_t ata_launch_count(void);
+
 #ifdef __cplusplus
 }
 #endif

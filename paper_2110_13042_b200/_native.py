@@ -38,7 +38,7 @@ OP_DTYPE = np.dtype([("type", "<i4"), ("m", "<i4"), ("n", "<i4"), ("k", "<i4"),
 EXPORTS = [
     "ata_last_error", "ata_strerror", "ata_version", "ata_abi_op_size",
     "ata_syrk_lower", "ata_gemm_atb", "ata_add_truncated", "ata_mirror_lower",
-    "ata_pack_lower", "ata_unpack_lower", "ata_run_plan", "ata_sync_ints_needed",
+    "ata_pack_lower", "ata_unpack_lower", "ata_run_plan", "ata_sync_ints_needed", "ata_launch_count",
 ]
 
 _CODE_TO_EXC = {
@@ -82,6 +82,8 @@ def load() -> ctypes.CDLL:
                                  c_vp, c_i64, c_vp, c_i64, c_dbl, c_vp]
     lib.ata_sync_ints_needed.argtypes = [ctypes.c_int, c_vp, c_i32]
     lib.ata_sync_ints_needed.restype = ctypes.c_int64
+    lib.ata_launch_count.restype = ctypes.c_int64
+    lib.ata_launch_count.argtypes = []
     for name in EXPORTS:
         getattr(lib, name).restype = getattr(lib, name).restype or ctypes.c_int
     if lib.ata_abi_op_size() != OP_DTYPE.itemsize:

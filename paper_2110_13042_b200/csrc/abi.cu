@@ -11,12 +11,16 @@
 #include <cstring>
 #include <string>
 #include <algorithm>
+#include <atomic>
 #include <map>
 #include <type_traits>
 #include <vector>
 
 #include "../../include/atamul_b200.h"
 #include "ata_common.cuh"
+
+// kernel launches issued through the executor (reported by ata_launch_count)
+static std::atomic<long long> g_launches{0};
 
 namespace {
 
@@ -414,6 +418,7 @@ int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, int* sync, int64_t 
           vb.p = prods.data();
           fill_batch(vb, first, last);
           cudaError_t e = ata::launch_batch_f64_global(prods.data(), vb.count, alpha, sync, s);
+          g_launches += 1;
           if (e == cudaSuccess) return ATA_OK;
           if (e != cudaErrorNotReady) return cuda_fail(e, "product launch");
           // capturing a graph with descriptors not yet resident: narrow batches instead
@@ -421,6 +426,7 @@ int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, int* sync, int64_t 
             std::memset(&nbatch, 0, sizeof(nbatch));
             fill_batch(nbatch, c0, std::min(last, c0 + ata::kMaxBatchNarrow));
             e = ata::launch_batch_f64_narrow(nbatch, s);
+            g_launches += 1;
             if (e != cudaSuccess) return cuda_fail(e, "product launch");
           }
           return ATA_OK;
@@ -429,6 +435,7 @@ int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, int* sync, int64_t 
           std::memset(&nbatch, 0, sizeof(nbatch));
           fill_batch(nbatch, c0, std::min(last, c0 + ata::kMaxBatchNarrow));
           cudaError_t e = ata::launch_batch_f64_narrow(nbatch, s);
+          g_launches += 1;
           if (e != cudaSuccess) return cuda_fail(e, "product launch");
         }
         return ATA_OK;
@@ -437,6 +444,7 @@ int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, int* sync, int64_t 
     std::memset(&batch, 0, sizeof(batch));
     fill_batch(batch, first, last);
     cudaError_t e = launch_batch<T>(batch, s, dtype);
+    g_launches += 1;
     if (e != cudaSuccess) return cuda_fail(e, "product launch");
     return ATA_OK;
   };
@@ -490,6 +498,7 @@ int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, int* sync, int64_t 
   };
   auto on_ew = [&](int i) -> int {
     if (int rc = join_all()) return rc;
+    g_launches += 1;
     const ata_op& op = ops[i];
     cudaError_t e = cudaSuccess;
     if (op.type == ATA_OP_COMBO || op.type == ATA_OP_UPDATE) {
@@ -543,12 +552,14 @@ int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, int* sync, int64_t 
       }
       for (int i = first; i < last; ++i) args.push_back(combo4_args<T>(ops[i], b));
       e = ata::launch_combo4_multi<T>(args.data(), (int)args.size(), s);
+      g_launches += (long long)(args.size() + 103) / 104;
     } else {
       for (int i = first; i < last; ++i) {
         args.push_back(postadd7_args<T>(ops[i], b));
         acc.push_back(ops[i].accumulate);
       }
       e = ata::launch_postadd7_multi<T>(args.data(), acc.data(), (int)args.size(), s);
+      g_launches += (long long)(args.size() + 95) / 96;
     }
     if (e != cudaSuccess) return cuda_fail(e, "elementwise launch");
     return ATA_OK;
@@ -579,6 +590,7 @@ const char* ata_strerror(int code) {
 }
 
 int ata_version(void) { return 100; }
+int64_t ata_launch_count(void) { return (int64_t)g_launches.load(); }
 int ata_abi_op_size(void) { return (int)sizeof(ata_op); }
 
 int64_t ata_sync_ints_needed(int dtype, const ata_op* ops, int32_t n_ops) {
