@@ -78,14 +78,27 @@ class ClockSampler:
         self.proc = None
 
     def __enter__(self):
+        # the sampler's first line is awaited before the timed region starts and
+        # one synchronous query follows it, so a timed region shorter than the
+        # 200 ms period (c1, c2) is still bracketed by samples
+        self.first = ""
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
                  "--format=csv,noheader,nounits", "-lms", "200"],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.first = self.proc.stdout.readline()
         except FileNotFoundError:
             self.proc = None
         return self
+
+    def _query(self):
+        try:
+            return subprocess.run(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                   "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                  timeout=10).stdout
+        except Exception:
+            return ""
 
     def __exit__(self, *exc):
         self.summary = {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
@@ -93,6 +106,9 @@ class ClockSampler:
             return False
         self.proc.terminate()
         out, _ = self.proc.communicate(timeout=10)
+        out = self.first + out
+        if len(out.strip().splitlines()) < 2:
+            out += "\n" + self._query()
         sm, smax, reasons = [], [], set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         for line in out.strip().splitlines():
