@@ -355,7 +355,7 @@ int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, int* sync, int64_t 
   }
   const bool ordering = supports_ordering<T>();
   ata::BatchArgs<T> batch;
-  static ata::BatchArgsNarrow64 nbatch;  // 28 KB: not on the stack
+  thread_local static ata::BatchArgsNarrow64 nbatch;  // 28 KB: not on the stack
   const bool narrow = std::is_same<T, double>::value && ata::f64_narrow_supported();
   auto fill_batch = [&](auto& batch, int first, int last) {
     batch.alpha = alpha;
