@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <atomic>
 #include <map>
+#include <mutex>
 #include <type_traits>
 #include <vector>
 
@@ -297,13 +298,17 @@ struct ForkJoin {
   cudaStream_t aux[K];
   cudaEvent_t fork, done[K];
   bool ok = false;
-  static ForkJoin& get() {
-    static std::map<int, ForkJoin> per_device;
+  // one set per (device, calling stream): plans on different streams (other
+  // host threads) never share fork/join events
+  static ForkJoin& get(cudaStream_t s) {
+    static std::mutex mu;
+    static std::map<std::pair<int, cudaStream_t>, ForkJoin> per_stream;
     int dev = 0;
     cudaGetDevice(&dev);
-    auto it = per_device.find(dev);
-    if (it != per_device.end()) return it->second;
-    ForkJoin& f = per_device[dev];
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = per_stream.find({dev, s});
+    if (it != per_stream.end()) return it->second;
+    ForkJoin& f = per_stream[{dev, s}];
     bool ok = cudaEventCreateWithFlags(&f.fork, cudaEventDisableTiming) == cudaSuccess;
     for (int k = 0; k < K && ok; ++k)
       ok = cudaStreamCreateWithFlags(&f.aux[k], cudaStreamNonBlocking) == cudaSuccess &&
@@ -452,7 +457,7 @@ int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, int* sync, int64_t 
   // order shared destinations (turn counters in the sync buffer), they run
   // concurrently on auxiliary streams forked from / joined back into `s`, so
   // groups of many small products fill the machine (graph-capturable).
-  ForkJoin& fj = ForkJoin::get();
+  ForkJoin& fj = ForkJoin::get(s);
   bool prev_cont = false;
   int aux_next = 0;
   bool forked = false, aux_used[ForkJoin::K] = {false};

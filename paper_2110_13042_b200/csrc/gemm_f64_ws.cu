@@ -30,6 +30,7 @@
 
 #include <unordered_map>
 #include <map>
+#include <mutex>
 #include <vector>
 #include <cstring>
 #include "ata_common.cuh"
@@ -580,7 +581,11 @@ struct DescCache {
   size_t bytes = 0;
   uint64_t clock = 0;
 };
-DescCache& desc_cache() {
+std::mutex& desc_mutex() {
+  static std::mutex mu;
+  return mu;
+}
+DescCache& desc_cache() {  // caller holds desc_mutex()
   static std::map<int, DescCache> per_device;
   int dev = 0;
   cudaGetDevice(&dev);
@@ -623,6 +628,7 @@ cudaError_t launch_batch_f64_global(DProdT<double, kNarrowDests>* prods, int cou
     const long long nt_i = p.kind == kSyrk ? (long long)p.tn * (p.tn + 1) / 2 : (long long)p.tn * p.tk;
     for (long long t = 0; t < nt_i; ++t) tp[p.tile_begin + t] = i;
   }
+  std::lock_guard<std::mutex> lock(desc_mutex());
   DescCache& cache = desc_cache();
   const uint64_t key = blob_hash(blob.data(), blob.size());
   auto it = cache.map.find(key);
