@@ -88,6 +88,20 @@ def run_plan(plan, dtype_code, A, a_elems, C, c_elems, alpha, ws=None, ws_elems=
     nat.check(rc)
 
 
+_CAPTURE_STREAMS: dict = {}
+
+
+def _capture_stream():
+    """One capture stream per device (the executor keeps fork/join resources
+    per calling stream)."""
+    import torch
+    dev = torch.cuda.current_device()
+    st = _CAPTURE_STREAMS.get(dev)
+    if st is None:
+        st = _CAPTURE_STREAMS[dev] = torch.cuda.Stream()
+    return st
+
+
 class PlanGraph:
     """One plan execution with fixed pointers captured as a CUDA graph.
 
@@ -100,7 +114,7 @@ class PlanGraph:
                  B=None, b_elems=0):
         import torch
         self.graph = torch.cuda.CUDAGraph()
-        side = torch.cuda.Stream()
+        side = _capture_stream()
         side.wait_stream(torch.cuda.current_stream())
         with torch.cuda.graph(self.graph, stream=side):
             run_plan(plan, dtype_code, A, a_elems, C, c_elems, alpha, ws=ws, ws_elems=ws_elems,
