@@ -386,6 +386,10 @@ def main():
                 "executed_flops_per_step": prod_flops // args.steps,
                 "algorithmic_flops_per_step": m * n * n,
                 "avg_launch_ms": prod_ms / max(1, prod_launches)}
+    try:   # DRAM bytes per launch of the dominant kernel from the committed ncu capture
+        roofline["traffic"] = json.load(open(os.path.join(ROOT, "profiles", "traffic.json")))[args.config]
+    except Exception:
+        pass
     hbm_peak = 6549.4
     try:
         hbm_peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
