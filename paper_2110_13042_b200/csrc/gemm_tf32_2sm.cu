@@ -7,11 +7,22 @@
 // bounds the single-CTA kernel on the tall-skinny config c5 (~11.6 TB/s of
 // L2->SM traffic measured).
 //
-// Roles per CTA (192 threads): warp 0 TMA producer (both CTAs load their halves,
-// completion counted on the leader's barrier), warp 1 TMEM allocation (both
-// CTAs, cta_group::2) + MMA issue (leader only), warps 2-5 epilogue (each CTA
-// drains its own 128 accumulator rows).  Every wait is bounded: a protocol
-// error traps instead of hanging the GPU.
+// Roles per CTA (192 threads): warp 0 TMA producer (both CTAs load their
+// halves, completion counted on the leader's barrier; windows that are whole
+// 32-column panels use a 3-D tensor map -- [panels][rows][32 cols], panel
+// stride 128 B -- so one instruction moves a CTA's [4 panels][BK rows][32 cols]
+// operand box), warp 1 TMEM allocation (both CTAs, cta_group::2) + MMA issue
+// (leader only), warps 2-5 epilogue (each CTA drains its own 128 accumulator
+// rows).  Every wait is bounded: a protocol error traps instead of hanging the
+// GPU.
+//
+// Measured bound (ncu, c5 launch): tensor pipe 94 % active while the executed
+// rate is ~69 % of the smem-resident issue-rate probe -- shared memory serves
+// the MMA operand reads and the TMA writes of the next stages at once.  A
+// 256 x 512 tile per pair (two N = 256 MMAs, single-buffered TMEM) cut the
+// L2->SM bytes by 22 % but was slower (11.0-11.9 ms vs 9.2-9.6 ms per c5 plan):
+// each MMA re-reads its A panel from smem, the epilogue stalls the tensor
+// pipe, and DRAM reads rose (17 -> 26 GB) with four chunks in flight.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
@@ -22,9 +33,27 @@
 
 namespace ata {
 
+// A/B experiment knobs (tools/ab_build.py -DTC2_...): pipeline depth, k-block
+// rows, rows per TMEM accumulator, epilogue without global traffic.  Measured on
+// c5 (tools/tf32_ab.py, whole plan incl. the 2.8 ms rounding pass): BK 32 /
+// 6 stages 10.9 ms with 2-D boxes, 10.1 ms with 3-D boxes; BK 48 / 4 stages
+// 9.2-9.6 ms; BK 64 / 3 stages 9.7 ms; BK 16 / 12 stages 12.4 ms -- a fixed
+// cost per k-block (TMA issue + barrier round trip), so fewer, larger blocks.
+#ifndef TC2_STAGES
+#define TC2_STAGES 4
+#endif
+#ifndef TC2_BK
+#define TC2_BK 48
+#endif
+#ifndef TC2_KROWS
+#define TC2_KROWS 8192
+#endif
+#ifndef TC2_NOEPI
+#define TC2_NOEPI 0
+#endif
 namespace tc2 {
-constexpr int BM = 256, BN = 256, BK = 32, STAGES = 6;   // per pair
-constexpr int KSUB = 256;  // k-blocks per TMEM accumulator (see gemm_tf32_tc.cu: fp32 accumulation bias)
+constexpr int BM = 256, BN = 256, BK = TC2_BK, STAGES = TC2_STAGES;   // per pair
+constexpr int KSUB = TC2_KROWS / BK;  // k-blocks per TMEM accumulator (see gemm_tf32_tc.cu: fp32 accumulation bias)
 constexpr int HALF = 128;                                 // rows of A / cols of B per CTA
 constexpr int A_BYTES = BK * HALF * 4;                    // 16 KB
 constexpr int B_BYTES = BK * HALF * 4;                    // 16 KB
@@ -51,6 +80,7 @@ struct Tc2Args {
   Tc2Prod p[tc2::kMax];
   int count;
   int total_tiles;
+  int tma3d;  // 1: every window is a whole number of 32-column panels -> 3-D maps, one TMA per operand
 };
 static_assert(sizeof(Tc2Args) <= 32000, "kernel parameter space (CUDA 12.1+: 32 KB)");
 
@@ -96,7 +126,7 @@ __device__ __forceinline__ void t2_cluster_sync() {
 __device__ __forceinline__ uint64_t t2_desc(uint32_t saddr) {
   uint64_t d = 0;
   d |= (uint64_t)((saddr >> 4) & 0x3FFF);
-  d |= (uint64_t)((4096 >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)(((tc2::BK * 128) >> 4) & 0x3FFF) << 16;  // LBO: 32-column panels of BK rows
   d |= (uint64_t)((512 >> 4) & 0x3FFF) << 32;
   d |= (uint64_t)1 << 46;
   d |= (uint64_t)1 << 61;  // SWIZZLE_128B_BASE32B (MN-major 32-bit)
@@ -189,20 +219,34 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(t2_smem(&full[s])),
                          "r"(2 * STAGE_BYTES)
                          : "memory");
-#pragma unroll
-          for (int g = 0; g < HALF / 32; ++g)
+          if (args.tma3d) {
+            // one box of [HALF/32 panels][BK rows][32 cols] per operand (3-D map)
             asm volatile(
-                "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-                " [%0], [%1, {%3, %4}], [%2];" ::"r"(t2_smem(sa + g * 4096)),
-                "l"(reinterpret_cast<uint64_t>(&P.ts)), "r"(bar), "r"(i0 + g * 32), "r"(kb * BK)
+                "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(t2_smem(sa)),
+                "l"(reinterpret_cast<uint64_t>(&P.ts)), "r"(bar), "r"(0), "r"(kb * BK), "r"(i0 / 32)
                 : "memory");
-#pragma unroll
-          for (int g = 0; g < HALF / 32; ++g)
             asm volatile(
-                "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
-                " [%0], [%1, {%3, %4}], [%2];" ::"r"(t2_smem(sb + g * 4096)),
-                "l"(reinterpret_cast<uint64_t>(mt)), "r"(bar), "r"(j0 + g * 32), "r"(kb * BK)
+                "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(t2_smem(sb)),
+                "l"(reinterpret_cast<uint64_t>(mt)), "r"(bar), "r"(0), "r"(kb * BK), "r"(j0 / 32)
                 : "memory");
+          } else {
+#pragma unroll
+            for (int g = 0; g < HALF / 32; ++g)
+              asm volatile(
+                  "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                  " [%0], [%1, {%3, %4}], [%2];" ::"r"(t2_smem(sa + g * BK * 128)),
+                  "l"(reinterpret_cast<uint64_t>(&P.ts)), "r"(bar), "r"(i0 + g * 32), "r"(kb * BK)
+                  : "memory");
+#pragma unroll
+            for (int g = 0; g < HALF / 32; ++g)
+              asm volatile(
+                  "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                  " [%0], [%1, {%3, %4}], [%2];" ::"r"(t2_smem(sb + g * BK * 128)),
+                  "l"(reinterpret_cast<uint64_t>(mt)), "r"(bar), "r"(j0 + g * 32), "r"(kb * BK)
+                  : "memory");
+          }
         }
       }
     }
@@ -283,7 +327,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
               "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
             : "r"(addr));
         asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-        if (row < P.drows) {
+        if (!TC2_NOEPI && row < P.drows) {
           const int col0 = t.tj * BN + c * 32;
           int cmax = P.dcols - col0;
           if (syrk) cmax = min(cmax, row - col0 + 1);
@@ -332,20 +376,38 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
 }
 
 // ---------------------------------------------------------------- host side
-static bool t2_map_term(CUtensorMap* map, const DTerm<float>& t) {
+static PFN_cuTensorMapEncodeTiled_v12000 t2_encoder() {
   static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
   if (enc == nullptr) {
     cudaDriverEntryPointQueryResult q;
     void* p = nullptr;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
         q != cudaDriverEntryPointSuccess)
-      return false;
+      return nullptr;
     enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return enc;
+}
+
+// 2-D map: boxes of [BK rows][32 cols] (one 128-byte swizzle span).  3-D map
+// (window cols a multiple of 32): the window seen as [panels][rows][32 cols]
+// (panel stride 128 B), boxes of [HALF/32 panels][BK rows][32 cols] -- the
+// smem panel layout the UMMA descriptors expect, in one TMA instruction.
+static bool t2_map_term(CUtensorMap* map, const DTerm<float>& t, bool three_d) {
+  auto enc = t2_encoder();
+  if (enc == nullptr) return false;
+  cuuint32_t estr[3] = {1, 1, 1};
+  if (three_d) {
+    cuuint64_t dims[3] = {32, (cuuint64_t)t.rows, (cuuint64_t)(t.cols / 32)};
+    cuuint64_t strides[2] = {(cuuint64_t)t.ld * 4, 128};
+    cuuint32_t box[3] = {32, tc2::BK, tc2::HALF / 32};
+    return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(t.p), dims, strides, box, estr,
+               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+               CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
   }
   cuuint64_t dims[2] = {(cuuint64_t)t.cols, (cuuint64_t)t.rows};
   cuuint64_t strides[1] = {(cuuint64_t)t.ld * 4};
-  cuuint32_t box[2] = {32, 32};
-  cuuint32_t estr[2] = {1, 1};
+  cuuint32_t box[2] = {32, tc2::BK};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(t.p), dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
@@ -372,11 +434,21 @@ cudaError_t launch_tf32_2sm(const DProd<float>* prods, int count, double alpha, 
     long long total = 0;
     int ptiles[kMax], pkinds[kMax];
     const int n = count - base < kMax ? count - base : kMax;
+#ifndef TC2_NO3D
+    bool three_d = true;
+#else
+    bool three_d = false;
+#endif
+    for (int i = 0; i < n; ++i) {
+      const DProd<float>& p = prods[base + i];
+      three_d = three_d && p.s[0].cols % 32 == 0 && (p.kind == kSyrk || p.t[0].cols % 32 == 0);
+    }
+    a.tma3d = three_d ? 1 : 0;
     for (int i = 0; i < n; ++i) {
       const DProd<float>& p = prods[base + i];
       Tc2Prod& q = a.p[i];
-      if (!t2_map_term(&q.ts, p.s[0])) return cudaErrorInvalidValue;
-      if (p.kind != kSyrk && !t2_map_term(&q.tt, p.t[0])) return cudaErrorInvalidValue;
+      if (!t2_map_term(&q.ts, p.s[0], three_d)) return cudaErrorInvalidValue;
+      if (p.kind != kSyrk && !t2_map_term(&q.tt, p.t[0], three_d)) return cudaErrorInvalidValue;
       q.d = p.d[0].p;
       q.ld = p.d[0].ld;
       q.drows = p.d[0].rows;
@@ -397,7 +469,11 @@ cudaError_t launch_tf32_2sm(const DProd<float>* prods, int count, double alpha, 
     a.count = n;
     a.total_tiles = (int)total;
     if (total == 0) continue;
+#ifdef TC2_MAXCL
+    const int clusters = periodic_workers(ptiles, pkinds, n, total, TC2_MAXCL);
+#else
     const int clusters = periodic_workers(ptiles, pkinds, n, total, sms / 2);
+#endif
     prod_tf32_2sm_kernel<<<clusters * 2, THREADS, smem, s>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
