@@ -55,6 +55,8 @@ def parse():
     p.add_argument("--leaf-cols", type=int, default=None)
     p.add_argument("--max-depth", type=int, default=None)
     p.add_argument("--min-dim", type=int, default=None)
+    p.add_argument("--fuse-leaf-sums", action="store_true",
+                   help="A/B: last Strassen level's operand sums summed in the product loads")
     p.add_argument("--dump-units", default=None, help="write per-launch timings (JSON) here")
     p.add_argument("--no-graph", action="store_true", help="eager launches for reference plans")
     return p.parse_args()
@@ -267,7 +269,9 @@ def main():
     packed = torch.empty(n * (n + 1) // 2, dtype=A.dtype, device=dev) if world > 1 else None
     params = auto_plan.AutoParams(**{k: v for k, v in (("leaf_cols", args.leaf_cols),
                                                         ("max_depth", args.max_depth),
-                                                        ("min_dim", args.min_dim)) if v is not None})
+                                                        ("min_dim", args.min_dim),
+                                                        ("fuse_leaf_sums", args.fuse_leaf_sums or None))
+                                                     if v is not None})
     mloc = r1 - r0
     if threshold == "auto":
         plan = auto_plan.plan_ata_auto(mloc, n, n, n, params, round_tf32=not f64)

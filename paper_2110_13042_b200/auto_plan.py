@@ -69,6 +69,11 @@ class AutoParams:
     min_chunk: int = 8192          # ... into chunks of at least this many rows
     tf32_tflops: float = 400.0     # single-pass TF32 leaf-product rate (tcgen05, profiles/)
     tf32_fill_waves: int = 8       # 128x256 tcgen05 tiles: more chunks to fill 148 SMs
+    fuse_leaf_sums: bool = False   # FP64: leaf products read their Strassen operand sums as two
+                                   # zero-extended terms summed in the kernel's load path (no
+                                   # combo4 pass for the last Strassen level).  Off: measured
+                                   # 2.1-2.2x slower on c3/c4 (the two-term kernel configuration
+                                   # runs at 14 TF/s vs 34 for plain operands)
     tail_split: bool = True        # FP64: K-split a group's trailing products (partial last wave)
     min_tail_rows: int = 1024      # ... only when every chunk keeps this many rows
 
@@ -97,6 +102,24 @@ def _quads(w: Win, r1: int, c1: int):
     quadrants beyond the actual extent are empty windows (zero-extended)."""
     return [_clip(w, 0, 0, r1, c1), _clip(w, 0, c1, r1, c1), _clip(w, r1, 0, r1, c1),
             _clip(w, r1, c1, r1, c1)]
+
+
+def _terms(x):
+    """A leaf operand as [(Win, coef)]: a plain window, or the <= 2 signed
+    quadrant terms of a fused Strassen operand sum."""
+    return [(x, 1.0)] if isinstance(x, Win) else list(x)
+
+
+def _clip_terms(x, r0: int, h: int):
+    """Rows [r0, r0 + h) of every term (contraction chunk); empty terms dropped
+    (an all-empty operand keeps one empty window: it reads as zero)."""
+    terms = [(_clip(w, r0, 0, h, w.cols), c) for w, c in _terms(x)]
+    out = [(w, c) for w, c in terms if w.rows and w.cols]
+    return out or terms[:1]
+
+
+def _empty(x) -> bool:
+    return all(w.rows == 0 or w.cols == 0 for w, _ in _terms(x))
 
 
 class _AutoPlanner:
@@ -155,7 +178,20 @@ class _AutoPlanner:
         if not self.worth_split(m, n, k, depth):
             leaves.append((m, n, k, a, b, out, sign, accumulate))
             return
-        S, T, m1, n1, k1 = self._sums(a, b, m, n, k)
+        m1, n1, k1 = _ceil2(m), _ceil2(n), _ceil2(k)
+        if (self.p.fuse_leaf_sums and self.esize == 8 and isinstance(a, Win) and isinstance(b, Win)
+                and not self.worth_split(m1, n1, k1, depth - 1)):
+            # the children are leaves: hand them their operand sums as two
+            # quadrant terms each (summed in the product kernel's load path)
+            # (positive term first: the kernel applies the sign to the second term)
+            S = [sorted([(w, float(c)) for w, c in zip(_quads(a, m1, n1), co) if c and w.rows and w.cols],
+                        key=lambda t: -t[1]) for co in _S]
+            T = [sorted([(w, float(c)) for w, c in zip(_quads(b, m1, k1), co) if c and w.rows and w.cols],
+                        key=lambda t: -t[1]) for co in _T]
+            if any(x and x[0][1] < 0 for x in S + T):   # a lone negative term: materialise instead
+                S, T, m1, n1, k1 = self._sums(a, b, m, n, k)
+        else:
+            S, T, m1, n1, k1 = self._sums(a, b, m, n, k)
         kids = [self.alloc(n1, k1) for _ in range(7)]
         for i in range(7):
             self.tree(S[i], T[i], m1, n1, k1, kids[i], 1.0, False, depth - 1, leaves, posts)
@@ -164,7 +200,7 @@ class _AutoPlanner:
     def emit(self, leaves, posts, extra=()):
         prods = []
         for (m, n, k, a, b, out, sign, accumulate) in leaves:
-            if a.rows == 0 or a.cols == 0 or b.rows == 0 or b.cols == 0:
+            if _empty(a) or _empty(b):
                 if not accumulate:            # an all-zero operand: the product buffer is zero
                     self.pb.fill(out)
                 continue
@@ -247,8 +283,8 @@ class _AutoPlanner:
         if S <= 1:
             split_from = self._tail_split(prods)
             for (kind, m, n, k, a, b, out, sign, accumulate) in prods[:split_from]:
-                T = [] if kind == "syrk" else [(b, 1.0)]
-                self.pb.product(kind, m, n, k, [(a, 1.0)], T, [(out, sign)],
+                T = [] if kind == "syrk" else _terms(b)
+                self.pb.product(kind, m, n, k, _terms(a), T, [(out, sign)],
                                 accumulate=int(accumulate), group=group)
             # tail products: K split into TAIL_CHUNKS ordered partial products
             # (chunk 0 writes, the rest accumulate in turn through the FP64
@@ -262,9 +298,9 @@ class _AutoPlanner:
                     rows = min(mc, m - r0)
                     if rows <= 0:
                         break
-                    ac = _clip(a, r0, 0, rows, a.cols)
-                    T = [] if kind == "syrk" else [(_clip(b, r0, 0, rows, b.cols), 1.0)]
-                    self.pb.product(kind, rows, n, k, [(ac, 1.0)], T, [(out, sign, region)],
+                    ac = _clip_terms(a, r0, rows)
+                    T = [] if kind == "syrk" else _clip_terms(b, r0, rows)
+                    self.pb.product(kind, rows, n, k, ac, T, [(out, sign, region)],
                                     accumulate=int(accumulate or c > 0), group=group)
             return
         # chunk-major order: the products of one row chunk are adjacent, so a
@@ -277,13 +313,13 @@ class _AutoPlanner:
                 rows = min(mc, m - r0)
                 if rows <= 0:
                     continue
-                ac = _clip(a, r0, 0, rows, a.cols)
-                bc = ac if b is None else _clip(b, r0, 0, rows, b.cols)
-                if ac.rows == 0 or bc.rows == 0:
+                ac = _clip_terms(a, r0, rows)
+                bc = ac if b is None else _clip_terms(b, r0, rows)
+                if _empty(ac) or _empty(bc):
                     continue
                 P = self.alloc(n, k)
-                T = [] if kind == "syrk" else [(bc, 1.0)]
-                self.pb.product(kind, rows, n, k, [(ac, 1.0)], T, [(P, 1.0)], accumulate=0,
+                T = [] if kind == "syrk" else bc
+                self.pb.product(kind, rows, n, k, ac, T, [(P, 1.0)], accumulate=0,
                                 group=group)
                 parts[pi].append(P)
         reductions = [(kind, out, sign, accumulate, parts[pi])

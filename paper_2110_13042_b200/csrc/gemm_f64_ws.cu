@@ -309,6 +309,9 @@ __global__ void __launch_bounds__(ws64::THREADS, 1)
         }
         mbar_arrive(&full[ring % STAGES]);
       };
+      // two-term operands: stage kt is combined once its copies have landed,
+      // LAG stages behind the newest issue (LAG groups stay in flight)
+      constexpr int LAG = STAGES > 3 ? STAGES - 2 : 1;
       for (int kt = 0; kt < KT; ++kt, ++kstep) {
         const int s = kstep % STAGES;
         if (kstep >= STAGES) mbar_wait(&empty[s], ((kstep / STAGES) - 1) & 1);
@@ -317,15 +320,15 @@ __global__ void __launch_bounds__(ws64::THREADS, 1)
           mbar_arrive_cpasync(&full[s]);
         } else {
           cp_async_commit();
-          if (kt >= 1) {
-            cp_async_wait<1>();
-            finish(kstep - 1);
+          if (kt >= LAG) {
+            cp_async_wait<LAG>();
+            finish(kstep - LAG);
           }
         }
       }
       if (comb) {
         cp_async_wait<0>();
-        finish(kstep - 1);
+        for (int d = (KT < LAG ? KT : LAG); d >= 1; --d) finish(kstep - d);
       }
     }
     cp_async_wait<0>();
@@ -543,6 +546,10 @@ static cudaError_t launch_ws(Args a, cudaStream_t s) {
   return ws_kernel_launch<BK, NS, NT>(a, total, s);
 }
 
+#ifndef WS2_BK
+#define WS2_BK 16  // k-block rows of the two-term (fused Strassen sum) configurations
+#endif
+
 template <typename Args>
 static cudaError_t launch_ws_any(const Args& a, cudaStream_t s) {
   int ns = 1, nt = 1;
@@ -562,9 +569,9 @@ static cudaError_t launch_ws_any(const Args& a, cudaStream_t s) {
     return launch_ws<16, 2, 2>(a, s);
   }
   if (ns == 1 && nt == 1) return launch_ws<16, 1, 1>(a, s);
-  if (ns == 2 && nt == 1) return launch_ws<16, 2, 1>(a, s);
-  if (ns == 1 && nt == 2) return launch_ws<16, 1, 2>(a, s);
-  return launch_ws<16, 2, 2>(a, s);
+  if (ns == 2 && nt == 1) return launch_ws<WS2_BK, 2, 1>(a, s);
+  if (ns == 1 && nt == 2) return launch_ws<WS2_BK, 1, 2>(a, s);
+  return launch_ws<WS2_BK, 2, 2>(a, s);
 }
 
 cudaError_t launch_batch_f64_ws(const BatchArgs<double>& a, cudaStream_t s) { return launch_ws_any(a, s); }
@@ -678,9 +685,9 @@ cudaError_t launch_batch_f64_global(DProdT<double, kNarrowDests>* prods, int cou
   a.gp = reinterpret_cast<const DProdT<double, kNarrowDests>*>(it->second.dev);
   a.tile_prod = reinterpret_cast<const int*>(reinterpret_cast<const unsigned char*>(it->second.dev) + dbytes);
   if (ns == 1 && nt == 1) return ws_kernel_launch<16, 1, 1>(a, total, s);
-  if (ns == 2 && nt == 1) return ws_kernel_launch<16, 2, 1>(a, total, s);
-  if (ns == 1 && nt == 2) return ws_kernel_launch<16, 1, 2>(a, total, s);
-  return ws_kernel_launch<16, 2, 2>(a, total, s);
+  if (ns == 2 && nt == 1) return ws_kernel_launch<WS2_BK, 2, 1>(a, total, s);
+  if (ns == 1 && nt == 2) return ws_kernel_launch<WS2_BK, 1, 2>(a, total, s);
+  return ws_kernel_launch<WS2_BK, 2, 2>(a, total, s);
 }
 cudaError_t launch_batch_f64_ws_narrow(const BatchArgsNarrow64& a, cudaStream_t s) { return launch_ws_any(a, s); }
 
