@@ -33,6 +33,8 @@
 #include <mutex>
 #include <vector>
 #include <cstring>
+#include <type_traits>
+
 #include "ata_common.cuh"
 
 namespace ata {
@@ -230,6 +232,9 @@ __global__ void __launch_bounds__(ws64::THREADS, 1)
   int* tinfo = reinterpret_cast<int*>(tempty + TSLOTS);  // TSLOTS entries
   int* bcast = tinfo + TSLOTS;                            // producer-internal broadcast
 
+  // producer-side copy of a device-memory tile descriptor (BatchArgsGlobal64)
+  __shared__ __align__(16) unsigned char
+      pdesc_raw[std::is_same<Args, BatchArgsGlobal64>::value ? sizeof(DProdT<double, kNarrowDests>) : 16];
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
 
@@ -264,7 +269,21 @@ __global__ void __launch_bounds__(ws64::THREADS, 1)
       }
       if (tile >= args.total_tiles) break;
       const TileInfo tl = decode_tile(args, tile);
-      typename ProdHold<Args>::type P = prod_of(args, tl.pi);
+      // the producers (40 registers) read their tile's descriptor from the
+      // parameter space, or -- device-memory descriptors -- from a shared copy
+      // made once per tile (a by-value copy would live in local memory)
+      using PD = std::remove_cv_t<std::remove_reference_t<decltype(prod_of(args, 0))>>;
+      const PD* Pp;
+      if constexpr (std::is_same<Args, BatchArgsGlobal64>::value) {
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(args.gp + tl.pi);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(pdesc_raw);
+        for (int i = pt; i < (int)(sizeof(PD) / 4); i += PRODUCERS) dst[i] = __ldg(src + i);
+        named_sync(1, PRODUCERS);
+        Pp = reinterpret_cast<const PD*>(pdesc_raw);
+      } else {
+        Pp = &prod_of(args, tl.pi);
+      }
+      const PD& P = *Pp;
       const bool syrk = P.kind == kSyrk;
       const bool same = syrk && tl.ti == tl.tj;
       const int ns = P.ns, nt = syrk ? 1 : P.nt;
