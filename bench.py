@@ -55,6 +55,10 @@ def parse():
     p.add_argument("--leaf-cols", type=int, default=None)
     p.add_argument("--max-depth", type=int, default=None)
     p.add_argument("--min-dim", type=int, default=None)
+    p.add_argument("--dist", choices=["auto", "rows", "tree"], default="auto",
+                   help="N>1 partition: row shards + NCCL reduce, or the reference's distributed task "
+                        "tree (leaf per rank, blocks retrieved over NCCL); auto = the tree where the "
+                        "reference's own tree is a bunch (fp64 configs, N >= 6), else rows")
     p.add_argument("--fuse-leaf-sums", action="store_true",
                    help="A/B: last Strassen level's operand sums summed in the product loads")
     p.add_argument("--dump-units", default=None, help="write per-launch timings (JSON) here")
@@ -256,7 +260,13 @@ def main():
     np_dt = np.float64 if f64 else np.float32
     precision = "fp32" if f64 else "tf32"
     threshold = cfg["threshold"]
-    r0, r1 = pdist.shard_rows(m, world, rank)
+    from paper_2110_13042_b200.tasktree import build_tree_distributed, leaf_task
+    tree = None
+    if world > 1:
+        t_ref = build_tree_distributed(world, m, n)
+        if args.dist == "tree" or (args.dist == "auto" and f64 and t_ref.root.bunch):
+            tree = t_ref
+    r0, r1 = pdist.tree_rows(tree, rank) if tree is not None else pdist.shard_rows(m, world, rank)
     # ---- inputs: seeded host draw of this rank's rows, then H2D ----
     t_gen = time.perf_counter()
     if cfg["dist"] == "uniform":
@@ -273,7 +283,29 @@ def main():
                                                         ("fuse_leaf_sums", args.fuse_leaf_sums or None))
                                                      if v is not None})
     mloc = r1 - r0
-    if threshold == "auto":
+    # what this rank's plan computes: the whole row shard into C, or (task
+    # tree) its leaf -- an AtA of a column block or an AtB of two -- into a
+    # private block that run_tree_process then retrieves up the tree
+    leaf = leaf_task(tree, rank) if tree is not None else None
+    A_ptr, B_ptr, C_out = int(A.data_ptr()), None, C
+    a_elems = A.numel()
+    if leaf is not None:
+        ar, br, cr = leaf.a_region, leaf.b_region, leaf.c_region
+        C_out = torch.zeros((cr.rows, cr.cols), dtype=A.dtype, device=dev)
+        A_ptr = int(A.data_ptr()) + ar.col_offset * A.element_size()
+        a_elems = A.numel() - ar.col_offset
+        if br is not None:
+            B_ptr = int(A.data_ptr()) + br.col_offset * A.element_size()
+        if threshold == "auto":
+            plan = auto_plan.plan_ata_auto(mloc, ar.cols, n, cr.cols, params, round_tf32=not f64) \
+                if br is None else auto_plan.plan_gemm_auto(mloc, ar.cols, br.cols, n, n, cr.cols, params)
+        elif br is None:
+            plan = ref_bfs.plan_ata_reference_bfs(mloc, ar.cols, n, cr.cols, threshold)
+        else:
+            plan = ref_bfs.plan_strassen_reference_bfs(mloc, ar.cols, br.cols, n, n, cr.cols, threshold)
+        wsbuf = torch.empty(max(1, plan.ws_scalars), dtype=A.dtype, device=dev) \
+            if plan.ws_scalars else None
+    elif threshold == "auto":
         plan = auto_plan.plan_ata_auto(mloc, n, n, n, params, round_tf32=not f64)
         wsbuf = torch.empty(max(1, plan.ws_scalars), dtype=A.dtype, device=dev) \
             if plan.ws_scalars else None
@@ -287,7 +319,9 @@ def main():
             wsbuf = ws.ensure(dev, extra=plan.ws_scalars)
     units, n_launch = launch_units(plan)
     code = nat.dtype_code(A.dtype, precision)
-    a_elems, c_elems = A.numel(), C.numel()
+    c_elems = C_out.numel()
+    b_kw = dict(B=B_ptr, b_elems=a_elems - (B_ptr - A_ptr) // A.element_size()) if B_ptr is not None else {}
+    link = pdist.tree_link() if tree is not None else None
     wptr = int(wsbuf.data_ptr()) if wsbuf is not None else 0
     wel = int(wsbuf.numel()) if wsbuf is not None else 0
     stream = torch.cuda.current_stream()
@@ -301,14 +335,21 @@ def main():
 
     def step(events=None):
         C.zero_()
+        if C_out is not C:
+            C_out.zero_()
         for u, sp in enumerate(sub):
             if events is not None:
                 events[u][0].record(stream)
-            engine.run_plan(sp, code, int(A.data_ptr()), a_elems, int(C.data_ptr()), c_elems, 1.0,
-                            ws=wptr, ws_elems=wel, stream=sptr)
+            engine.run_plan(sp, code, A_ptr, a_elems, int(C_out.data_ptr()), c_elems, 1.0,
+                            ws=wptr, ws_elems=wel, stream=sptr, **b_kw)
             if events is not None:
                 events[u][1].record(stream)
-        if world > 1:
+        if tree is not None:     # retrieve the leaf blocks up the reference's task tree (NCCL p2p)
+            top = pdist.run_tree_process(tree, rank, None, link, dtype=A.dtype, device=dev,
+                                         leaf_block=C_out)
+            if rank == 0:
+                pdist.add_lower_into(C, top)
+        elif world > 1:
             P.pack_lower(C, out=packed)
             pdist.reduce_packed(packed, 0)
             if rank == 0:
@@ -333,7 +374,7 @@ def main():
     # per-launch roofline events come from one extra eager step afterwards.
     graph = None
     if threshold != "auto" and world == 1 and not args.no_graph:
-        graph = engine.PlanGraph(plan, code, int(A.data_ptr()), a_elems, int(C.data_ptr()), c_elems,
+        graph = engine.PlanGraph(plan, code, A_ptr, a_elems, int(C_out.data_ptr()), c_elems,
                                  1.0, ws=wptr, ws_elems=wel)
         for _ in range(2):
             C.zero_()
@@ -420,11 +461,17 @@ def main():
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64" if f64 else "f32 (tf32 products)", "data": "synthetic",
             "config": {"workload": workload_name(args.config),
-                       "parallelism": f"row-shard x{world}" if world > 1 else "single GPU",
+                       "parallelism": (f"task-tree x{world} (reference build_tree_distributed; rank 0 "
+                                       f"leaf {leaf.computation.value} A{leaf.a_region})" if tree is not None
+                                       else f"row-shard x{world}" if world > 1 else "single GPU"),
                        "l2": "inputs larger than L2 (A is %.1f GB)" % (A.numel() * A.element_size() / 1e9),
                        "plan": {"kind": plan.kind, "ops": len(plan.ops), "launches": n_launch,
                                 "executed_mults": plan.mults,
-                                "mults_over_classical": plan.mults / (mloc * n * (n + 1) / 2)},
+                                "mults_over_classical": plan.mults / (
+                                    mloc * n * (n + 1) / 2 if leaf is None else
+                                    mloc * leaf.a_region.cols * (leaf.a_region.cols + 1) / 2
+                                    if leaf.b_region is None else
+                                    mloc * leaf.a_region.cols * leaf.b_region.cols)},
                        "effective_pct_of_peak": value / 1e3 / peak},
             "roofline": roofline,
             "clocks": clk.summary,

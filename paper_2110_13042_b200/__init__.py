@@ -8,7 +8,11 @@ Drop-in surface (reference pkg/src/atamul/__init__.py:9-27, hot path only):
 ``naive_syrk_lower``, ``add_truncated``, ``mirror_lower_to_upper``,
 ``pack_lower``/``unpack_lower``/``PackedLowerTriangular``, ``split4``,
 ``DenseMatrix``/``MatrixView``, ``MultCounter``, ``effective_gflops``,
-``gen_matrix``, the exception classes, and the multi-GPU entry ``ata_dist``.
+``gen_matrix``, the exception classes, the multi-GPU entries ``dist.ata_dist``
+(row shards) and ``dist.ata_tree`` (the reference's distributed task tree),
+and the formats/callers either side of the path: ATAM ``read_matrix`` /
+``write_matrix``, the task trees (``build_tree_*``, ``render_tree``) and the
+``atamul`` command line (``python -m paper_2110_13042_b200.cli``).
 """
 from .ata import AUTO, ata, ata_full, ata_mult_count, workspace_for_ata
 from .errors import (AtamulError, InvalidMeasurementError, NativeError, ProtocolError,
@@ -16,9 +20,12 @@ from .errors import (AtamulError, InvalidMeasurementError, NativeError, Protocol
                      UnsplittableError, UnsupportedSizeError, WorkspaceUndersizedError)
 from .matrix import (DenseMatrix, MatrixView, MultCounter, PackedLowerTriangular, add_truncated,
                      count_allocations, mirror_lower_to_upper, naive_gemm_atb, naive_syrk_lower,
-                     pack_lower, split4, unpack_lower)
+                     pack_lower, read_matrix, split4, unpack_lower, write_matrix)
 from .measure import check_tolerance, effective_gflops, gen_matrix
 from .strassen import fast_strassen, strassen_mult_count, workspace_for
+from .tasktree import (ComputationType, Region, Task, TaskTree, build_tree_distributed,
+                       build_tree_shared, leaf_task, levels_distributed, levels_shared, path_to_root,
+                       render_tree)
 from .workspace import DEFAULT_THRESHOLD, StrassenWorkspace
 
 __version__ = "0.1.0"
@@ -32,4 +39,8 @@ __all__ = [
     "effective_gflops", "fast_strassen", "gen_matrix", "mirror_lower_to_upper",
     "naive_gemm_atb", "naive_syrk_lower", "pack_lower", "split4", "strassen_mult_count",
     "unpack_lower", "workspace_for", "workspace_for_ata",
+    # callers / formats either side of the path
+    "ComputationType", "Region", "Task", "TaskTree", "build_tree_distributed",
+    "build_tree_shared", "leaf_task", "levels_distributed", "levels_shared", "path_to_root",
+    "read_matrix", "render_tree", "write_matrix",
 ]

@@ -430,3 +430,22 @@ def plan_ata_auto(m: int, n: int, lda: int, ldc: int, params: AutoParams = AutoP
     plan = ap.pb.finish()
     plan.ws_scalars = max(plan.ws_scalars, ap.ws_peak)
     return plan
+
+
+def plan_gemm_auto(m: int, n: int, k: int, lda: int, ldb: int, ldc: int,
+                   params: AutoParams = AutoParams()) -> Plan:
+    """GPU plan for C (n x k) += alpha A^T B (fast_strassen with threshold
+    "auto"; the A^T B leaves of the multi-GPU task tree): one Strassen tree
+    chosen by the same cost model as the C21 blocks of plan_ata_auto, breadth
+    first when its workspace fits the budget."""
+    if min(m, n, k) < 1:
+        raise ShapeMismatchError("shape mismatch: empty operand")
+    ap = _AutoPlanner(params)
+    ap.budget = int(params.ws_budget_gb * 1e9 / 8)
+    A = Win(nat.BASE_A, 0, lda, m, n)
+    B = Win(nat.BASE_B, 0, ldb, m, k)
+    C = Win(nat.BASE_C, 0, ldc, n, k)
+    ap.node(A, B, m, n, k, C, 1.0, True, params.max_depth)
+    plan = ap.pb.finish()
+    plan.ws_scalars = max(plan.ws_scalars, ap.ws_peak)
+    return plan

@@ -71,3 +71,211 @@ def ata_dist(A_shard, C, alpha=1.0, threshold="auto", root: int = 0, packed=None
     if rank == root:
         unpack_lower(PackedLowerTriangular(n, packed), C)
     return C
+
+
+# --------------------------------------------------------------------------
+# Task-tree partition (the reference's distribute-compute-retrieve layout)
+#
+# tasktree.build_tree_distributed(P, m, n) assigns one leaf task to every
+# process: an AtA of an operand block into a diagonal C block, or an AtB of
+# two operand blocks into a rectangular C block (scheduler.py:283-363; at
+# P = 8 on c4: four quadrant AtA's and four AtB tiles of C21).  Each rank
+# computes its leaf with the single-GPU plans (ata / fast_strassen), then the
+# results travel up the tree as in the reference's retrieve phase
+# (distsim.py:253-267): every process walks its ownership chain
+# (path_to_root) leaf first, assembling each owned node's C block from its own
+# child's block plus the blocks the other children's owners send it, and
+# finally sends its chain top to the parent's owner.  AtA blocks travel as
+# packed lower triangles (distsim.py:192-199), AtB blocks as rectangles.
+# Over NCCL these are point-to-point sends; the tree has one message per
+# non-root process and no cycles, so the blocking order cannot deadlock.
+
+def _block_words(task) -> int:
+    c = task.c_region
+    if task.b_region is None:           # lower triangle of a diagonal block
+        return c.rows * (c.rows + 1) // 2
+    return c.rows * c.cols
+
+
+def tree_comm_stats(tree):
+    """Retrieve-phase traffic of the tree (words and messages per process):
+    the CommStats counters of distsim.py:72-111 restricted to result blocks."""
+    from .tasktree import path_to_root
+    P = tree.procs
+    st = {k: [0] * P for k in ("sent_messages", "sent_words", "recv_messages", "recv_words")}
+    for q in range(1, P):
+        top = path_to_root(tree, q)[-1]
+        dst = tree.nodes[top.parent_id].task.owner
+        w = _block_words(top.task)
+        st["sent_messages"][q] += 1
+        st["sent_words"][q] += w
+        st["recv_messages"][dst] += 1
+        st["recv_words"][dst] += w
+    return st
+
+
+def write_comm_csv(path, stats, procs: int) -> None:
+    """The reference's --comm-csv layout (distsim.py:101-111)."""
+    import csv
+    with open(path, "w", newline="") as fh:
+        w = csv.writer(fh)
+        w.writerow(["process", "sent_messages", "sent_words", "recv_messages", "recv_words"])
+        for p in range(procs):
+            w.writerow([p, stats["sent_messages"][p], stats["sent_words"][p],
+                        stats["recv_messages"][p], stats["recv_words"][p]])
+        w.writerow(["critical_path", stats["sent_messages"][0], stats["sent_words"][0],
+                    stats["recv_messages"][0], stats["recv_words"][0]])
+
+
+class _LocalLink:
+    """In-process transport: all processes of the tree run on this GPU in
+    decreasing label order (a non-first child's owner always has a larger
+    label than its parent's), so every block is produced before it is read."""
+
+    def __init__(self):
+        self.box = {}
+
+    def send(self, block, src: int, dst: int, node) -> None:
+        self.box[(src, dst, node.id)] = block
+
+    def recv(self, shape_like, src: int, dst: int, node):
+        return self.box.pop((src, dst, node.id))
+
+
+class _DistLink:
+    """torch.distributed point-to-point (NCCL; gloo stages through the host)."""
+
+    def __init__(self, group=None):
+        import torch.distributed as dist
+        self.dist, self.group = dist, group
+        self.gloo = dist.get_backend(group) == "gloo"
+
+    def _peer(self, r):
+        return r if self.group is None else self.dist.get_global_rank(self.group, r)
+
+    def send(self, block, src: int, dst: int, node) -> None:
+        t = block.cpu() if (self.gloo and block.is_cuda) else block
+        self.dist.send(t.contiguous(), dst=self._peer(dst), group=self.group)
+
+    def recv(self, shape_like, src: int, dst: int, node):
+        import torch
+        buf = torch.empty(shape_like[0], dtype=shape_like[1], device="cpu" if self.gloo else shape_like[2])
+        self.dist.recv(buf, src=self._peer(src), group=self.group)
+        return buf.to(shape_like[2]) if self.gloo else buf
+
+
+def _leaf_block(task, get_block, alpha, threshold, dtype, device, counter, precision):
+    """This process's leaf: a fresh C block (zeros) += alpha * leaf product."""
+    import torch
+    from .ata import ata
+    from .strassen import fast_strassen
+    c = task.c_region
+    out = torch.zeros((c.rows, c.cols), dtype=dtype, device=device)
+    a = get_block(task.a_region)
+    if task.b_region is None:
+        ata(a, out, alpha, threshold, counter=counter, precision=precision)
+    else:
+        fast_strassen(a, get_block(task.b_region), out, alpha, threshold=threshold, counter=counter)
+    return out
+
+
+def _wire(task, block):
+    """Block as sent: packed lower triangle for AtA, rectangle for AtB."""
+    if task.b_region is None:
+        from .matrix import pack_lower
+        return pack_lower(block).data
+    return block
+
+
+def _unwire(task, wire, dtype, device):
+    import torch
+    c = task.c_region
+    if task.b_region is None:
+        from .matrix import PackedLowerTriangular, unpack_lower
+        out = torch.zeros((c.rows, c.rows), dtype=dtype, device=device)
+        unpack_lower(PackedLowerTriangular(c.rows, wire), out)
+        return out
+    return wire.view(c.rows, c.cols)
+
+
+def run_tree_process(tree, p: int, get_block, link, alpha=1.0, threshold="auto", dtype=None,
+                     device=None, counter=None, precision: str = "fp32", leaf_block=None):
+    """Process p's part of the tree: its leaf (or the caller's `leaf_block`,
+    already computed), then every node it owns (assembling children's
+    blocks), then the send of its chain top.  Returns the chain top's C block
+    (the whole n x n result on process 0)."""
+    from .tasktree import path_to_root
+    chain = path_to_root(tree, p)
+    block = leaf_block if leaf_block is not None else \
+        _leaf_block(chain[0].task, get_block, alpha, threshold, dtype, device, counter, precision)
+    for prev, node in zip(chain, chain[1:]):
+        import torch
+        c = node.task.c_region
+        out = torch.zeros((c.rows, c.cols), dtype=dtype, device=device)
+        for child in tree.children_of(node):
+            if child.id == prev.id:
+                blk = block
+            else:
+                q = child.task.owner
+                wire = link.recv((_block_words(child.task), dtype, device), q, p, child)
+                blk = _unwire(child.task, wire, dtype, device)
+            cc = child.task.c_region
+            r0, c0 = cc.row_offset - c.row_offset, cc.col_offset - c.col_offset
+            out[r0:r0 + cc.rows, c0:c0 + cc.cols] += blk
+        block = out
+    top = chain[-1]
+    if top.parent_id is not None:
+        link.send(_wire(top.task, block), p, tree.nodes[top.parent_id].task.owner, top)
+    return block
+
+
+def add_lower_into(C, block):
+    """lower(C) += lower(block) (C's strict upper triangle untouched)."""
+    import torch
+    n = int(C.shape[0])
+    il = torch.tril_indices(n, n, device=block.device)
+    C[il[0], il[1]] += block[il[0], il[1]]
+
+
+def tree_link(group=None):
+    """The torch.distributed transport of run_tree_process."""
+    return _DistLink(group)
+
+
+def ata_tree(get_block, m: int, n: int, C, alpha=1.0, threshold="auto", procs: int | None = None,
+             group=None, counter=None, precision: str = "fp32"):
+    """lower(C) += alpha * A^T A over the reference's distributed task tree.
+
+    With a torch.distributed group of P > 1 ranks, every rank runs its own
+    leaf and chain (get_block only needs to serve that rank's regions) and
+    rank 0's C receives the result.  Without one, ``procs`` processes are
+    simulated on this GPU one after another (the reference's in-process
+    distributed executor, ata_d).  get_block(Region) -> CUDA tensor view."""
+    from .tasktree import build_tree_distributed
+    import torch.distributed as dist
+    dtype, device = C.dtype, C.device
+    if procs is None and dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        P, rank = dist.get_world_size(group), dist.get_rank(group)
+        tree = build_tree_distributed(P, m, n)
+        top = run_tree_process(tree, rank, get_block, _DistLink(group), alpha, threshold, dtype, device,
+                               counter, precision)
+        if rank == 0:
+            add_lower_into(C, top)
+        return tree
+    P = procs or 1
+    tree = build_tree_distributed(P, m, n)
+    link = _LocalLink()
+    top = None
+    for p in reversed(range(P)):
+        top = run_tree_process(tree, p, get_block, link, alpha, threshold, dtype, device, counter,
+                               precision)
+    add_lower_into(C, top)
+    return tree
+
+
+def tree_rows(tree, rank: int):
+    """Row range [r0, r1) of A that `rank`'s leaf reads (its a and b regions
+    share their rows) -- what a rank must generate or receive."""
+    from .tasktree import leaf_task
+    t = leaf_task(tree, rank)
+    return t.a_region.row_offset, t.a_region.row_offset + t.a_region.rows

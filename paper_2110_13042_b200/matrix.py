@@ -10,6 +10,7 @@ Nothing is ever computed on the CPU.
 from __future__ import annotations
 
 import contextlib
+import struct
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -427,3 +428,51 @@ def mirror_lower_to_upper(C) -> None:
     C_ = DeviceOperand(c, writable=True)
     nat.check(nat.load().ata_mirror_lower(_dtcode(C_.t), C_.ptr, C_.ld, n, _stream_ptr()))
     C_.commit()
+
+
+# ------------------------------------------------------------ ATAM files
+# The reference's binary matrix format (matrix.py:383-417): magic b"ATAM",
+# three little-endian uint64 (rows, cols, scalar width 4 or 8), then the
+# row-major little-endian scalars.  Device tensors are staged through the host.
+
+_ATAM = b"ATAM"
+_ATAM_HEAD = struct.Struct("<4sQQQ")
+
+
+def write_matrix(path, M) -> None:
+    """Write an f32/f64 matrix (numpy, torch host or device, DenseMatrix,
+    MatrixView) as an ATAM file; other dtypes are ShapeMismatchError, as in
+    the reference (matrix.py:392-402)."""
+    a = as_array(M)
+    torch = _torch()
+    if isinstance(a, torch.Tensor):
+        a = a.detach().cpu().numpy()
+    width = a.dtype.itemsize if a.dtype.type in (np.float32, np.float64) else 0
+    if width not in (4, 8):
+        raise ShapeMismatchError("shape mismatch: only f32/f64 matrices supported")
+    data = np.ascontiguousarray(a, dtype="<f4" if width == 4 else "<f8")
+    with open(path, "wb") as fh:
+        fh.write(_ATAM_HEAD.pack(_ATAM, data.shape[0], data.shape[1], width))
+        fh.write(data.tobytes())
+
+
+def read_matrix(path, device=None) -> DenseMatrix:
+    """Read an ATAM file into a DenseMatrix (host numpy, or a torch tensor on
+    `device`).  Bad magic / scalar width -> ValueError (matrix.py:405-417)."""
+    with open(path, "rb") as fh:
+        head = fh.read(_ATAM_HEAD.size)
+        if len(head) < 4 or head[:4] != _ATAM:
+            raise ValueError(f"not an ATAM file: bad magic {head[:4]!r}")
+        if len(head) < _ATAM_HEAD.size:
+            raise ValueError("truncated ATAM header")
+        _, rows, cols, width = _ATAM_HEAD.unpack(head)
+        if width not in (4, 8):
+            raise ValueError(f"bad ATAM scalar width {width}")
+        payload = fh.read(rows * cols * width)
+    if len(payload) != rows * cols * width:
+        raise ValueError("truncated ATAM payload")
+    data = np.frombuffer(payload, dtype="<f4" if width == 4 else "<f8").reshape(rows, cols)
+    data = data.astype(np.float32 if width == 4 else np.float64)
+    if device is None:
+        return DenseMatrix(data)
+    return DenseMatrix(_torch().from_numpy(data).to(device))

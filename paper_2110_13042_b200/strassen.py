@@ -27,8 +27,11 @@ def workspace_for(m: int, n: int, k: int, threshold: int = DEFAULT_THRESHOLD,
 
 
 def fast_strassen(A, B, C, alpha=1.0, ws: StrassenWorkspace | None = None,
-                  threshold: int = DEFAULT_THRESHOLD, counter: MultCounter | None = None) -> None:
-    """C += alpha * A^T B with A (m x n), B (m x k), C (n x k)."""
+                  threshold: int = DEFAULT_THRESHOLD, counter: MultCounter | None = None, *,
+                  auto_params=None) -> None:
+    """C += alpha * A^T B with A (m x n), B (m x k), C (n x k).  threshold
+    "auto": the GPU plan (auto_plan.plan_gemm_auto) instead of the reference
+    recursion."""
     a, b, c = as_array(A), as_array(B), as_array(C)
     m, n = int(a.shape[0]), int(a.shape[1])
     if b.shape[0] != m:
@@ -36,10 +39,13 @@ def fast_strassen(A, B, C, alpha=1.0, ws: StrassenWorkspace | None = None,
     k = int(b.shape[1])
     if tuple(c.shape) != (n, k):
         raise ShapeMismatchError(f"shape mismatch: C {tuple(c.shape)} != {(n, k)}")
-    threshold = int(threshold)
     C_ = DeviceOperand(c, writable=True)
     A_ = DeviceOperand(a, dtype=C_.t.dtype, device=C_.t.device)
     B_ = DeviceOperand(b, dtype=C_.t.dtype, device=C_.t.device)
+    if threshold == "auto":
+        _fast_strassen_auto(A_, B_, C_, m, n, k, alpha, counter, auto_params, ws)
+        return
+    threshold = int(threshold)
     if ws is None:
         ws = workspace_for(m, n, k, threshold, dtype=C_.t.dtype)
     elif not ws.covers(m, n, k, threshold):
@@ -67,6 +73,33 @@ def fast_strassen(A, B, C, alpha=1.0, ws: StrassenWorkspace | None = None,
     C_.commit()
     if counter is not None:
         counter.add(plan.mults)
+
+
+def _fast_strassen_auto(A_, B_, C_, m, n, k, alpha, counter, auto_params, ws=None):
+    """threshold="auto": the GPU plan; scratch from `ws` (a StrassenWorkspace,
+    e.g. one per concurrent stream) or a per-(device, dtype) arena."""
+    from . import auto_plan
+    params = auto_params or auto_plan.AutoParams()
+    key = ("gemm-auto", m, n, k, A_.ld, B_.ld, C_.ld, params)
+    plan = engine.cached_plan(key, lambda: auto_plan.plan_gemm_auto(m, n, k, A_.ld, B_.ld, C_.ld, params))
+    wbuf = None
+    if plan.ws_scalars > 0 and ws is not None:
+        wbuf = ws.ensure(C_.t.device, extra=plan.ws_scalars)
+    elif plan.ws_scalars > 0:
+        wbuf = _AUTO_WS.get((str(C_.t.device), str(C_.t.dtype)))
+        if wbuf is None or wbuf.numel() < plan.ws_scalars:
+            import torch
+            wbuf = torch.empty(plan.ws_scalars, dtype=C_.t.dtype, device=C_.t.device)
+            _AUTO_WS[(str(C_.t.device), str(C_.t.dtype))] = wbuf
+    engine.run_plan(plan, nat.dtype_code(C_.t.dtype), A_.ptr, A_.elems, C_.ptr, C_.elems, alpha,
+                    ws=int(wbuf.data_ptr()) if wbuf is not None else 0,
+                    ws_elems=int(wbuf.numel()) if wbuf is not None else 0, B=B_.ptr, b_elems=B_.elems)
+    C_.commit()
+    if counter is not None:
+        counter.add(plan.mults)
+
+
+_AUTO_WS: dict = {}   # scratch of auto GEMM plans, one per (device, dtype), grown on demand
 
 
 def strassen_mult_count(n: int) -> int:
