@@ -89,6 +89,45 @@ __global__ void combo4_kernel(const __grid_constant__ EwArgs<T> a) {
   }
 }
 
+// Two adjacent elements (c0 even) with one 16-byte (f64) / 8-byte (f32) access
+// when the window allows it: base aligned to two elements and an even pitch.
+template <typename T> struct Pair;
+template <> struct Pair<double> { using V = double2; };
+template <> struct Pair<float> { using V = float2; };
+template <typename T>
+__device__ __forceinline__ bool pair_ok(const T* p, long long ld) {
+  return ((reinterpret_cast<uintptr_t>(p) & (2 * sizeof(T) - 1)) == 0) && ((ld & 1) == 0);
+}
+template <typename T>
+__device__ __forceinline__ void load_pair(const T* q, int avail, bool vec, T& x, T& y) {
+  if (vec && avail >= 2) {
+    const typename Pair<T>::V v = __ldcs(reinterpret_cast<const typename Pair<T>::V*>(q));
+    x = v.x;
+    y = v.y;
+  } else {
+    x = avail > 0 ? __ldcs(q) : T(0);
+    y = avail > 1 ? __ldcs(q + 1) : T(0);
+  }
+}
+template <typename T>
+__device__ __forceinline__ void store_pair(T* q, int avail, bool vec, T x, T y, bool accumulate) {
+  if (vec && avail >= 2) {
+    typename Pair<T>::V* pv = reinterpret_cast<typename Pair<T>::V*>(q);
+    if (accumulate) {
+      const typename Pair<T>::V o = *pv;
+      x += o.x;
+      y += o.y;
+    }
+    typename Pair<T>::V v;
+    v.x = x;
+    v.y = y;
+    *pv = v;
+  } else {
+    if (avail > 0) q[0] = accumulate ? q[0] + x : x;
+    if (avail > 1) q[1] = accumulate ? q[1] + y : y;
+  }
+}
+
 // postadd7: the 4 output quadrants of one Strassen node from its 7 children
 // (one read of each child, one write (or RMW) of each output quadrant).
 template <typename T>
@@ -99,13 +138,10 @@ __global__ void postadd7_kernel(const __grid_constant__ EwArgs<T> a, int accumul
     T p[7][2];
 #pragma unroll
     for (int i = 0; i < 7; ++i) {
-      p[i][0] = p[i][1] = T(0);
       const DTerm<T>& S = a.src[i];
-      if (r < S.rows) {
-        const T* q = S.p + (long long)r * S.ld + c0;
-        if (c0 < S.cols) p[i][0] = __ldcs(q);
-        if (c0 + 1 < S.cols) p[i][1] = __ldcs(q + 1);
-      }
+      const bool ok = r < S.rows;
+      load_pair(S.p + (ok ? (long long)r * S.ld + c0 : 0), ok ? S.cols - c0 : 0, pair_ok(S.p, S.ld),
+                p[i][0], p[i][1]);
     }
     T o[4][2];
 #pragma unroll
@@ -119,15 +155,9 @@ __global__ void postadd7_kernel(const __grid_constant__ EwArgs<T> a, int accumul
     for (int j = 0; j < 4; ++j) {
       const DDest<T>& D = a.dst[j];
       if (r >= D.rows) continue;
-      T* q = D.p + (long long)r * D.ld + c0;
       const T sg = T(D.sign);
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        if (c0 + e < D.cols) {
-          const T v = sg * o[j][e];
-          q[e] = accumulate ? q[e] + v : v;
-        }
-      }
+      store_pair(D.p + (long long)r * D.ld + c0, D.cols - c0, pair_ok(D.p, D.ld), sg * o[j][0], sg * o[j][1],
+                 accumulate != 0);
     }
   }
 }
