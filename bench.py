@@ -55,6 +55,8 @@ def parse():
     p.add_argument("--leaf-cols", type=int, default=None)
     p.add_argument("--max-depth", type=int, default=None)
     p.add_argument("--min-dim", type=int, default=None)
+    p.add_argument("--gain", type=float, default=None,
+                   help="auto plan: split a Strassen node when saved time > gain x added time")
     p.add_argument("--dist", choices=["auto", "rows", "tree"], default="auto",
                    help="N>1 partition: row shards + NCCL reduce, or the reference's distributed task "
                         "tree (leaf per rank, blocks retrieved over NCCL); auto = the tree where the "
@@ -280,6 +282,7 @@ def main():
     params = auto_plan.AutoParams(**{k: v for k, v in (("leaf_cols", args.leaf_cols),
                                                         ("max_depth", args.max_depth),
                                                         ("min_dim", args.min_dim),
+                                                        ("gain", args.gain),
                                                         ("fuse_leaf_sums", args.fuse_leaf_sums or None))
                                                      if v is not None})
     mloc = r1 - r0
