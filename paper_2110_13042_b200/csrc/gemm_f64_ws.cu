@@ -39,11 +39,16 @@
 
 namespace ata {
 
+#ifndef WS_CW
+#define WS_CW 8  // consumer warps: 8 (2 x 4 grid of 64 x 32 warp tiles) or 16 (4 x 4 of 32 x 32)
+#endif
 namespace ws64 {
 constexpr int BM = 128, BN = 128, LD = BM + 4;
-constexpr int CONSUMERS = 8, PRODUCERS = 128, THREADS = CONSUMERS * 32 + PRODUCERS;
-constexpr int PRODUCER_REGS = 40, CONSUMER_REGS = 232;  // 128*40 + 256*232 = 384*168 (the launch allocation)
-constexpr int WTM = 8, WTN = 4;  // 64 x 32 per consumer warp
+constexpr int CONSUMERS = WS_CW, PRODUCERS = 128, THREADS = CONSUMERS * 32 + PRODUCERS;
+// setmaxnreg split of the launch allocation: 8 warps 128*40 + 256*232 = 384*168;
+// 16 warps 128*40 + 512*104 <= 640*96
+constexpr int PRODUCER_REGS = 40, CONSUMER_REGS = CONSUMERS == 8 ? 232 : 104;
+constexpr int WTM = CONSUMERS == 8 ? 8 : 4, WTN = 4;  // 64 x 32 or 32 x 32 per consumer warp
 constexpr int SMEM_BUDGET = 225 * 1024;
 constexpr int TSLOTS = 2;        // tile-info ring
 }  // namespace ws64
