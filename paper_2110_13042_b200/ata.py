@@ -110,7 +110,13 @@ def _default_workspace(m, n, threshold, dtype):
 
 
 PIPELINE_MIN_BYTES = 1 << 30      # host A at least this large: copy/compute pipeline
-PIPELINE_BLOCK_BYTES = 4 << 30    # ~ bytes of A per row block
+PIPELINE_BLOCK_BYTES = 4 << 30    # ~ bytes of A per row block (PCIe-bound TF32 plans)
+PIPELINE_GEOMETRIC = True         # compute-bound plans: geometric row blocks (_row_blocks)
+PIPELINE_GEOMETRIC_BLOCKS = 3     # measured (tools/e2e_ab.py): c4 e2e 1718 -> 1683 ms at 3 blocks,
+                                  # 4-5 blocks no gain (each block repeats the plan's C-sized work)
+PIPELINE_PCIE_GBS = 50.0          # measured pinned H2D on the box (e2e h2d bytes / time)
+PIPELINE_FP64_TFLOPS = 40.0       # effective AtA rate of the fp64 auto plans (bench c3/c4)
+PIPELINE_TF32_TFLOPS = 460.0
 
 
 def _first_c_writer(ops) -> int:
@@ -211,8 +217,6 @@ def _pipelined_host_ata(a, c, m, n, alpha, ws, counter, auto_params, precision) 
     es = a.element_size()
     if m * n * es < PIPELINE_MIN_BYTES or m < 2:
         return False
-    R = max(2, min(8, -(-m * n * es // PIPELINE_BLOCK_BYTES)))
-    rb = -(-m // R)
     dev = torch.device("cuda", torch.cuda.current_device())
     main = torch.cuda.current_stream(dev)
     copy = _copy_stream(dev)
@@ -222,8 +226,7 @@ def _pipelined_host_ata(a, c, m, n, alpha, ws, counter, auto_params, precision) 
     round_tf32 = precision == "tf32" and c.dtype == torch.float32
     params = auto_params or auto_plan.AutoParams()
     blocks = []
-    for r0 in range(0, m, rb):
-        rows = min(rb, m - r0)
+    for (r0, rows) in _row_blocks(m, n, es, round_tf32 or es == 4):
         key = ("ata-auto", rows, n, n, n, params, round_tf32)
         blocks.append((r0, rows, engine.cached_plan(
             key, lambda rows=rows: auto_plan.plan_ata_auto(rows, n, n, n, params, round_tf32=round_tf32))))
@@ -283,6 +286,31 @@ def _pipelined_host_ata(a, c, m, n, alpha, ws, counter, auto_params, precision) 
     if counter is not None:
         counter.add(mults)
     return True
+
+
+def _row_blocks(m: int, n: int, es: int, tensor_rate: bool):
+    """Row blocks of the host pipeline.  Each block after the first must cross
+    PCIe while the GPU computes the previous one, and every block repeats the
+    C-sized work of a plan (post-additions, C updates), so: when the per-row
+    compute time exceeds the per-row upload time by `ratio` (fp64: ~n / 6400),
+    use PIPELINE_GEOMETRIC_BLOCKS blocks growing by g = min(4, 0.75 ratio) -- a
+    small first block (short exposed upload), few blocks in total -- when
+    ratio >= 4 (c4; at c3's 2.6 two equal blocks measured better).  Otherwise
+    (TF32: PCIe bound) up to 8 equal blocks of ~PIPELINE_BLOCK_BYTES."""
+    rate = (PIPELINE_TF32_TFLOPS if tensor_rate else PIPELINE_FP64_TFLOPS) * 1e12
+    ratio = n * PIPELINE_PCIE_GBS * 1e9 / (rate * es)
+    if PIPELINE_GEOMETRIC and ratio >= 4.0:
+        g = min(4.0, 0.75 * ratio)
+        R = PIPELINE_GEOMETRIC_BLOCKS
+        w = [g ** i for i in range(R)]
+        cuts = [0]
+        for i in range(R - 1):
+            cuts.append(max(cuts[-1] + 1, int(round(m * sum(w[:i + 1]) / sum(w)))))
+        cuts = [c for c in cuts if c < m] + [m]
+        return [(a, b - a) for a, b in zip(cuts, cuts[1:])]
+    R = max(2, min(8, -(-m * n * es // PIPELINE_BLOCK_BYTES)))
+    rb = -(-m // R)
+    return [(r0, min(rb, m - r0)) for r0 in range(0, m, rb)]
 
 
 _COPY_STREAMS = {}
