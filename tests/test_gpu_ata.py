@@ -136,8 +136,9 @@ def test_config_c2_full_parity():
     assert O.rel_frobenius_lower(c, O.gram_blas(a)) <= 1e-10
 
 
-@pytest.mark.parametrize("dtype,precision", [("f64", "fp32"), ("f32", "tf32")])
-def test_pipelined_host_ata(monkeypatch, dtype, precision):
+@pytest.mark.parametrize("dtype,precision,geometric", [("f64", "fp32", False), ("f32", "tf32", False),
+                                                       ("f64", "fp32", True)])
+def test_pipelined_host_ata(monkeypatch, dtype, precision, geometric):
     """Pinned host A and C: A crosses PCIe in row blocks on a copy stream while
     the GPU runs the blocks already resident (ata._pipelined_host_ata).  Same
     result as the device path within the dtype tolerance, upper triangle of C
@@ -148,6 +149,9 @@ def test_pipelined_host_ata(monkeypatch, dtype, precision):
     ata_mod = importlib.import_module("paper_2110_13042_b200.ata")
     monkeypatch.setattr(ata_mod, "PIPELINE_MIN_BYTES", 1 << 20)
     monkeypatch.setattr(ata_mod, "PIPELINE_BLOCK_BYTES", 3 << 20)
+    if geometric:   # compute-bound regime: 3 geometric row blocks (ata._row_blocks)
+        monkeypatch.setattr(ata_mod, "PIPELINE_FP64_TFLOPS", 0.05)
+        assert len(ata_mod._row_blocks(20011, 300, 8, False)) == 3
     tdt = torch.float64 if dtype == "f64" else torch.float32
     rng = np.random.default_rng(21)
     a = rng.standard_normal((20011, 300))
