@@ -5,8 +5,8 @@
 // launch per node would be launch-latency bound.
 //
 // Node descriptors are compact windows packed into the kernel parameters
-// (<= 30 KB per launch); blockIdx.z selects the node, (x, y) tile its
-// rows x cols extent with the same per-element arithmetic as the single-node
+// (<= 30 KB per launch); blockIdx.z selects the node, blockIdx.x and the
+// threads cover its rows x column-pairs as one flat range, with the same per-element arithmetic as the single-node
 // kernels in elementwise.cu (zero-extended sources, truncated outputs).
 #include <cstring>
 
@@ -16,7 +16,7 @@ namespace ata {
 
 namespace {
 
-constexpr int kMtX = 128, kMtY = 2;
+constexpr int kMtThreads = 256;
 
 // Two adjacent elements (c0 even) with one 16-byte (f64) / 8-byte (f32) access
 // when the window allows it: base aligned to two elements and an even pitch.
@@ -95,23 +95,32 @@ struct P7Batch {
 };
 static_assert(sizeof(C4Batch<double>) <= 30000 && sizeof(P7Batch<double>) <= 30000, "kernel parameter space");
 
+// Work split: blockIdx.z = node; the node's rows x ceil(cols/2) column pairs
+// are one flat index space over blockIdx.x and the 256 threads (consecutive
+// threads take consecutive pairs of a row: coalesced), so narrow nodes of deep
+// recursion levels keep every thread busy.
 template <typename T>
 __global__ void combo4_multi_kernel(const __grid_constant__ C4Batch<T> b) {
   const C4Node<T>& a = b.n[blockIdx.z];
-  const int c0 = (blockIdx.x * blockDim.x + threadIdx.x) * 2;
-  if (c0 >= a.cols) return;
-  for (int r = blockIdx.y * blockDim.y + threadIdx.y; r < a.rows; r += gridDim.y * blockDim.y) {
+  const int cp = (a.cols + 1) >> 1;
+  const int x0 = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+  const int dr = stride / cp, dc = stride - dr * cp;   // the flat index advanced incrementally
+  int r = x0 / cp, cc = x0 - (x0 / cp) * cp;
+  for (; r < a.rows; r += dr, cc += dc) {
+    if (cc >= cp) {
+      cc -= cp;
+      if (++r >= a.rows) break;
+    }
+    const int c0 = cc * 2;
     T v[4][2];
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       v[q][0] = v[q][1] = T(0);
       if (q < a.nsrc) {
         const Win<T>& S = a.src[q];
-        if (r < S.rows) {
-          const T* p = S.p + (long long)r * S.ld + c0;
-          if (c0 < S.cols) v[q][0] = __ldcs(p);
-          if (c0 + 1 < S.cols) v[q][1] = __ldcs(p + 1);
-        }
+        const bool ok = r < S.rows;
+        load_pair(S.p + (ok ? (long long)r * S.ld + c0 : 0), ok ? S.cols - c0 : 0, pair_ok(S.p, S.ld),
+                  v[q][0], v[q][1]);
       }
     }
 #pragma unroll
@@ -127,10 +136,8 @@ __global__ void combo4_multi_kernel(const __grid_constant__ C4Batch<T> b) {
         if (cq == 1) o0 += v[q][0], o1 += v[q][1];
         else if (cq == 2) o0 -= v[q][0], o1 -= v[q][1];
       }
-      T* p = D.p + (long long)r * D.ld + c0;
       const int cmax = a.lower ? min(D.cols, r + 1) : D.cols;
-      if (c0 < cmax) __stcs(p, o0);
-      if (c0 + 1 < cmax) __stcs(p + 1, o1);
+      store_pair(D.p + (long long)r * D.ld + c0, cmax - c0, pair_ok(D.p, D.ld), o0, o1, false);
     }
   }
 }
@@ -138,9 +145,16 @@ __global__ void combo4_multi_kernel(const __grid_constant__ C4Batch<T> b) {
 template <typename T>
 __global__ void postadd7_multi_kernel(const __grid_constant__ P7Batch<T> b) {
   const P7Node<T>& a = b.n[blockIdx.z];
-  const int c0 = (blockIdx.x * blockDim.x + threadIdx.x) * 2;
-  if (c0 >= a.cols) return;
-  for (int r = blockIdx.y * blockDim.y + threadIdx.y; r < a.rows; r += gridDim.y * blockDim.y) {
+  const int cp = (a.cols + 1) >> 1;
+  const int x0 = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+  const int dr = stride / cp, dc = stride - dr * cp;   // the flat index advanced incrementally
+  int r = x0 / cp, cc = x0 - (x0 / cp) * cp;
+  for (; r < a.rows; r += dr, cc += dc) {
+    if (cc >= cp) {
+      cc -= cp;
+      if (++r >= a.rows) break;
+    }
+    const int c0 = cc * 2;
     T p[7][2];
 #pragma unroll
     for (int i = 0; i < 7; ++i) {
@@ -189,12 +203,14 @@ Win<T> win_of(const DDest<T>& d) {
 
 // grid for `count` nodes of at most maxcols x maxrows: ~32 blocks per SM in total
 static dim3 multi_grid(int count, int maxrows, int maxcols) {
-  const int gx = (maxcols + 2 * kMtX - 1) / (2 * kMtX);
-  long long gy = 148LL * 32 / ((long long)gx * count);
-  const long long need = (maxrows + kMtY - 1) / kMtY;
-  if (gy > need) gy = need;
-  if (gy < 1) gy = 1;
-  return dim3(gx, (unsigned)gy, count);
+  // one block row per 256 column pairs of the largest node, capped so the
+  // launch has ~16 blocks per SM (grid-stride loop inside)
+  const long long pairs = (long long)maxrows * ((maxcols + 1) / 2);
+  long long gx = (pairs + kMtThreads - 1) / kMtThreads;
+  const long long cap = 148LL * 16 / count;
+  if (gx > cap) gx = cap;
+  if (gx < 1) gx = 1;
+  return dim3((unsigned)gx, 1, count);
 }
 
 }  // namespace
@@ -226,7 +242,7 @@ cudaError_t launch_combo4_multi(const EwArgs<T>* nodes, int count, cudaStream_t 
       maxcols = maxcols > a.cols ? maxcols : a.cols;
     }
     if (b.count == 0) continue;
-    combo4_multi_kernel<T><<<multi_grid(b.count, b.maxrows, maxcols), dim3(kMtX, kMtY), 0, s>>>(b);
+    combo4_multi_kernel<T><<<multi_grid(b.count, b.maxrows, maxcols), kMtThreads, 0, s>>>(b);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
@@ -255,7 +271,7 @@ cudaError_t launch_postadd7_multi(const EwArgs<T>* nodes, const int* accumulate,
       maxcols = maxcols > a.cols ? maxcols : a.cols;
     }
     if (b.count == 0) continue;
-    postadd7_multi_kernel<T><<<multi_grid(b.count, b.maxrows, maxcols), dim3(kMtX, kMtY), 0, s>>>(b);
+    postadd7_multi_kernel<T><<<multi_grid(b.count, b.maxrows, maxcols), kMtThreads, 0, s>>>(b);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }
