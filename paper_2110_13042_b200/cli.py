@@ -74,23 +74,23 @@ def _threshold(text: str):
 def build_parser() -> argparse.ArgumentParser:
     p = argparse.ArgumentParser(prog="atamul", description="Benchmark the recursive A^T A kernels (B200).")
     p.add_argument("--mode", choices=["seq", "shared", "dist", "oracle", "auto"], default="seq")
-    p.add_argument("--m", type=int, default=None, help="rows of A (defaults to --n)")
-    p.add_argument("--n", type=int, default=1024, help="columns of A")
-    p.add_argument("--procs", type=int, default=None, help="workers/processes (shared and dist modes only)")
+    p.add_argument("--m", type=int, default=None, help="row count of A; --n when omitted")
+    p.add_argument("--n", type=int, default=1024, help="column count of A (and order of C)")
+    p.add_argument("--procs", type=int, default=None, help="task-tree processes; shared/dist modes only")
     p.add_argument("--threshold", type=_threshold, default=None,
-                   help="base-case element-count threshold (default 32768, or env ATA_THRESHOLD; 'auto')")
+                   help="leaf threshold in elements (32768 unless ATA_THRESHOLD is set) or 'auto'")
     p.add_argument("--dtype", choices=["f32", "f64"], default="f64")
     p.add_argument("--seed", type=int, default=0)
-    p.add_argument("--reps", type=int, default=5, help="timed repetitions; the median is reported")
-    p.add_argument("--check", action="store_true", help="compare each result against the classical kernel")
-    p.add_argument("--csv", metavar="PATH", help="append the record to a CSV")
-    p.add_argument("--comm-csv", metavar="PATH", help="write per-process communication counters (dist only)")
-    p.add_argument("--count-mults", action="store_true", help="report the exact scalar-multiplication count")
-    p.add_argument("--in", dest="in_path", metavar="PATH", help="read A from an ATAM file instead of generating")
-    p.add_argument("--out", dest="out_path", metavar="PATH", help="write the generated A to an ATAM file")
+    p.add_argument("--reps", type=int, default=5, help="timed runs after one warm-up; prints the median")
+    p.add_argument("--check", action="store_true", help="check every run against one classical SYRK kernel")
+    p.add_argument("--csv", metavar="PATH", help="append the result row to this CSV file")
+    p.add_argument("--comm-csv", metavar="PATH", help="dist mode: write the retrieve-phase message/word counters")
+    p.add_argument("--count-mults", action="store_true", help="print the exact number of scalar multiplications")
+    p.add_argument("--in", dest="in_path", metavar="PATH", help="load A from this ATAM file (no generation)")
+    p.add_argument("--out", dest="out_path", metavar="PATH", help="save the input matrix as an ATAM file")
     p.add_argument("--leaf-kernel", choices=["fast", "naive"], default="fast",
                    help="kernel used by dist-mode leaves (naive: one classical product per leaf)")
-    p.add_argument("--dump-tree", action="store_true", help="print the scheduler tree and exit")
+    p.add_argument("--dump-tree", action="store_true", help="render the task tree of the mode and stop")
     return p
 
 
