@@ -58,9 +58,9 @@ def parse():
     p.add_argument("--gain", type=float, default=None,
                    help="auto plan: split a Strassen node when saved time > gain x added time")
     p.add_argument("--dist", choices=["auto", "rows", "tree"], default="auto",
-                   help="N>1 partition: row shards + NCCL reduce, or the reference's distributed task "
-                        "tree (leaf per rank, blocks retrieved over NCCL); auto = the tree where the "
-                        "reference's own tree is a bunch (fp64 configs, N >= 6), else rows")
+                   help="N>1 partition: row shards + one NCCL reduce (auto; the reference's tree for "
+                        "N <= 5), or the reference's distributed task tree (leaf per rank, blocks "
+                        "retrieved over NCCL point-to-point; its N >= 6 layout)")
     p.add_argument("--fuse-leaf-sums", action="store_true",
                    help="A/B: last Strassen level's operand sums summed in the product loads")
     p.add_argument("--dump-units", default=None, help="write per-launch timings (JSON) here")
@@ -266,7 +266,7 @@ def main():
     tree = None
     if world > 1:
         t_ref = build_tree_distributed(world, m, n)
-        if args.dist == "tree" or (args.dist == "auto" and f64 and t_ref.root.bunch):
+        if args.dist == "tree":
             tree = t_ref
     r0, r1 = pdist.tree_rows(tree, rank) if tree is not None else pdist.shard_rows(m, world, rank)
     # ---- inputs: seeded host draw of this rank's rows, then H2D ----

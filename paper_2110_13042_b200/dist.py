@@ -230,11 +230,12 @@ def run_tree_process(tree, p: int, get_block, link, alpha=1.0, threshold="auto",
 
 
 def add_lower_into(C, block):
-    """lower(C) += lower(block) (C's strict upper triangle untouched)."""
-    import torch
+    """lower(C) += lower(block), C's strict upper triangle untouched: the
+    native pack / accumulate-unpack kernels (one pass each over the triangle)."""
+    from .matrix import PackedLowerTriangular, pack_lower, unpack_lower
     n = int(C.shape[0])
-    il = torch.tril_indices(n, n, device=block.device)
-    C[il[0], il[1]] += block[il[0], il[1]]
+    packed = pack_lower(block)
+    unpack_lower(PackedLowerTriangular(n, packed.data), C, accumulate=True)
 
 
 def tree_link(group=None):
