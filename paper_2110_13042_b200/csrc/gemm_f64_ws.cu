@@ -50,7 +50,7 @@ constexpr int CONSUMERS = WS_CW, PRODUCERS = 128, THREADS = CONSUMERS * 32 + PRO
 constexpr int PRODUCER_REGS = 40, CONSUMER_REGS = CONSUMERS == 8 ? 232 : 104;
 constexpr int WTM = CONSUMERS == 8 ? 8 : 4, WTN = 4;  // 64 x 32 or 32 x 32 per consumer warp
 constexpr int SMEM_BUDGET = 225 * 1024;
-constexpr int TSLOTS = 2;        // tile-info ring
+constexpr int TSLOTS = 3;        // tile-info ring capacity (device-memory descriptors use 3 slots, parameter-space 2)
 }  // namespace ws64
 
 __device__ __forceinline__ void dmma_ws(double (&c)[2], double a, double b) {
@@ -237,9 +237,15 @@ __global__ void __launch_bounds__(ws64::THREADS, 1)
   int* tinfo = reinterpret_cast<int*>(tempty + TSLOTS);  // TSLOTS entries
   int* bcast = tinfo + TSLOTS;                            // producer-internal broadcast
 
-  // producer-side copy of a device-memory tile descriptor (BatchArgsGlobal64)
+  // Device-memory descriptors (BatchArgsGlobal64, thousands of small products):
+  // the producers copy each tile's descriptor into a shared slot and decode
+  // the tile once; consumers read both from the slot and release it after
+  // their epilogue.  Parameter-space descriptors need none of it.
+  constexpr bool kSmemDesc = std::is_same<Args, BatchArgsGlobal64>::value;
+  constexpr int kSlots = kSmemDesc ? 3 : 2;
   __shared__ __align__(16) unsigned char
-      pdesc_raw[std::is_same<Args, BatchArgsGlobal64>::value ? sizeof(DProdT<double, kNarrowDests>) : 16];
+      pdesc_raw[kSmemDesc ? kSlots * sizeof(DProdT<double, kNarrowDests>) : 16];
+  __shared__ int tdec[kSmemDesc ? kSlots : 1][3];  // decoded tile (product, tile row, tile col) per slot
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
 
@@ -266,26 +272,44 @@ __global__ void __launch_bounds__(ws64::THREADS, 1)
       named_sync(1, PRODUCERS);
       const int tile = *bcast;
       named_sync(1, PRODUCERS);
-      const int slot = it % TSLOTS;
-      if (pt == 0) {
-        if (it >= TSLOTS) mbar_wait(&tempty[slot], ((it / TSLOTS) - 1) & 1);
-        tinfo[slot] = tile;
-        mbar_arrive(&tfull[slot]);
-      }
-      if (tile >= args.total_tiles) break;
-      const TileInfo tl = decode_tile(args, tile);
-      // the producers (40 registers) read their tile's descriptor from the
-      // parameter space, or -- device-memory descriptors -- from a shared copy
-      // made once per tile (a by-value copy would live in local memory)
+      const int slot = it % kSlots;
       using PD = std::remove_cv_t<std::remove_reference_t<decltype(prod_of(args, 0))>>;
       const PD* Pp;
-      if constexpr (std::is_same<Args, BatchArgsGlobal64>::value) {
-        const uint32_t* src = reinterpret_cast<const uint32_t*>(args.gp + tl.pi);
-        uint32_t* dst = reinterpret_cast<uint32_t*>(pdesc_raw);
-        for (int i = pt; i < (int)(sizeof(PD) / 4); i += PRODUCERS) dst[i] = __ldg(src + i);
+      TileInfo tl;
+      if constexpr (kSmemDesc) {
+        // the slot (tile index, decoded tile, descriptor copy) is free once the
+        // consumers have finished the tile that last used it
+        if (pt == 0 && it >= kSlots) mbar_wait(&tempty[slot], ((it / kSlots) - 1) & 1);
         named_sync(1, PRODUCERS);
-        Pp = reinterpret_cast<const PD*>(pdesc_raw);
+        if (tile >= args.total_tiles) {
+          if (pt == 0) {
+            tinfo[slot] = tile;
+            mbar_arrive(&tfull[slot]);
+          }
+          break;
+        }
+        tl = decode_tile(args, tile);
+        // the producers (40 registers) read the copy too (a by-value copy would live in local memory)
+        const uint32_t* src = reinterpret_cast<const uint32_t*>(args.gp + tl.pi);
+        uint32_t* dst = reinterpret_cast<uint32_t*>(pdesc_raw) + slot * (sizeof(PD) / 4);
+        for (int i = pt; i < (int)(sizeof(PD) / 4); i += PRODUCERS) dst[i] = __ldg(src + i);
+        Pp = reinterpret_cast<const PD*>(dst);
+        named_sync(1, PRODUCERS);
+        if (pt == 0) {
+          tinfo[slot] = tile;
+          tdec[slot][0] = tl.pi;
+          tdec[slot][1] = tl.ti;
+          tdec[slot][2] = tl.tj;
+          mbar_arrive(&tfull[slot]);   // release: the descriptor copy and decoded tile
+        }
       } else {
+        if (pt == 0) {
+          if (it >= kSlots) mbar_wait(&tempty[slot], ((it / kSlots) - 1) & 1);
+          tinfo[slot] = tile;
+          mbar_arrive(&tfull[slot]);
+        }
+        if (tile >= args.total_tiles) break;
+        tl = decode_tile(args, tile);
         Pp = &prod_of(args, tl.pi);
       }
       const PD& P = *Pp;
@@ -368,14 +392,24 @@ __global__ void __launch_bounds__(ws64::THREADS, 1)
   const int g = lane >> 2, q = lane & 3;
   int kstep = 0;
   for (int it = 0;; ++it) {
-    const int slot = it % TSLOTS;
-    mbar_wait(&tfull[slot], (it / TSLOTS) & 1);
+    const int slot = it % kSlots;
+    mbar_wait(&tfull[slot], (it / kSlots) & 1);
     const int tile = tinfo[slot];
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&tempty[slot]);
-    if (tile >= args.total_tiles) break;
-    const TileInfo tl = decode_tile(args, tile);
-    typename ProdHold<Args>::type P = prod_of(args, tl.pi);
+    TileInfo tl;
+    if constexpr (kSmemDesc) {
+      if (tile >= args.total_tiles) break;
+      tl.pi = tdec[slot][0];
+      tl.ti = tdec[slot][1];
+      tl.tj = tdec[slot][2];
+    } else {   // parameter-space descriptor: the slot is free at once
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[slot]);
+      if (tile >= args.total_tiles) break;
+      tl = decode_tile(args, tile);
+    }
+    using PDc = std::remove_cv_t<std::remove_reference_t<decltype(prod_of(args, 0))>>;
+    const PDc& P = kSmemDesc ? *reinterpret_cast<const PDc*>(pdesc_raw + slot * sizeof(PDc))
+                             : prod_of(args, tl.pi);
     const bool syrk = P.kind == kSyrk;
     const bool same = syrk && tl.ti == tl.tj;
     const int i0 = tl.ti * BM, j0 = tl.tj * BN;
@@ -475,6 +509,10 @@ __global__ void __launch_bounds__(ws64::THREADS, 1)
         named_sync(2, CONSUMERS * 32);
         if (ctid == 0) st_release(sem, turn + 1);
       }
+    }
+    if (kSmemDesc) {    // the shared descriptor copy was read up to here
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[slot]);
     }
   }
 }
