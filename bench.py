@@ -55,6 +55,11 @@ def parse():
     p.add_argument("--leaf-cols", type=int, default=None)
     p.add_argument("--max-depth", type=int, default=None)
     p.add_argument("--min-dim", type=int, default=None)
+    p.add_argument("--autotune", action="store_true",
+                   help="auto plan: measure the leaf-product / addition rates and pick the SYRK leaf "
+                        "width on this GPU before the timed region (autotune.tune); on by default for "
+                        "c3, whose BASELINE cutoff is 'auto-tuned'")
+    p.add_argument("--no-autotune", action="store_true")
     p.add_argument("--gain", type=float, default=None,
                    help="auto plan: split a Strassen node when saved time > gain x added time")
     p.add_argument("--dist", choices=["auto", "rows", "tree"], default="auto",
@@ -286,6 +291,11 @@ def main():
                                                         ("fuse_leaf_sums", args.fuse_leaf_sums or None))
                                                      if v is not None})
     mloc = r1 - r0
+    tuned = None
+    if (args.autotune or (args.config == "c3" and not args.no_autotune)) and threshold == "auto" and f64:
+        from paper_2110_13042_b200 import autotune
+        params = autotune.tune(mloc, n, dev, base=params)
+        tuned = {"leaf_cols": params.leaf_cols, "dmma_tflops": params.dmma_tflops, "hbm_gbs": params.hbm_gbs}
     # what this rank's plan computes: the whole row shard into C, or (task
     # tree) its leaf -- an AtA of a column block or an AtB of two -- into a
     # private block that run_tree_process then retrieves up the tree
@@ -474,7 +484,8 @@ def main():
                                     mloc * n * (n + 1) / 2 if leaf is None else
                                     mloc * leaf.a_region.cols * (leaf.a_region.cols + 1) / 2
                                     if leaf.b_region is None else
-                                    mloc * leaf.a_region.cols * leaf.b_region.cols)},
+                                    mloc * leaf.a_region.cols * leaf.b_region.cols),
+                                "autotuned": tuned},
                        "effective_pct_of_peak": value / 1e3 / peak},
             "roofline": roofline,
             "clocks": clk.summary,

@@ -57,7 +57,10 @@ def ata(A, C, alpha=1.0, threshold=DEFAULT_THRESHOLD, ws: StrassenWorkspace | No
     """Lower triangle of C += alpha * A^T A for A (m x n), C (n x n).
 
     ``precision`` only matters for f32: "fp32" (3xTF32 products, fp32-level
-    accuracy like the reference's f32 einsum) or "tf32" (single-pass TF32)."""
+    accuracy like the reference's f32 einsum) or "tf32" (single-pass TF32).
+    ``auto_params`` (threshold "auto"): AutoParams, or "tune" to measure the
+    leaf-product and addition rates and pick the leaf width on this device
+    (autotune.py; the first call per shape pays the measurement)."""
     a, c = as_array(A), as_array(C)
     m, n = int(a.shape[0]), int(a.shape[1])
     if tuple(c.shape) != (n, n):
@@ -66,6 +69,10 @@ def ata(A, C, alpha=1.0, threshold=DEFAULT_THRESHOLD, ws: StrassenWorkspace | No
         threshold = int(threshold)
         if threshold < 1:
             raise ShapeMismatchError("shape mismatch: threshold must be >= 1")
+    if threshold == AUTO and isinstance(auto_params, str):
+        if auto_params != "tune":
+            raise ValueError(f"auto_params must be AutoParams, None or 'tune', not {auto_params!r}")
+        auto_params = _tuned_params(a, c, m, n)
     if threshold == AUTO and _pipelined_host_ata(a, c, m, n, alpha, ws, counter, auto_params, precision):
         return
     C_ = DeviceOperand(c, writable=True, lower=True)   # kernels touch only lower(C)
@@ -93,6 +100,19 @@ def ata(A, C, alpha=1.0, threshold=DEFAULT_THRESHOLD, ws: StrassenWorkspace | No
 
 
 _WS_CACHE: dict = {}
+
+
+def _tuned_params(a, c, m, n):
+    """auto_params="tune": rates and SYRK leaf width measured on the device
+    that runs the plan (autotune.tune, cached per shape); fp64 only -- other
+    dtypes keep the default parameters."""
+    import torch
+    from . import autotune
+    dt = getattr(c, "dtype", None)
+    if dt not in (torch.float64, np.float64):
+        return None
+    dev = c.device if isinstance(c, torch.Tensor) and c.is_cuda else None
+    return autotune.tune(m, n, dev)
 
 
 def _default_workspace(m, n, threshold, dtype):

@@ -100,3 +100,23 @@ def test_cli_seq_count_matches_reference_and_atam(tmp_path):
     r2 = _cli("--mode", "seq", "--in", str(path), "--threshold", "512", "--count-mults", "--reps", "1",
               "--check")
     assert r2.returncode == 0 and f", {want[0]} scalar mults" in r2.stdout
+
+
+def test_autotune_rates_and_leaf_choice(rng):
+    """autotune.calibrate measures the FP64 leaf-product and addition-pass
+    rates on this GPU; tune picks the SYRK leaf width by timing candidate
+    plans; ata(auto_params="tune") computes the same Gram matrix."""
+    import torch
+    import paper_2110_13042_b200 as P
+    from paper_2110_13042_b200 import autotune
+    tf, gbs = autotune.calibrate()
+    assert 15.0 <= tf <= 40.0, tf            # DMMA peak 37.2 TF/s
+    assert 1500.0 <= gbs <= 7000.0, gbs      # HBM copy 6.5 TB/s
+    m, n = 3000, 2600
+    p = autotune.tune(m, n)
+    assert p.leaf_cols in autotune.LEAF_CANDIDATES and p.dmma_tflops == tf and p.hbm_gbs == gbs
+    assert autotune.tune(m, n) is p          # cached per shape
+    a = rng.uniform(-1, 1, (m, n))
+    C = torch.zeros((n, n), dtype=torch.float64, device="cuda")
+    P.ata(torch.from_numpy(a).cuda(), C, 1.0, threshold="auto", auto_params="tune")
+    assert O.rel_frobenius_lower(C.cpu().numpy(), O.gram_blas(a)) <= 1e-12
