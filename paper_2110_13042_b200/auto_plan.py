@@ -69,6 +69,8 @@ class AutoParams:
     min_chunk: int = 8192          # ... into chunks of at least this many rows
     tf32_tflops: float = 400.0     # single-pass TF32 leaf-product rate (tcgen05, profiles/)
     tf32_fill_waves: int = 8       # 128x256 tcgen05 tiles: more chunks to fill 148 SMs
+    tf32_ring: bool = True         # single-pass TF32: round through the product kernel's L2 ring
+                                   # instead of an HBM rounding pass when the plan allows (_ringify)
     fuse_leaf_sums: bool = False   # FP64: leaf products read their Strassen operand sums as two
                                    # zero-extended terms summed in the kernel's load path (no
                                    # combo4 pass for the last Strassen level).  Off: measured
@@ -419,6 +421,79 @@ class _AutoPlanner:
         self.emit_products(diag_prods)
 
 
+RING_PIECE_ROWS = 192    # scratch sized for pieces of up to 192 rows (tc2::PR, gemm_tf32_2sm.cu)
+RING_SLOTS = 64   # scratch for up to 64 slots per ring (the kernel uses TC2_RING_SLOTS)
+
+
+def _tc2_tiles(kind: int, n: int, k: int) -> int:
+    """256 x 256 CTA-pair tiles of one product (gemm_tf32_2sm.cu t2_decode)."""
+    tn, tk = -(-n // 256), -(-k // 256)
+    return tn * (tn + 1) // 2 if kind == nat.OP_SYRK else tn * tk
+
+
+def _ringify(plan: Plan, m: int, n: int, lda: int) -> Plan:
+    """Single-pass TF32 plan [ROUND A -> R, one product group over row chunks of
+    R, partial sums]: when the product group is chunk-major with equal chunks,
+    an even chunk count and two chunks per wave of the CTA-pair kernel's
+    persistent grid (25..37 tiles per chunk on 74 pairs), the products read
+    A's raw rows and the ROUND op becomes the kernel's L2 rounding ring
+    (accumulate = 2, d[0] = a ~50 MB ring scratch in the rounded copy's
+    former workspace region): no rounded copy of A is written to HBM.
+    Otherwise the plan is returned unchanged."""
+    ops = plan.ops
+    if len(ops) < 2 or int(ops[0]["type"]) != nat.OP_ROUND or lda % 4 or n % 32:
+        return plan
+    src, dst = ops[0]["s"][0], ops[0]["d"][0]
+    if int(dst["ld"]) != lda or int(src["base"]) != nat.BASE_A or int(src["off"]) != 0:
+        return plan
+    prods = [i for i in range(1, len(ops)) if int(ops[i]["type"]) in (nat.OP_GEMM, nat.OP_SYRK)]
+    if not prods or prods != list(range(1, 1 + len(prods))) or len(prods) > MAX_BATCH:
+        return plan
+    if len({int(ops[i]["group"]) for i in prods}) != 1:
+        return plan
+    r_off, r_end = int(dst["off"]), int(dst["off"]) + m * lda
+    chunk_rows, chunks, tiles = None, [], {}
+    for i in prods:
+        op = ops[i]
+        if int(op["ns"]) != 1 or (int(op["type"]) == nat.OP_GEMM and int(op["nt"]) != 1):
+            return plan
+        terms = [op["s"][0]] + ([op["t"][0]] if int(op["type"]) == nat.OP_GEMM else [])
+        rows0 = None
+        for t in terms:
+            if int(t["base"]) != nat.BASE_WS or not r_off <= int(t["off"]) < r_end or int(t["ld"]) != lda:
+                return plan
+            row = (int(t["off"]) - r_off) // lda
+            chunk_rows = chunk_rows or int(t["rows"])
+            if int(t["rows"]) != chunk_rows or row % chunk_rows or (rows0 is not None and row != rows0):
+                return plan
+            rows0 = row
+        c = rows0 // chunk_rows
+        if chunks and c not in (chunks[-1], chunks[-1] + 1):
+            return plan
+        chunks.append(c)
+        tiles[c] = tiles.get(c, 0) + _tc2_tiles(int(op["type"]), int(op["n"]), int(op["k"]))
+    tpc = set(tiles.values())
+    nch = len(tiles)
+    if len(tpc) != 1 or nch % 2 or chunk_rows * nch != m or not 25 <= next(iter(tpc)) <= 37:
+        return plan
+    out = ops.copy()
+    ring_elems = 2 * RING_SLOTS * RING_PIECE_ROWS * n + 4 * RING_SLOTS
+    out[0]["accumulate"] = 2
+    if -(-ring_elems // n) * n > m * lda:
+        return plan
+    out[0]["d"][0]["off"] = r_off
+    out[0]["d"][0]["ld"] = n
+    out[0]["d"][0]["rows"] = -(-ring_elems // n)
+    out[0]["d"][0]["cols"] = n
+    for i in prods:
+        for fld, cnt in (("s", int(out[i]["ns"])), ("t", int(out[i]["nt"]))):
+            for j in range(cnt):
+                t = out[i][fld][j]
+                t["base"] = nat.BASE_A
+                t["off"] = int(t["off"]) - r_off
+    return Plan(out, plan.mults, plan.ws_scalars, plan.launches - 1, plan.kind)
+
+
 def plan_ata_auto(m: int, n: int, lda: int, ldc: int, params: AutoParams = AutoParams(),
                   round_tf32: bool = False) -> Plan:
     """GPU plan for lower(C) += alpha A^T A (see module docstring).  round_tf32:
@@ -429,6 +504,8 @@ def plan_ata_auto(m: int, n: int, lda: int, ldc: int, params: AutoParams = AutoP
     ap.ata(m, n, lda, ldc, round_tf32)
     plan = ap.pb.finish()
     plan.ws_scalars = max(plan.ws_scalars, ap.ws_peak)
+    if round_tf32 and params.tf32_ring:
+        plan = _ringify(plan, m, n, lda)
     return plan
 
 

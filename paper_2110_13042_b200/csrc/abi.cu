@@ -153,6 +153,11 @@ int validate_op(const ata_op& op, const Bases& b, int i) {
       if (op.nd != 1) return fail(ATA_E_ARG, "fill needs 1 dest");
       return ATA_OK;
     case ATA_OP_ROUND:
+      if (op.accumulate == 2) {   // L2 ring: d[0] is the ring scratch (any shape), s[0] the raw operand
+        if (op.ns != 1 || op.nd != 1) return fail(ATA_E_ARG, "ring round needs one source and one scratch window");
+        if (b.esize != 4) return fail(ATA_E_ARG, "round: fp32 plans only");
+        return ATA_OK;
+      }
       if (op.ns != 1 || op.nd != 1 || op.s[0].rows != op.d[0].rows || op.s[0].cols != op.d[0].cols)
         return fail(ATA_E_SHAPE, "shape mismatch: round needs one source and one equal-shape dest");
       if (b.esize != 4) return fail(ATA_E_ARG, "round: fp32 plans only");
@@ -503,6 +508,7 @@ int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, int* sync, int64_t 
   };
   auto on_ew = [&](int i) -> int {
     if (int rc = join_all()) return rc;
+    ata::set_tf32_ring(nullptr);   // a ring belongs to the product group right after its ROUND op
     g_launches += 1;
     const ata_op& op = ops[i];
     cudaError_t e = cudaSuccess;
@@ -530,6 +536,20 @@ int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, int* sync, int64_t 
       e = ata::launch_fill<T>(d.p, d.ld, d.rows, d.cols, s);
     } else if (op.type == ATA_OP_COMBO4) {
       e = ata::launch_combo4<T>(combo4_args<T>(op, b), s);
+    } else if (op.type == ATA_OP_ROUND && op.accumulate == 2) {
+      // no pass: the next TF32 product group rounds its operands through the L2 ring
+      const ata::DTerm<T> src = term_of<T>(op.s[0], b);
+      const ata::DDest<T> dst = dest_of<T>(op.d[0], b);
+      ata::Tf32Ring r;
+      r.a = reinterpret_cast<const float*>(src.p);
+      r.lda = src.ld;
+      r.rows = src.rows;
+      r.cols = src.cols;
+      r.buf = reinterpret_cast<float*>(dst.p);
+      r.buf_elems = (long long)dst.rows * dst.ld;
+      ata::set_tf32_ring(&r);
+      g_launches -= 1;
+      return ATA_OK;
     } else if (op.type == ATA_OP_ROUND) {
       const ata::DTerm<T> src = term_of<T>(op.s[0], b);
       const ata::DDest<T> dst = dest_of<T>(op.d[0], b);
@@ -543,6 +563,7 @@ int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, int* sync, int64_t 
   };
   auto on_ew_run = [&](int first, int last) -> int {
     if (int rc = join_all()) return rc;
+    ata::set_tf32_ring(nullptr);
     std::vector<ata::EwArgs<T>> args;
     std::vector<int> acc;
     args.reserve(last - first);
@@ -571,6 +592,7 @@ int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, int* sync, int64_t 
   };
   int rc = walk_batches(ops, n_ops, ordering, narrow, on_batch, on_ew, on_ew_run);
   int rj = join_all();
+  ata::set_tf32_ring(nullptr);
   return rc ? rc : rj;
 }
 

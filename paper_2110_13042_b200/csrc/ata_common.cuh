@@ -112,6 +112,17 @@ template <typename T> cudaError_t launch_update(const EwArgs<T>& a, cudaStream_t
 template <typename T> cudaError_t launch_combo4(const EwArgs<T>& a, cudaStream_t s);
 cudaError_t launch_round_tf32(const float* src, long long lds, float* dst, long long ldd, int rows, int cols,
                               cudaStream_t s);
+// L2 rounding ring for the next single-pass TF32 product launch on this thread
+// (ATA_OP_ROUND with accumulate == 2): the products read the raw rows of `a`;
+// `buf` (buf_elems floats) holds the two rings and their flags.
+struct Tf32Ring {
+  const float* a;
+  long long lda;
+  int rows, cols;
+  float* buf;
+  long long buf_elems;
+};
+void set_tf32_ring(const Tf32Ring* r);  // nullptr clears
 template <typename T> cudaError_t launch_postadd7(const EwArgs<T>& a, int accumulate, cudaStream_t s);
 // many independent nodes per launch (elementwise_multi.cu); combo4 nodes: <= 5 outputs
 template <typename T> cudaError_t launch_combo4_multi(const EwArgs<T>* nodes, int count, cudaStream_t s);

@@ -58,9 +58,18 @@ constexpr int HALF = 128;                                 // rows of A / cols of
 constexpr int A_BYTES = BK * HALF * 4;                    // 16 KB
 constexpr int B_BYTES = BK * HALF * 4;                    // 16 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;            // 32 KB per CTA
-constexpr int THREADS = 192;
+constexpr int THREADS = 448;   // warps 6-13: ring rounders (idle without the ring)
+constexpr int ROUNDERS = THREADS - 192;
 constexpr int TMEM_COLS = 512;
 constexpr int kMax = 48;   // = kMaxBatch: one launch per plan group (15 KB of kernel parameters)
+#ifndef TC2_RING_ROWS
+#define TC2_RING_ROWS 96
+#endif
+constexpr int PR = TC2_RING_ROWS;  // rows per ring piece (a whole number of k-blocks)
+#ifndef TC2_RING_PARTS
+#define TC2_RING_PARTS 2
+#endif
+constexpr int RH = TC2_RING_PARTS;  // CTAs rounding one piece (PR / RH rows each); ready counts RH per piece
 constexpr uint32_t IDESC = (1u << 4) | (2u << 7) | (2u << 10) | (1u << 15) | (1u << 16) |
                            (uint32_t(BN >> 3) << 17) | (uint32_t(BM >> 4) << 24);
 }  // namespace tc2
@@ -76,11 +85,32 @@ struct alignas(64) Tc2Prod {
   int tn, tk, tile_begin, accumulate;
 };
 
+// L2 rounding ring (single-pass TF32 without an HBM rounding pass): the
+// products read raw fp32 row chunks of A; rounder warps of every CTA round
+// pieces of PR rows into two small rings (one per chunk of the running wave)
+// that stay in L2, and the TMA producers read the rounded pieces from there.
+// Flags (cumulative per slot): ready = parts written (RH per occupancy),
+// consumed = tiles (CTA pairs) whose TMA loads of the slot have landed.
+struct Tc2Ring {
+  CUtensorMap rmap[2];       // 3-D maps over ring 0 / 1: {32, nslot * PR, ncols / 32}
+  float* ring[2];
+  const float* a;            // raw A (chunk c starts at row c * chunk_rows)
+  long long lda;
+  int* ready;                // [2][nslot]
+  int* consumed;             // [2][nslot]
+  int chunk_rows, pieces;    // rows per chunk, pieces per chunk (PR rows each)
+  int nslot, nwave, tpc, ncols;
+  int chunk[tc2::kMax];      // chunk of each product
+  int col_s[tc2::kMax], col_t[tc2::kMax];  // first A column of each product's S / T window
+};
+
 struct Tc2Args {
   Tc2Prod p[tc2::kMax];
   int count;
   int total_tiles;
   int tma3d;  // 1: every window is a whole number of 32-column panels -> 3-D maps, one TMA per operand
+  int ring;   // 1: operands are rounded through the L2 ring (rg)
+  Tc2Ring rg;
 };
 static_assert(sizeof(Tc2Args) <= 32000, "kernel parameter space (CUDA 12.1+: 32 KB)");
 
@@ -109,6 +139,35 @@ __device__ __forceinline__ void t2_wait(uint64_t* bar, unsigned parity) {
     if (ok) return;
     if (t2_now() - t0 > 10000000000ull) __trap();  // 10 s: protocol error, fail loudly
   }
+}
+__device__ __forceinline__ int t2_ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ int t2_ld_relaxed(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+// Poll with relaxed loads (an acquire load invalidates L1 on every try), then
+// one acquire load -- not a fence: in the TMA producer a gpu-scope fence would
+// also wait for the thread's bulk copies in flight.  Bounded: traps on a
+// protocol error instead of hanging.
+__device__ __forceinline__ void t2_spin_ge(const int* p, int target) {
+  if (t2_ld_relaxed(p) < target) {
+    const uint64_t t0 = t2_now();
+    while (t2_ld_relaxed(p) < target) {
+      __nanosleep(100);
+      if (t2_now() - t0 > 10000000000ull) __trap();
+    }
+  }
+  (void)t2_ld_acquire(p);
+}
+__device__ __forceinline__ uint32_t t2_rna(float x) {  // round to nearest TF32, ties away (= ATA_OP_ROUND)
+  uint32_t r;
+  asm("cvt.rna.tf32.f32 %0, %1;" : "=r"(r) : "f"(x));
+  return r;
 }
 __device__ __forceinline__ uint32_t t2_rank() {
   uint32_t r;
@@ -209,8 +268,29 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
         const CUtensorMap* mt = P.kind == kSyrk ? &P.ts : &P.tt;
         const int i0 = t.ti * BM + rank * HALF, j0 = t.tj * BN + rank * HALF;
         const int KT = (P.m + BK - 1) / BK;
+        const int rc = args.ring ? args.rg.chunk[t.pi] : 0, rr = rc & 1;
+        const int rs = args.ring ? (args.rg.col_s[t.pi] + i0) / 32 : 0;
+        const int rt = args.ring ? ((P.kind == kSyrk ? args.rg.col_s[t.pi] : args.rg.col_t[t.pi]) + j0) / 32 : 0;
+        int ahead = -1;   // ready count of the next piece's slot, read one piece early (latency hidden)
         for (int kb = 0; kb < KT; ++kb, ++ks) {
           const int s = ks % STAGES;
+          int ring_row = 0;
+          if (args.ring) {   // the piece holding rows [kb*BK, kb*BK + BK) must be rounded into its slot
+            const int k = (rc >> 1) * args.rg.pieces + kb * BK / PR;   // occupancy index in ring rr
+            const int slot = k % args.rg.nslot;
+            ring_row = slot * PR + kb * BK % PR;
+            if (kb * BK % PR == 0) {
+              // cumulative: RH parts per occupancy of this slot; k / nslot earlier occupancies
+              const int* flag = args.rg.ready + rr * args.rg.nslot + slot;
+              const int target = RH * (k / args.rg.nslot + 1);
+              if (ahead < target || t2_ld_acquire(flag) < target) t2_spin_ge(flag, target);
+              asm volatile("fence.proxy.async.global;" ::: "memory");
+              if ((kb + PR / BK) * BK < P.m) {
+                const int* nf = args.rg.ready + rr * args.rg.nslot + (k + 1) % args.rg.nslot;
+                asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(ahead) : "l"(nf) : "memory");
+              }
+            }
+          }
           t2_wait(&empty[s], ((ks / STAGES) & 1) ^ 1);
           uint8_t* sa = smem + s * STAGE_BYTES;
           uint8_t* sb = sa + A_BYTES;
@@ -219,7 +299,18 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(t2_smem(&full[s])),
                          "r"(2 * STAGE_BYTES)
                          : "memory");
-          if (args.tma3d) {
+          if (args.ring) {
+            asm volatile(
+                "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(t2_smem(sa)),
+                "l"(reinterpret_cast<uint64_t>(&args.rg.rmap[rr])), "r"(bar), "r"(0), "r"(ring_row), "r"(rs)
+                : "memory");
+            asm volatile(
+                "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(t2_smem(sb)),
+                "l"(reinterpret_cast<uint64_t>(&args.rg.rmap[rr])), "r"(bar), "r"(0), "r"(ring_row), "r"(rt)
+                : "memory");
+          } else if (args.tma3d) {
             // one box of [HALF/32 panels][BK rows][32 cols] per operand (3-D map)
             asm volatile(
                 "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
@@ -289,10 +380,77 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
                   "%1;" ::"r"(t2_smem(&tfull[buf])),
                   "h"((uint16_t)3)
                   : "memory");
+            if (args.ring && ((kb * BK + BK) % PR == 0 || kb == KT - 1)) {
+              // both CTAs' boxes of this piece are in shared memory: its ring slot may be reused
+              const int rc = args.rg.chunk[t.pi];
+              const int k = (rc >> 1) * args.rg.pieces + kb * BK / PR;
+              int* cons = args.rg.consumed + (rc & 1) * args.rg.nslot + k % args.rg.nslot;
+              // relaxed: the boxes have already landed (observed through the full barrier);
+              // a release here would also wait for this thread's queued MMAs
+              asm volatile("red.relaxed.gpu.global.add.s32 [%0], 1;" ::"l"(cons) : "memory");
+            }
           }
           __syncwarp();
         }
        }
+      }
+    }
+  } else if (warp >= 6) {
+    // ================= ring rounders (warps 6..13, both CTAs) =================
+    // work items g = (((wave * pieces + piece) * 2 + ring) * RH + part) in
+    // increasing order, item g on CTA g mod gridDim.x; a part overwrites the
+    // slot's previous occupant only after all tpc tiles of that chunk have
+    // loaded it, and adds 1 to the slot's ready count when written
+    if (args.ring) {
+      const Tc2Ring& R = args.rg;
+      const int rt = threadIdx.x - 6 * 32;
+      const int items = R.nwave * R.pieces * 2 * RH;
+      const int q4 = R.ncols / 4;
+      for (int g = blockIdx.x; g < items; g += gridDim.x) {
+        const int h = g % RH, gg = g / RH;             // part h of piece gg
+        const int ring = gg & 1, k = gg >> 1;          // occupancy index of ring `ring`
+        const int piece = k % R.pieces, wave = k / R.pieces;
+        const int chunk = wave * 2 + ring, slot = k % R.nslot;
+        if (rt == 0) t2_spin_ge(R.consumed + ring * R.nslot + slot, (k / R.nslot) * R.tpc);
+        asm volatile("bar.sync 3, %0;" ::"n"(ROUNDERS) : "memory");
+        constexpr int HR = PR / RH;                    // rows of this part
+        float4* dst = reinterpret_cast<float4*>(R.ring[ring] + ((long long)slot * PR + h * HR) * R.ncols);
+        const long long row0 = (long long)chunk * R.chunk_rows + (long long)piece * PR + h * HR;
+        const int valid = min(HR, R.chunk_rows - piece * PR - h * HR);
+        // U independent 16-byte loads in flight per thread, then round and store
+#ifndef TC2_RING_U
+#define TC2_RING_U 16
+#endif
+        constexpr int U = TC2_RING_U;
+        const int total = HR * q4;
+        for (int base = rt; base < total; base += ROUNDERS * U) {
+          float4 v[U];
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int e = base + u * ROUNDERS;
+            const int r = e / q4, c4 = e - r * q4;
+            v[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (e < total && r < valid) v[u] = __ldcs(reinterpret_cast<const float4*>(R.a + (row0 + r) * R.lda) + c4);
+          }
+#pragma unroll
+          for (int u = 0; u < U; ++u) {
+            const int e = base + u * ROUNDERS;
+            if (e < total) {
+              float4 w = v[u];
+              w.x = __uint_as_float(t2_rna(w.x));
+              w.y = __uint_as_float(t2_rna(w.y));
+              w.z = __uint_as_float(t2_rna(w.z));
+              w.w = __uint_as_float(t2_rna(w.w));
+              dst[e] = w;
+            }
+          }
+        }
+        // each writer orders its generic stores before later async-proxy (TMA)
+        // reads; the barrier + the releasing reduction publish the whole part
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        asm volatile("bar.sync 3, %0;" ::"n"(ROUNDERS) : "memory");
+        if (rt == 0)
+          asm volatile("red.release.gpu.global.add.s32 [%0], 1;" ::"l"(R.ready + ring * R.nslot + slot) : "memory");
       }
     }
   } else {
@@ -413,6 +571,90 @@ static bool t2_map_term(CUtensorMap* map, const DTerm<float>& t, bool three_d) {
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+static thread_local Tf32Ring g_ring;
+static thread_local bool g_ring_set = false;
+void set_tf32_ring(const Tf32Ring* r) {
+  g_ring_set = r != nullptr;
+  if (r) g_ring = *r;
+}
+
+// Ring mode for the products [base, base + n): every window a chunk of rows of
+// g_ring.a (same row count), chunk-major with equal tiles per chunk, two chunks
+// per wave of `clusters` CTA pairs.  Returns false when the launch does not fit.
+static bool t2_ring_setup(Tc2Args& a, const DProd<float>* prods, int n, const int* ptiles, int clusters,
+                          cudaStream_t s) {
+  using namespace tc2;
+  const Tf32Ring& G = g_ring;
+  Tc2Ring& R = a.rg;
+  std::memset(&R, 0, sizeof(R));
+  int chunk_rows = -1, first_chunk = -1, last_chunk = -1;
+  for (int i = 0; i < n; ++i) {
+    const DProd<float>& p = prods[i];
+    const DTerm<float>* terms[2] = {&p.s[0], p.kind == kSyrk ? &p.s[0] : &p.t[0]};
+    int rows0 = -1, cols[2];
+    for (int j = 0; j < 2; ++j) {
+      const long long off = terms[j]->p - G.a;
+      if (off < 0 || terms[j]->ld != G.lda) return false;
+      const long long row = off / G.lda, col = off % G.lda;
+      if (chunk_rows < 0) chunk_rows = terms[j]->rows;
+      if (terms[j]->rows != chunk_rows || row % chunk_rows != 0 || col % 32 != 0) return false;
+      if (rows0 >= 0 && row != rows0) return false;
+      rows0 = (int)row;
+      cols[j] = (int)col;
+    }
+    const int c = rows0 / chunk_rows;
+    if (first_chunk < 0) first_chunk = c;
+    if (c < last_chunk || c > last_chunk + 1) {
+      if (last_chunk >= 0) return false;   // chunk-major, consecutive
+    }
+    last_chunk = c;
+    R.chunk[i] = c - first_chunk;
+    R.col_s[i] = cols[0];
+    R.col_t[i] = cols[1];
+  }
+  const int nchunks = last_chunk - first_chunk + 1;
+  long long tpc = -1;
+  for (int c = 0; c < nchunks; ++c) {
+    long long t = 0;
+    for (int i = 0; i < n; ++i) t += R.chunk[i] == c ? ptiles[i] : 0;
+    if (tpc >= 0 && t != tpc) return false;
+    tpc = t;
+  }
+  if (nchunks % 2 != 0 || clusters != 2 * tpc) return false;
+  const int pieces = (chunk_rows + PR - 1) / PR;
+  const long long per_slot = (long long)PR * G.cols;
+#ifndef TC2_RING_SLOTS
+#define TC2_RING_SLOTS 32
+#endif
+  int nslot = TC2_RING_SLOTS;
+  while (nslot > 4 && 2 * nslot * per_slot + 4 * nslot > G.buf_elems) nslot /= 2;
+  if (2 * nslot * per_slot + 4 * nslot > G.buf_elems) return false;
+  R.ring[0] = G.buf;
+  R.ring[1] = G.buf + nslot * per_slot;
+  R.ready = reinterpret_cast<int*>(G.buf + 2 * nslot * per_slot);
+  R.consumed = R.ready + 2 * nslot;
+  R.a = G.a + (long long)first_chunk * chunk_rows * G.lda;
+  R.lda = G.lda;
+  R.chunk_rows = chunk_rows;
+  R.pieces = pieces;
+  R.nslot = nslot;
+  R.nwave = nchunks / 2;
+  R.tpc = (int)tpc;
+  R.ncols = G.cols;
+  for (int r = 0; r < 2; ++r) {
+    DTerm<float> t;
+    t.p = R.ring[r];
+    t.ld = G.cols;
+    t.rows = nslot * PR;
+    t.cols = G.cols;
+    t.sign = 1.0;
+    if (!t2_map_term(&R.rmap[r], t, true)) return false;
+  }
+  if (cudaMemsetAsync(R.ready, 0, 4 * nslot * sizeof(int), s) != cudaSuccess) return false;
+  a.ring = 1;
+  return true;
+}
+
 cudaError_t launch_tf32_2sm(const DProd<float>* prods, int count, double alpha, cudaStream_t s) {
   using namespace tc2;
   static int sms = 0;
@@ -474,6 +716,10 @@ cudaError_t launch_tf32_2sm(const DProd<float>* prods, int count, double alpha, 
 #else
     const int clusters = periodic_workers(ptiles, pkinds, n, total, sms / 2);
 #endif
+    if (g_ring_set) {
+      // the operands are raw fp32: without the ring they would be truncated -- fail loudly
+      if (!three_d || !t2_ring_setup(a, prods + base, n, ptiles, clusters, s)) return cudaErrorNotSupported;
+    }
     prod_tf32_2sm_kernel<<<clusters * 2, THREADS, smem, s>>>(a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;

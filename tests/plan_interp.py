@@ -67,6 +67,8 @@ def run(ops, A, C, alpha=1.0, WS=None, B=None):
                 w += float(op["d"][j]["sign"]) * src[:w.shape[0], :w.shape[1]]
         elif t == OP_FILL:
             _win(bases, op["d"][0], write=True)[...] = 0
+        elif t == OP_ROUND and int(op["accumulate"]) == 2:
+            pass          # L2 rounding ring: the product kernel rounds its operand loads
         elif t == OP_ROUND:   # round-to-nearest (ties away) to TF32, fp32 storage
             src = _win(bases, op["s"][0]).astype(np.float32)
             bits = src.view(np.uint32).astype(np.uint64)

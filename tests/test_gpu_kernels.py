@@ -205,3 +205,30 @@ def test_ata_tf32_tall_skinny():
     assert np.all(np.triu(got, 1) == 0)
     assert O.rel_frobenius_lower(got, O.gram_blas(a)) <= 1e-4
 
+
+
+def test_tf32_l2_ring_matches_rounding_pass():
+    """Single-pass TF32 through the CTA-pair kernel's L2 rounding ring (rounder
+    warps round 96-row pieces of A into two small rings, TMA reads them back)
+    gives bit-for-bit the result of the HBM rounding pass: same cvt.rna
+    rounding, same products in the same order."""
+    import torch
+    from paper_2110_13042_b200 import auto_plan, engine, _native as nat
+    m, n = 1 << 17, 2048
+    g = torch.Generator(device="cuda").manual_seed(5)
+    A = torch.randn((m, n), device="cuda", generator=g)
+    out = []
+    for ring in (True, False):
+        plan = auto_plan.plan_ata_auto(m, n, n, n, auto_plan.AutoParams(tf32_ring=ring), round_tf32=True)
+        assert (int(plan.ops[0]["accumulate"]) == 2) == ring
+        ws = torch.empty(plan.ws_scalars, device="cuda")
+        C = torch.zeros((n, n), device="cuda")
+        for _ in range(2):   # second run: flags and ring reused
+            C.zero_()
+            engine.run_plan(plan, nat.ATA_TF32, A.data_ptr(), A.numel(), C.data_ptr(), C.numel(), 1.0,
+                            ws=ws.data_ptr(), ws_elems=ws.numel())
+        torch.cuda.synchronize()
+        out.append(C.clone())
+    assert torch.equal(out[0], out[1])
+    ref = O.gram_blas(A.double().cpu().numpy())
+    assert O.rel_frobenius_lower(out[0].cpu().numpy(), ref) <= 1e-4

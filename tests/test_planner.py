@@ -259,3 +259,24 @@ def test_bfs_reference_plan_launches():
     d = planner.plan_ata_reference(m, n, n, n, t, workspace_for_ata(m, n, t).level_offsets())
     assert p.mults == d.mults
     assert p.launches * 10 < d.launches
+
+
+def test_tf32_ring_plan_reads_raw_rows():
+    """Single-pass TF32 tall-skinny plans whose chunks fit the CTA-pair kernel's
+    waves use the L2 rounding ring: no HBM rounding pass (ROUND op with
+    accumulate = 2, a small ring scratch), products read A itself; the other
+    shapes keep the rounding pass.  The ring plan computes the same Gram."""
+    m, n = 1 << 17, 2048
+    p = auto_plan.plan_ata_auto(m, n, n, n, auto_plan.AutoParams(), round_tf32=True)
+    assert int(p.ops[0]["type"]) == 7 and int(p.ops[0]["accumulate"]) == 2
+    prods = [o for o in p.ops if int(o["type"]) in (0, 1)]
+    assert prods and all(int(o["s"][0]["base"]) == 0 for o in prods)
+    q = auto_plan.plan_ata_auto(m, n, n, n, auto_plan.AutoParams(tf32_ring=False), round_tf32=True)
+    assert int(q.ops[0]["accumulate"]) == 0 and int(q.ops[1]["s"][0]["base"]) == 2
+    small = auto_plan.plan_ata_auto(6000, 96, 96, 96, auto_plan.AutoParams(leaf_cols=32, min_chunk=512),
+                                    round_tf32=True)
+    assert int(small.ops[0]["accumulate"]) == 0
+    a = np.random.default_rng(9).standard_normal((m, n)).astype(np.float32)[:, :n]
+    c = np.zeros((n, n), dtype=np.float32)
+    plan_interp.run(p.ops, a, c, 1.0, WS=np.full(p.ws_scalars, np.nan, dtype=np.float32))
+    assert O.rel_frobenius_lower(c, O.gram_blas(a)) <= 1e-5

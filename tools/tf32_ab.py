@@ -19,7 +19,9 @@ m, n = 1 << 20, 2048
 torch.manual_seed(0)
 A = torch.randn(m, n, device="cuda")
 C = torch.zeros(n, n, device="cuda")
-plan = auto_plan.plan_ata_auto(m, n, n, n, auto_plan.AutoParams(), round_tf32=True)
+import os
+plan = auto_plan.plan_ata_auto(m, n, n, n, auto_plan.AutoParams(tf32_ring=os.environ.get("TF32_RING", "1") == "1"),
+                               round_tf32=True)
 ws = torch.empty(max(1, plan.ws_scalars), device="cuda")
 run = lambda: engine.run_plan(plan, nat.ATA_TF32, A.data_ptr(), A.numel(), C.data_ptr(), C.numel(), 1.0,
                               ws=ws.data_ptr(), ws_elems=ws.numel())
