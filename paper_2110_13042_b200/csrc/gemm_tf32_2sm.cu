@@ -13,8 +13,10 @@
 // stride 128 B -- so one instruction moves a CTA's [4 panels][BK rows][32 cols]
 // operand box), warp 1 TMEM allocation (both CTAs, cta_group::2) + MMA issue
 // (leader only), warps 2-5 epilogue (each CTA drains its own 128 accumulator
-// rows).  Every wait is bounded: a protocol error traps instead of hanging the
-// GPU.
+// rows), warps 6-13 ring rounders (only with the L2 rounding ring, Tc2Ring:
+// they round raw fp32 rows of A to TF32 into two L2-resident rings the TMA
+// producers read, replacing the HBM rounding pass).  Every wait is bounded: a
+// protocol error traps instead of hanging the GPU.
 //
 // Measured bound (ncu, c5 launch): tensor pipe 94 % active while the executed
 // rate is ~69 % of the smem-resident issue-rate probe -- shared memory serves
