@@ -39,6 +39,9 @@
 
 namespace ata {
 
+#ifndef WS_PRODUCER_SUM
+#define WS_PRODUCER_SUM 0  // 1: the producers add two-term operands in place (the old path)
+#endif
 #ifndef WS_CW
 #define WS_CW 8  // consumer warps: 8 (2 x 4 grid of 64 x 32 warp tiles) or 16 (4 x 4 of 32 x 32)
 #endif
@@ -323,7 +326,11 @@ __global__ void __launch_bounds__(ws64::THREADS, 1)
       const DTerm<double>& T1 = P.t[1];
       const bool vs = vec16_ok(S0) && (ns < 2 || vec16_ok(S1));
       const bool vt = vec16_ok(T0) && (nt < 2 || vec16_ok(T1));
-      const bool comb = (NS == 2 && ns == 2) || (NT == 2 && nt == 2);
+      // two-term operands: both terms land in their own buffers and the
+      // consumers add them while loading fragments (WS_PRODUCER_SUM: the
+      // producers combine in place instead -- measured slower: the in-place
+      // pass throttles the producer ring)
+      const bool comb = WS_PRODUCER_SUM && ((NS == 2 && ns == 2) || (NT == 2 && nt == 2));
       const int KT = (P.m + BK - 1) / BK;
       auto issue = [&](int kt, int ring) {
         double* base = smem + (ring % STAGES) * STAGE;
@@ -423,6 +430,11 @@ __global__ void __launch_bounds__(ws64::THREADS, 1)
 
     const int aoff = wm * (WTM * 8) + g + q * LD;
     const int boff = (same ? 0 : NS * BUF) + wn * (WTN * 8) + g + q * LD;
+    // second operand terms (consumer-side sum): S1 / T1 sit one buffer after S0 / T0
+    const bool two_a = !WS_PRODUCER_SUM && NS == 2 && P.ns == 2;
+    const bool two_b = !WS_PRODUCER_SUM && (same ? two_a : (NT == 2 && P.nt == 2));
+    const double sa = two_a ? P.s[1].sign : 0.0;
+    const double sb = same ? sa : (two_b ? P.t[1].sign : 0.0);
     for (int kt = 0; kt < KT; ++kt, ++kstep) {
       const int s = kstep % STAGES;
       mbar_wait(&full[s], (kstep / STAGES) & 1);
@@ -435,6 +447,14 @@ __global__ void __launch_bounds__(ws64::THREADS, 1)
         for (int r = 0; r < WTM; ++r) a[r] = As[kk * 4 * LD + r * 8];
 #pragma unroll
         for (int c = 0; c < WTN; ++c) b[c] = Bs[kk * 4 * LD + c * 8];
+        if (NS == 2 && two_a) {
+#pragma unroll
+          for (int r = 0; r < WTM; ++r) a[r] = fma(sa, As[BUF + kk * 4 * LD + r * 8], a[r]);
+        }
+        if ((NS == 2 || NT == 2) && two_b) {
+#pragma unroll
+          for (int c = 0; c < WTN; ++c) b[c] = fma(sb, Bs[BUF + kk * 4 * LD + c * 8], b[c]);
+        }
 #pragma unroll
         for (int r = 0; r < WTM; ++r)
 #pragma unroll
