@@ -36,6 +36,7 @@ multiplication count differs (reported as plan.mults).
 """
 from __future__ import annotations
 
+import os
 from dataclasses import dataclass
 
 from . import _native as nat
@@ -442,6 +443,8 @@ def _ringify(plan: Plan, m: int, n: int, lda: int) -> Plan:
     Otherwise the plan is returned unchanged."""
     ops = plan.ops
     if len(ops) < 2 or int(ops[0]["type"]) != nat.OP_ROUND or lda % 4 or n % 32:
+        return plan
+    if os.environ.get("ATA_TF32_TC", "2") != "2":   # only the CTA-pair kernel has the ring
         return plan
     src, dst = ops[0]["s"][0], ops[0]["d"][0]
     if int(dst["ld"]) != lda or int(src["base"]) != nat.BASE_A or int(src["off"]) != 0:

@@ -123,6 +123,7 @@ struct Tf32Ring {
   long long buf_elems;
 };
 void set_tf32_ring(const Tf32Ring* r);  // nullptr clears
+bool tf32_ring_pending();
 template <typename T> cudaError_t launch_postadd7(const EwArgs<T>& a, int accumulate, cudaStream_t s);
 // many independent nodes per launch (elementwise_multi.cu); combo4 nodes: <= 5 outputs
 template <typename T> cudaError_t launch_combo4_multi(const EwArgs<T>* nodes, int count, cudaStream_t s);

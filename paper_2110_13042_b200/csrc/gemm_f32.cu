@@ -336,6 +336,8 @@ cudaError_t launch_batch_f32(const BatchArgs<float>& a, cudaStream_t s, bool spl
   }
   if (ntc > 0) {
     // 2 = CTA-pair tcgen05 kernel (cta_group::2), 1 = single-CTA tcgen05 kernel
+    // (which has no L2 rounding ring: raw operands would be truncated -- refuse)
+    if (use_tc != 2 && tf32_ring_pending()) return cudaErrorNotSupported;
     cudaError_t e = use_tc == 2 ? launch_tf32_2sm(tcp, ntc, a.alpha, s) : launch_tf32_tc(tcp, ntc, a.alpha, s);
     if (e != cudaSuccess) return e;
   }

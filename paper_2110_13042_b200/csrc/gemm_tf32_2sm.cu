@@ -579,6 +579,7 @@ void set_tf32_ring(const Tf32Ring* r) {
   g_ring_set = r != nullptr;
   if (r) g_ring = *r;
 }
+bool tf32_ring_pending() { return g_ring_set; }
 
 // Ring mode for the products [base, base + n): every window a chunk of rows of
 // g_ring.a (same row count), chunk-major with equal tiles per chunk, two chunks
