@@ -13,6 +13,8 @@ or anything the reference accepts (staged through the device).
 """
 from __future__ import annotations
 
+import os
+
 import numpy as np
 
 from . import _native as nat
@@ -132,6 +134,8 @@ def _default_workspace(m, n, threshold, dtype):
 PIPELINE_MIN_BYTES = 1 << 30      # host A at least this large: copy/compute pipeline
 PIPELINE_BLOCK_BYTES = 4 << 30    # ~ bytes of A per row block (PCIe-bound TF32 plans)
 PIPELINE_GEOMETRIC = True         # compute-bound plans: geometric row blocks (_row_blocks)
+PIPELINE_ZERO_C = bool(int(os.environ.get("ATA_PIPE_ZERO_C", "1")))   # device C starts at zero (_pipelined_host_ata)
+_PIPE_CIN: dict = {}   # the staged host-C buffer of the pipeline, one per (device, n, dtype)
 PIPELINE_GEOMETRIC_BLOCKS = 3     # measured (tools/e2e_ab.py): c4 e2e 1718 -> 1683 ms at 3 blocks,
                                   # 4-5 blocks no gain (each block repeats the plan's C-sized work)
 PIPELINE_PCIE_GBS = 50.0          # measured pinned H2D on the box (e2e h2d bytes / time)
@@ -257,29 +261,53 @@ def _pipelined_host_ata(a, c, m, n, alpha, ws, counter, auto_params, precision) 
     wptr = int(wbuf.data_ptr()) if wbuf is not None else 0
     wel = int(wbuf.numel()) if wbuf is not None else 0
     copy.wait_stream(main)                 # dA / dC / scratch are free to overwrite
+    # zero-start C pays one extra add pass but lets block 0 run without C; it
+    # wins with the small first block of geometric row blocks (c4: 1680 -> 1642
+    # ms e2e), not with two equal blocks (c3: 138.1 vs 139.2 ms)
+    zero_start = PIPELINE_ZERO_C and len(blocks) >= 3 and blocks[0][1] * 2 < blocks[1][1]
     events = []
     c_ready = torch.cuda.Event()
+    if zero_start:
+        # C starts at zero on the device, so no block waits for C's upload; the
+        # host C's lower trapezoids cross PCIe after all of A into a zeroed
+        # buffer and are added in (whole square: the diagonal tiles' upper parts
+        # come back as uploaded) just before the last block
+        dC.zero_()
+        key = (str(dev), n, str(c.dtype))
+        dCin = _PIPE_CIN.get(key)
+        if dCin is None:
+            _PIPE_CIN.clear()
+            dCin = _PIPE_CIN[key] = torch.empty((n, n), dtype=c.dtype, device=dev)
+        dCin.zero_()
     with torch.cuda.stream(copy):
         for i, (r0, rows, _) in enumerate(blocks):
             dA[r0:r0 + rows].copy_(a[r0:r0 + rows], non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(copy)
             events.append(ev)
-            if i == 0:
+            if i == 0 and not zero_start:
                 _copy_lower(dC, c, to_device=True)
                 c_ready.record(copy)
+        if zero_start:
+            _copy_lower(dCin, c, to_device=True)
+            c_ready.record(copy)
     mults = 0
     last = len(blocks) - 1
     for i, (r0, rows, plan) in enumerate(blocks):
         main.wait_event(events[i])
         ops = plan.ops
         A_ptr = int(dA.data_ptr()) + r0 * n * es
-        # segment boundaries: the first C writer of block 0 waits for C's upload;
-        # in the last block, C tiles whose last writer has run go home early
+        # segment boundaries: the first C writer of block 0 waits for C's upload
+        # (unless C starts at zero); in the last block, C tiles whose last writer
+        # has run go home early
         cuts, downloads = [], {}
-        if i == 0:
+        if i == 0 and not zero_start:
             cuts.append(_first_c_writer(ops))
         if i == last:
+            if zero_start:
+                main.wait_event(c_ready)
+                engine.run_plan(_add_plan(n), code, int(dCin.data_ptr()), dCin.numel(), int(dC.data_ptr()),
+                                dC.numel(), 1.0)
             sched = _download_schedule(plan, n)
             for cut, tiles in sched:
                 cuts.append(cut)
@@ -290,7 +318,7 @@ def _pipelined_host_ata(a, c, m, n, alpha, ws, counter, auto_params, precision) 
                 engine.run_plan(_SubPlan(ops[prev:cut]), code, A_ptr, rows * n, int(dC.data_ptr()), dC.numel(),
                                 alpha, ws=wptr, ws_elems=wel)
                 prev = cut
-            if i == 0 and cut == cuts[0]:
+            if i == 0 and not zero_start and cut == cuts[0]:
                 main.wait_event(c_ready)
             if cut in downloads:
                 ev = torch.cuda.Event()
@@ -306,6 +334,16 @@ def _pipelined_host_ata(a, c, m, n, alpha, ws, counter, auto_params, precision) 
     if counter is not None:
         counter.add(mults)
     return True
+
+
+def _add_plan(n: int):
+    """One combo4 pass: C = C + A over the whole n x n square."""
+    def build():
+        pb = planner.PlanBuilder("add-square")
+        c = planner.Win(nat.BASE_C, 0, n, n, n)
+        pb.combo4([c, planner.Win(nat.BASE_A, 0, n, n, n)], [(c, (1, 1))])
+        return pb.finish()
+    return engine.cached_plan(("add-square", n), build)
 
 
 def _row_blocks(m: int, n: int, es: int, tensor_rate: bool):
