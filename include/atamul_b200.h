@@ -70,7 +70,12 @@ extern "C" {
  * with accumulate selecting += (into C) or = (into a parent's product buffer). */
 #define ATA_OP_POSTADD7 6
 /* ATA_OP_ROUND: d[0] = round-to-nearest TF32 of s[0] (fp32 only; equal extents).
- * Emitted once per operand by single-pass-TF32 plans before the tcgen05 products. */
+ * Emitted once per operand by single-pass-TF32 plans before the tcgen05 products.
+ * With accumulate = 2 no pass runs: s[0] is the raw operand the next product group
+ * reads directly and d[0] a scratch window (>= 2 * 32 * 192 * cols + 128 scalars)
+ * for the CTA-pair kernel's L2 rounding ring, which rounds the operand pieces on
+ * chip just before its TMA loads them (auto_plan._ringify decides when the group
+ * fits: equal row chunks, two chunks per wave of the persistent grid). */
 #define ATA_OP_ROUND 7
 #define ATA_MAX_TERMS 4
 #define ATA_MAX_DESTS 8
