@@ -136,6 +136,7 @@ PIPELINE_BLOCK_BYTES = 4 << 30    # ~ bytes of A per row block (PCIe-bound TF32 
 PIPELINE_GEOMETRIC = True         # compute-bound plans: geometric row blocks (_row_blocks)
 PIPELINE_ZERO_C = bool(int(os.environ.get("ATA_PIPE_ZERO_C", "1")))   # device C starts at zero (_pipelined_host_ata)
 _PIPE_CIN: dict = {}   # the staged host-C buffer of the pipeline, one per (device, n, dtype)
+PIPELINE_GEOMETRIC_MIN_RATIO = 4.0
 PIPELINE_GEOMETRIC_BLOCKS = 3     # measured (tools/e2e_ab.py): c4 e2e 1718 -> 1683 ms at 3 blocks,
                                   # 4-5 blocks no gain (each block repeats the plan's C-sized work)
 PIPELINE_PCIE_GBS = 50.0          # measured pinned H2D on the box (e2e h2d bytes / time)
@@ -357,7 +358,7 @@ def _row_blocks(m: int, n: int, es: int, tensor_rate: bool):
     (TF32: PCIe bound) up to 8 equal blocks of ~PIPELINE_BLOCK_BYTES."""
     rate = (PIPELINE_TF32_TFLOPS if tensor_rate else PIPELINE_FP64_TFLOPS) * 1e12
     ratio = n * PIPELINE_PCIE_GBS * 1e9 / (rate * es)
-    if PIPELINE_GEOMETRIC and ratio >= 4.0:
+    if PIPELINE_GEOMETRIC and ratio >= PIPELINE_GEOMETRIC_MIN_RATIO:
         g = min(4.0, 0.75 * ratio)
         R = PIPELINE_GEOMETRIC_BLOCKS
         w = [g ** i for i in range(R)]
