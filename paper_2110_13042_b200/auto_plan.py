@@ -327,16 +327,25 @@ class _AutoPlanner:
                 parts[pi].append(P)
         reductions = [(kind, out, sign, accumulate, parts[pi])
                       for pi, (kind, m, n, k, a, b, out, sign, accumulate) in enumerate(prods)]
+        # each product's partials are summed by a chain of combo4 passes; the
+        # chains are independent, so passes of equal depth form one multi-node
+        # launch (depth-major emission, one group per depth)
+        chains = []
         for (kind, out, sign, accumulate, parts) in reductions:
-            srcs = list(parts)
-            first = True
+            srcs, first, chain = list(parts), True, []
             while srcs or first:
                 head = [] if (first and not accumulate) else [out]
                 take = srcs[:4 - len(head)]
                 srcs = srcs[len(take):]
                 coefs = tuple([1] * len(head) + [int(sign)] * len(take))
-                self.pb.combo4(head + take, [(out, coefs)], lower=(kind == "syrk"))
+                chain.append((head + take, [(out, coefs)], kind == "syrk"))
                 first = False
+            chains.append(chain)
+        for d in range(max((len(c) for c in chains), default=0)):
+            level = [c[d] for c in chains if d < len(c)]
+            g = self.pb.new_group() if len(level) > 1 else -1
+            for (srcs, outs, lower) in level:
+                self.pb.combo4(srcs, outs, lower=lower, group=g)
 
     def node(self, a, b, m, n, k, out, sign, accumulate, depth):
         """Depth-first at this node when its breadth-first workspace exceeds the budget."""
