@@ -136,6 +136,7 @@ class _AutoPlanner:
         self.esize = 8
         self.fill_waves = params.fill_waves
         self.tile = (TILE, TILE)
+        self.defer_sums = None   # breadth-first trees: [(depth_left, quadrants, outputs)] emitted by emit()
 
     # ---------------------------------------------------------------- workspace
     def alloc(self, rows: int, cols: int) -> Win:
@@ -156,8 +157,9 @@ class _AutoPlanner:
         return saved_s > self.p.gain * added_s
 
     # --------------------------------------------------------------- Strassen
-    def _sums(self, a: Win, b: Win, m: int, n: int, k: int):
-        """Emit one node's operand sums; return (S[7], T[7], m1, n1, k1)."""
+    def _sums(self, a: Win, b: Win, m: int, n: int, k: int, depth: int = 0):
+        """Emit (or, inside a breadth-first tree, defer) one node's operand
+        sums; return (S[7], T[7], m1, n1, k1)."""
         m1, n1, k1 = _ceil2(m), _ceil2(n), _ceil2(k)
         S, T = [None] * 7, [None] * 7
         for X, coefs, out, cols in ((_quads(a, m1, n1), _S, S, n1), (_quads(b, m1, k1), _T, T, k1)):
@@ -168,13 +170,16 @@ class _AutoPlanner:
                 else:
                     out[i] = self.alloc(m1, cols)
                     outs.append((out[i], coef))
-            self.pb.combo4(X, outs)                      # one pass over the quadrants
+            if self.defer_sums is not None:
+                self.defer_sums.append((depth, X, outs))
+            else:
+                self.pb.combo4(X, outs)                  # one pass over the quadrants
         return S, T, m1, n1, k1
 
-    def _post(self, kids, out: Win, sign: float, n1: int, k1: int, accumulate: bool):
+    def _post(self, kids, out: Win, sign: float, n1: int, k1: int, accumulate: bool, group: int = -1):
         q = [_clip(out, 0, 0, n1, k1), _clip(out, 0, k1, n1, k1), _clip(out, n1, 0, n1, k1),
              _clip(out, n1, k1, n1, k1)]
-        self.pb.postadd7(kids, [(w, sign) for w in q], accumulate)
+        self.pb.postadd7(kids, [(w, sign) for w in q], accumulate, group=group)
 
     def tree(self, a, b, m, n, k, out, sign, accumulate, depth, leaves, posts):
         """Breadth-first: emit sums now (pre-order), collect leaves and post-adds."""
@@ -192,15 +197,23 @@ class _AutoPlanner:
             T = [sorted([(w, float(c)) for w, c in zip(_quads(b, m1, k1), co) if c and w.rows and w.cols],
                         key=lambda t: -t[1]) for co in _T]
             if any(x and x[0][1] < 0 for x in S + T):   # a lone negative term: materialise instead
-                S, T, m1, n1, k1 = self._sums(a, b, m, n, k)
+                S, T, m1, n1, k1 = self._sums(a, b, m, n, k, depth)
         else:
-            S, T, m1, n1, k1 = self._sums(a, b, m, n, k)
+            S, T, m1, n1, k1 = self._sums(a, b, m, n, k, depth)
         kids = [self.alloc(n1, k1) for _ in range(7)]
         for i in range(7):
             self.tree(S[i], T[i], m1, n1, k1, kids[i], 1.0, False, depth - 1, leaves, posts)
-        posts.append((kids, out, sign, n1, k1, accumulate))
+        posts.append((kids, out, sign, n1, k1, accumulate, depth))
 
     def emit(self, leaves, posts, extra=()):
+        # deferred operand sums, shallowest level first; the nodes of one level
+        # are independent and run as one multi-node combo4 launch
+        sums, self.defer_sums = self.defer_sums or [], None
+        for d in sorted({d for d, _, _ in sums}, reverse=True):
+            level = [(X, outs) for dd, X, outs in sums if dd == d]
+            g = self.pb.new_group() if len(level) > 1 else -1
+            for X, outs in level:
+                self.pb.combo4(X, outs, group=g)
         prods = []
         for (m, n, k, a, b, out, sign, accumulate) in leaves:
             if _empty(a) or _empty(b):
@@ -214,8 +227,12 @@ class _AutoPlanner:
         prods = [p for p in prods if p[6].base != nat.BASE_C] + list(extra) + \
             [p for p in prods if p[6].base == nat.BASE_C]
         self.emit_products(prods)
-        for (kids, out, sign, n1, k1, accumulate) in posts:
-            self._post(kids, out, sign, n1, k1, accumulate)
+        # post-additions deepest level first, one multi-node launch per level
+        for d in sorted({p[6] for p in posts}):
+            level = [p for p in posts if p[6] == d]
+            g = self.pb.new_group() if len(level) > 1 else -1
+            for (kids, out, sign, n1, k1, accumulate, _) in level:
+                self._post(kids, out, sign, n1, k1, accumulate, group=g)
 
     def _tiles(self, kind, n, k):
         """Output tiles of one product on the leaf kernel this plan runs on
@@ -353,6 +370,7 @@ class _AutoPlanner:
         if self.ws_top + need <= self.budget or not self.worth_split(m, n, k, depth):
             leaves, posts = [], []
             mark = self.ws_top
+            self.defer_sums = []
             self.tree(a, b, m, n, k, out, sign, accumulate, depth, leaves, posts)
             self.emit(leaves, posts)
             self.ws_top = mark
@@ -418,6 +436,7 @@ class _AutoPlanner:
                            for (a, b, _) in blocks)
                 if need <= self.budget:
                     leaves, posts = [], []
+                    self.defer_sums = []
                     for (a, b, c) in blocks:
                         self.tree(a, b, a.rows, a.cols, b.cols, c, 1.0, True, self.p.max_depth,
                                   leaves, posts)
