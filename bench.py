@@ -465,7 +465,7 @@ def main():
                          "m": int(ops_u[0]["m"]), "n": int(ops_u[0]["n"]), "k": int(ops_u[0]["k"]),
                          "ms": ms, "rate": fl / (ms * 1e-3) / (1e12 if is_prod else 1e9 / A.element_size())})
         json.dump(rows, open(args.dump_units, "w"), indent=0)
-    roofline["secondary"] = {"kernel": "combo4_kernel (Strassen operand sums)", "bound": "hbm",
+    roofline["secondary"] = {"kernel": "Strassen additions (combo4 / postadd7, single- and multi-node launches)", "bound": "hbm",
                              "achieved": ew_gbs, "peak": hbm_peak, "unit": "GB/s",
                              "frac": ew_gbs / hbm_peak if ew_gbs else None,
                              "share_of_step": ew_ms / total_ms if total_ms else None}
