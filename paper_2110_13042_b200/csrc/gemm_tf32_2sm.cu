@@ -60,6 +60,9 @@ constexpr int HALF = 128;                                 // rows of A / cols of
 constexpr int A_BYTES = BK * HALF * 4;                    // 16 KB
 constexpr int B_BYTES = BK * HALF * 4;                    // 16 KB
 constexpr int STAGE_BYTES = A_BYTES + B_BYTES;            // 32 KB per CTA
+#ifndef TC2_RING_HINT
+#define TC2_RING_HINT 0   // bit 0: ring stores evict_last in L2; bit 1: ring TMA loads evict_last
+#endif
 constexpr int THREADS = 448;   // warps 6-13: ring rounders (idle without the ring)
 constexpr int ROUNDERS = THREADS - 192;
 constexpr int TMEM_COLS = 512;
@@ -302,6 +305,23 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
                          "r"(2 * STAGE_BYTES)
                          : "memory");
           if (args.ring) {
+#if TC2_RING_HINT & 2
+            // ring slots are re-read by every tile of the wave: keep them in L2
+            uint64_t pol;
+            asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+            asm volatile(
+                "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                ".L2::cache_hint [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(t2_smem(sa)),
+                "l"(reinterpret_cast<uint64_t>(&args.rg.rmap[rr])), "r"(bar), "r"(0), "r"(ring_row), "r"(rs),
+                "l"(pol)
+                : "memory");
+            asm volatile(
+                "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+                ".L2::cache_hint [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(t2_smem(sb)),
+                "l"(reinterpret_cast<uint64_t>(&args.rg.rmap[rr])), "r"(bar), "r"(0), "r"(ring_row), "r"(rt),
+                "l"(pol)
+                : "memory");
+#else
             asm volatile(
                 "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
                 " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(t2_smem(sa)),
@@ -312,6 +332,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
                 " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(t2_smem(sb)),
                 "l"(reinterpret_cast<uint64_t>(&args.rg.rmap[rr])), "r"(bar), "r"(0), "r"(ring_row), "r"(rt)
                 : "memory");
+#endif
           } else if (args.tma3d) {
             // one box of [HALF/32 panels][BK rows][32 cols] per operand (3-D map)
             asm volatile(
@@ -425,6 +446,10 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
 #endif
         constexpr int U = TC2_RING_U;
         const int total = HR * q4;
+#if TC2_RING_HINT & 1
+        uint64_t pol_last;
+        asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol_last));
+#endif
         for (int base = rt; base < total; base += ROUNDERS * U) {
           float4 v[U];
 #pragma unroll
@@ -443,7 +468,13 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
               w.y = __uint_as_float(t2_rna(w.y));
               w.z = __uint_as_float(t2_rna(w.z));
               w.w = __uint_as_float(t2_rna(w.w));
+#if TC2_RING_HINT & 1
+              asm volatile("st.global.L2::cache_hint.v4.f32 [%0], {%1, %2, %3, %4}, %5;" ::"l"(dst + e), "f"(w.x),
+                           "f"(w.y), "f"(w.z), "f"(w.w), "l"(pol_last)
+                           : "memory");
+#else
               dst[e] = w;
+#endif
             }
           }
         }
