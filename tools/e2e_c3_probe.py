@@ -1,3 +1,5 @@
+"""e2e probe at the c3 shape (16384^2 fp64, pinned host A and C through ata()):
+wall time per geometric-pipeline setting (min ratio, block count)."""
 import os, sys, time, importlib
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
