@@ -136,7 +136,8 @@ PIPELINE_BLOCK_BYTES = 4 << 30    # ~ bytes of A per row block (PCIe-bound TF32 
 PIPELINE_GEOMETRIC = True         # compute-bound plans: geometric row blocks (_row_blocks)
 PIPELINE_ZERO_C = bool(int(os.environ.get("ATA_PIPE_ZERO_C", "1")))   # device C starts at zero (_pipelined_host_ata)
 _PIPE_CIN: dict = {}   # the staged host-C buffer of the pipeline, one per (device, n, dtype)
-PIPELINE_GEOMETRIC_MIN_RATIO = 4.0
+PIPELINE_GEOMETRIC_MIN_RATIO = 4.0    # PIPELINE_GEOMETRIC_BLOCKS geometric blocks from here
+PIPELINE_GEOMETRIC_MIN_RATIO2 = 2.0   # two geometric blocks from here
 PIPELINE_GEOMETRIC_BLOCKS = 3     # measured (tools/e2e_ab.py): c4 e2e 1718 -> 1683 ms at 3 blocks,
                                   # 4-5 blocks no gain (each block repeats the plan's C-sized work)
 PIPELINE_PCIE_GBS = 50.0          # measured pinned H2D on the box (e2e h2d bytes / time)
@@ -354,13 +355,15 @@ def _row_blocks(m: int, n: int, es: int, tensor_rate: bool):
     compute time exceeds the per-row upload time by `ratio` (fp64: ~n / 6400),
     use PIPELINE_GEOMETRIC_BLOCKS blocks growing by g = min(4, 0.75 ratio) -- a
     small first block (short exposed upload), few blocks in total -- when
-    ratio >= 4 (c4; at c3's 2.6 two equal blocks measured better).  Otherwise
-    (TF32: PCIe bound) up to 8 equal blocks of ~PIPELINE_BLOCK_BYTES."""
+    ratio >= 4 (c4), two such blocks when 2 <= ratio < 4 (c3's 2.6: 137.2 -> 135.0 ms
+    against two equal blocks in tools/e2e_c3_probe.py; neutral inside bench.py's c3
+    e2e, 136.0-137.2 ms either way).  Otherwise (TF32: PCIe bound)
+    up to 8 equal blocks of ~PIPELINE_BLOCK_BYTES."""
     rate = (PIPELINE_TF32_TFLOPS if tensor_rate else PIPELINE_FP64_TFLOPS) * 1e12
     ratio = n * PIPELINE_PCIE_GBS * 1e9 / (rate * es)
-    if PIPELINE_GEOMETRIC and ratio >= PIPELINE_GEOMETRIC_MIN_RATIO:
+    if PIPELINE_GEOMETRIC and ratio >= PIPELINE_GEOMETRIC_MIN_RATIO2:
         g = min(4.0, 0.75 * ratio)
-        R = PIPELINE_GEOMETRIC_BLOCKS
+        R = PIPELINE_GEOMETRIC_BLOCKS if ratio >= PIPELINE_GEOMETRIC_MIN_RATIO else 2
         w = [g ** i for i in range(R)]
         cuts = [0]
         for i in range(R - 1):
