@@ -642,7 +642,9 @@ static cudaError_t launch_ws_any(const Args& a, cudaStream_t s) {
   static int bk = -1;
   if (bk < 0) {
     const char* e = std::getenv("ATA_WS_BK");
-    bk = e ? std::atoi(e) : 16;
+    // single-term leaves: 32-row k-blocks x 3 stages (c4 45.71 -> 45.97 TF/s, c3 40.43 ->
+    // 40.54, c2 unchanged); ATA_WS_BK=16 selects 16-row k-blocks x 6 stages
+    bk = e ? std::atoi(e) : 32;
   }
   if (bk == 32) {
     if (ns == 1 && nt == 1) return launch_ws<32, 1, 1>(a, s);
