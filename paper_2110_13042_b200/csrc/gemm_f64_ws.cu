@@ -768,7 +768,10 @@ cudaError_t launch_batch_f64_global(DProdT<double, kNarrowDests>* prods, int cou
   { const char* e = std::getenv("ATA_DBG"); a.dbg = e ? std::atoi(e) : 0; }
   a.gp = reinterpret_cast<const DProdT<double, kNarrowDests>*>(it->second.dev);
   a.tile_prod = reinterpret_cast<const int*>(reinterpret_cast<const unsigned char*>(it->second.dev) + dbytes);
-  if (ns == 1 && nt == 1) return ws_kernel_launch<16, 1, 1>(a, total, s);
+#ifndef WSG_BK
+#define WSG_BK 16   // k-block rows of single-term device-descriptor batches
+#endif
+  if (ns == 1 && nt == 1) return ws_kernel_launch<WSG_BK, 1, 1>(a, total, s);
   if (ns == 2 && nt == 1) return ws_kernel_launch<WS2_BK, 2, 1>(a, total, s);
   if (ns == 1 && nt == 2) return ws_kernel_launch<WS2_BK, 1, 2>(a, total, s);
   return ws_kernel_launch<WS2_BK, 2, 2>(a, total, s);
