@@ -15,9 +15,11 @@ One JSON line on rank 0 (the driver contract):
                buffers (H2D of A and C, D2H of C inside the timed region; N=1)
   roofline   = dominant kernel (the fused product kernel) against the measured
                FP64 DMMA peak (profiles/fp64_peak.txt) or the TF32 peak
-  cpu_baseline = the CPU oracle port of the reference (oracle/atamul_oracle.py,
-               threaded like the reference's AtA-S) on a bounded sample
-``--impl reference`` instead times that CPU port alone (rank 0), same metric.
+  cpu_baseline = the reference's own CPU path (atamul.SharedRunner, installed
+               unmodified into oracle/_ref by oracle/build_ref.sh; the oracle
+               port when absent) on all host cores, on a bounded sample
+``--impl reference`` instead times that CPU path alone (rank 0), same metric
+and config (oracle/cpu_baseline.py).
 """
 from __future__ import annotations
 
@@ -39,9 +41,6 @@ sys.path.insert(0, ROOT)
 FP64_PEAK_TFLOPS = 37.17
 # TF32: cuBLAS TF32 GEMM measured 766-839 TF/s (profiles/fp64_peak.txt); nominal dense 1100.
 TF32_PEAK_TFLOPS = 1112.0   # measured tcgen05 kind::tf32 MN-major issue rate (profiles/fp64_peak.txt)
-CPU_SAMPLE = {"c4": (16384, 4096), "c3": (16384, 4096), "c2": (6001, 4097), "c5": (65536, 2048),
-              "c1": (1024, 1024)}
-
 
 def parse():
     p = argparse.ArgumentParser()
@@ -167,16 +166,19 @@ def launch_units(plan):
         flops = 0
         for op in ops[i:j]:
             ot = int(op["type"])
-            if ot == nat.OP_ROUND and t in (nat.OP_GEMM, nat.OP_SYRK):
-                continue
+            if ot == nat.OP_ROUND and (t in (nat.OP_GEMM, nat.OP_SYRK) or int(op["accumulate"]) == 2):
+                continue    # fused rounding, or the L2 ring's setup (the rounding runs inside the product launch)
             m, n, k = int(op["m"]), int(op["n"]), int(op["k"])
             if ot == nat.OP_GEMM:
                 flops += 2 * m * n * k
             elif ot == nat.OP_SYRK:
                 flops += m * n * (n + 1)
-            else:  # elementwise: algorithmic elements moved (each source read once, each output written)
-                flops += sum(int(r["rows"]) * int(r["cols"]) for r in op["s"][:int(op["ns"])])
-                flops += sum(int(r["rows"]) * int(r["cols"]) for r in op["d"][:int(op["nd"])])
+            else:  # elementwise: algorithmic elements moved (each source read once, each output written;
+                # lower-triangular combo4 passes touch only the lower part of each window)
+                tri = ot == nat.OP_COMBO4 and int(op["accumulate"]) == 1
+                wins = list(op["s"][:int(op["ns"])]) + list(op["d"][:int(op["nd"])])
+                flops += sum(_tri_elems(int(r["rows"]), int(r["cols"])) if tri
+                             else int(r["rows"]) * int(r["cols"]) for r in wins)
         units.append((i, j, t in (nat.OP_GEMM, nat.OP_SYRK), flops))
         i = j
     # the executor splits groups beyond 48 products into several launches
@@ -186,26 +188,37 @@ def launch_units(plan):
     return units, launches
 
 
+def _tri_elems(rows, cols):
+    """Elements of a rows x cols window on or below its diagonal: row r holds min(cols, r + 1)."""
+    if rows <= cols:
+        return rows * (rows + 1) // 2
+    return cols * (cols + 1) // 2 + (rows - cols) * cols
+
+
 def _nprod(ops, i, j):
     from paper_2110_13042_b200 import _native as nat
     return sum(1 for o in ops[i:j] if int(o["type"]) in (nat.OP_GEMM, nat.OP_SYRK))
 
 
 def cpu_sample_rate(cfg_name, cores):
-    """Oracle port (threaded AtA-S restatement) on a bounded sample of the
-    config's own seeded stream; returns (eff GFLOP/s, seconds, sample text)."""
-    from oracle import atamul_oracle as O
-    from paper_2110_13042_b200.measure import CONFIGS, config_matrix
-    r, c = CPU_SAMPLE[cfg_name]
-    a = config_matrix(cfg_name, rows=r)[:, :c]
-    a = np.ascontiguousarray(a)
-    t = 1 << 19
-    t0 = time.perf_counter()
-    O.ata_shared(a, procs=cores, t=t)
-    dt = time.perf_counter() - t0
-    sample = (f"first {r} rows x {c} cols of {cfg_name}'s seeded A, oracle port of the reference "
-              f"AtA-S (threads={cores}, threshold={t})")
-    return r * c * c / dt / 1e9, dt, sample
+    """The reference's own CPU path (oracle/_ref, else the oracle port) on a
+    bounded sample of the config's seeded input (oracle/cpu_baseline.py);
+    returns (eff GFLOP/s, seconds, CpuBaseline)."""
+    from oracle.cpu_baseline import CpuBaseline
+    cb = CpuBaseline(cfg_name, cores)
+    cb.tune()
+    dt = cb.step()
+    return cb.rate(dt), dt, cb
+
+
+METRIC = "AtA effective GFLOP/s (m*n^2/time)"
+
+
+def bench_config(name):
+    """The `config` object of both arms (ours and --impl reference)."""
+    return {"workload": workload_name(name),
+            "l2": "inputs larger than L2 (no flush needed)" if name in ("c3", "c4", "c5")
+            else "inputs smaller than L2; consecutive steps re-read them from L2"}
 
 
 def workload_name(name):
@@ -216,25 +229,31 @@ def workload_name(name):
 
 
 def run_reference(args, world, rank):
+    """--impl reference: the reference's own CPU implementation (unmodified
+    atamul from oracle/_ref: SharedRunner.prepare() untimed, run() timed, as
+    the reference's bench does) on all host cores, each step one bounded
+    sample of the workload (oracle/cpu_baseline.py).  Rank 0 only."""
     if rank != 0:
         return
-    cores = os.cpu_count() or 1
+    from oracle.cpu_baseline import CpuBaseline
     from paper_2110_13042_b200.measure import CONFIGS
     cfg = CONFIGS[args.config]
-    rates = []
-    for i in range(args.warmup + args.steps):
-        rate, dt, sample = cpu_sample_rate(args.config, cores)
-        if i >= args.warmup:
-            rates.append((rate, dt))
-    value = statistics.median(r for r, _ in rates)
-    ms = statistics.median(d for _, d in rates) * 1e3
-    line = {"metric": "AtA effective GFLOP/s (m*n^2/time)", "value": value, "unit": "GFLOP/s",
+    cb = CpuBaseline(args.config)
+    sweep = cb.tune()                       # threshold sweep = the first warm-up work
+    for _ in range(max(0, args.warmup - len(sweep))):
+        cb.step()
+    times = [cb.step() for _ in range(args.steps)]
+    total = sum(times)
+    ms = total / args.steps * 1e3
+    value = cb.rate(total / args.steps)
+    line = {"metric": METRIC, "value": value, "unit": "GFLOP/s",
             "impl": "reference", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64" if cfg["dtype"] == "f64" else "f32", "data": "synthetic",
-            "config": {"workload": workload_name(args.config), "sample": sample},
-            "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": cores, "kind": "port",
-                             "sample": sample},
+            "config": bench_config(args.config),
+            "cpu_baseline": {"value": value, "unit": "GFLOP/s", "cores": cb.cores, "kind": cb.kind,
+                             "sample": cb.describe(),
+                             "threshold_sweep_s": {str(k): v for k, v in sweep.items()}},
             "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -292,9 +311,13 @@ def main():
                                                      if v is not None})
     mloc = r1 - r0
     tuned = None
-    if (args.autotune or (args.config == "c3" and not args.no_autotune)) and threshold == "auto" and f64:
-        from paper_2110_13042_b200 import autotune
-        params = autotune.tune(mloc, n, dev, base=params)
+    # the plan the full-size parity tests check (tests/test_gpu_configs.py)
+    from paper_2110_13042_b200.measure import bench_plan_params
+    base_params = params
+    params, precision = bench_plan_params(args.config, mloc, dev, base=params,
+                                          autotune=True if args.autotune else False if args.no_autotune else None)
+    params = params if params is not None else base_params
+    if params is not base_params:
         tuned = {"leaf_cols": params.leaf_cols, "dmma_tflops": params.dmma_tflops, "hbm_gbs": params.hbm_gbs}
     # what this rank's plan computes: the whole row shard into C, or (task
     # tree) its leaf -- an AtA of a column block or an AtB of two -- into a
@@ -408,10 +431,17 @@ def main():
         e1.record(stream)
         barrier()
     total_ms = e0.elapsed_time(e1)
+    # per-launch events: the timed steps themselves, or -- for a graph-replayed
+    # plan -- K extra eager steps, whose own total is then the share denominator
+    unit_total_ms = total_ms
     if graph is not None:
+        e2, e3 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e2.record(stream)
         for s in range(args.steps):
             step(ev[s])
+        e3.record(stream)
         torch.cuda.synchronize()
+        unit_total_ms = e2.elapsed_time(e3)
     if world > 1:
         import torch.distributed as dist
         t = torch.tensor([total_ms], device=dev)
@@ -420,13 +450,20 @@ def main():
     ms_step = total_ms / args.steps
     value = m * n * n / (ms_step * 1e-3) / 1e9
     # ---- roofline of the dominant kernel (fused product kernel) ----
-    prod_ms, prod_flops, ew_ms, ew_elems = 0.0, 0, 0.0, 0
+    # Elementwise launches whose whole working set fits in L2 (c5's partial-sum
+    # passes read partials the product launch just wrote) are not HBM-bound:
+    # they are reported apart from the HBM roofline of the additions.
+    L2_BYTES = 126 * 2 ** 20
+    prod_ms, prod_flops, ew_ms, ew_elems, l2_ms, l2_elems = 0.0, 0, 0.0, 0, 0.0, 0
     for s in range(args.steps):
         for u, (i, j, is_prod, fl) in enumerate(units):
             d = ev[s][u][0].elapsed_time(ev[s][u][1])
             if is_prod:
                 prod_ms += d
                 prod_flops += fl
+            elif fl * A.element_size() <= L2_BYTES:
+                l2_ms += d
+                l2_elems += fl
             else:
                 ew_ms += d
                 ew_elems += fl
@@ -440,7 +477,10 @@ def main():
                                 "(profiles/fp64_peak.txt); MEASURED_PEAKS.json has no FP64 figure")
                 if f64 else ("measured tcgen05.mma kind::tf32 issue rate on this pool's B200 "
                              "(profiles/fp64_peak.txt; cuBLAS TF32 reaches 766-839)"),
-                "share_of_step": prod_ms / total_ms if total_ms else None,
+                "share_of_step": prod_ms / unit_total_ms if unit_total_ms else None,
+                "share_basis": ("events around every launch of the timed steps" if graph is None else
+                                f"events around every launch of {args.steps} eager steps after the "
+                                f"graph-timed loop ({unit_total_ms / args.steps:.3f} ms/step eager)"),
                 "executed_flops_per_step": prod_flops // args.steps,
                 "algorithmic_flops_per_step": m * n * n,
                 "avg_launch_ms": prod_ms / max(1, prod_launches)}
@@ -468,25 +508,33 @@ def main():
     roofline["secondary"] = {"kernel": "Strassen additions (combo4 / postadd7, single- and multi-node launches)", "bound": "hbm",
                              "achieved": ew_gbs, "peak": hbm_peak, "unit": "GB/s",
                              "frac": ew_gbs / hbm_peak if ew_gbs else None,
-                             "share_of_step": ew_ms / total_ms if total_ms else None}
-    line = {"metric": "AtA effective GFLOP/s (m*n^2/time)", "value": value, "unit": "GFLOP/s",
+                             "share_of_step": ew_ms / unit_total_ms if unit_total_ms else None,
+                             "bytes_counted": "8 or 4 B x (elements of every source window read once + every "
+                                              "output written once; lower-triangular passes count the "
+                                              "lower part only)",
+                             "l2_resident": {"note": "elementwise launches whose working set fits the 126 MB "
+                                                     "L2, excluded from the HBM roofline",
+                                             "share_of_step": l2_ms / unit_total_ms if unit_total_ms else None,
+                                             "gbs": l2_elems * A.element_size() / (l2_ms * 1e-3) / 1e9
+                                             if l2_ms > 0 else None}}
+    line = {"metric": METRIC, "value": value, "unit": "GFLOP/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
             "dtype": "f64" if f64 else "f32 (tf32 products)", "data": "synthetic",
-            "config": {"workload": workload_name(args.config),
-                       "parallelism": (f"task-tree x{world} (reference build_tree_distributed; rank 0 "
-                                       f"leaf {leaf.computation.value} A{leaf.a_region})" if tree is not None
-                                       else f"row-shard x{world}" if world > 1 else "single GPU"),
-                       "l2": "inputs larger than L2 (A is %.1f GB)" % (A.numel() * A.element_size() / 1e9),
-                       "plan": {"kind": plan.kind, "ops": len(plan.ops), "launches": n_launch,
-                                "executed_mults": plan.mults,
-                                "mults_over_classical": plan.mults / (
-                                    mloc * n * (n + 1) / 2 if leaf is None else
-                                    mloc * leaf.a_region.cols * (leaf.a_region.cols + 1) / 2
-                                    if leaf.b_region is None else
-                                    mloc * leaf.a_region.cols * leaf.b_region.cols),
-                                "autotuned": tuned},
-                       "effective_pct_of_peak": value / 1e3 / peak},
+            "config": bench_config(args.config),
+            "parallelism": (f"task-tree x{world} (reference build_tree_distributed; rank 0 "
+                            f"leaf {leaf.computation.value} A{leaf.a_region})" if tree is not None
+                            else f"row-shard x{world}" if world > 1 else "single GPU"),
+            "a_bytes": A.numel() * A.element_size(),
+            "plan": {"kind": plan.kind, "ops": len(plan.ops), "launches": n_launch,
+                     "executed_mults": plan.mults,
+                     "mults_over_classical": plan.mults / (
+                         mloc * n * (n + 1) / 2 if leaf is None else
+                         mloc * leaf.a_region.cols * (leaf.a_region.cols + 1) / 2
+                         if leaf.b_region is None else
+                         mloc * leaf.a_region.cols * leaf.b_region.cols),
+                     "autotuned": tuned},
+            "effective_pct_of_peak": value / 1e3 / peak,
             "roofline": roofline,
             "clocks": clk.summary,
             # our kernels in the timed region, counted by the native executor on a
@@ -523,10 +571,9 @@ def main():
                        "d2h_bytes_per_step": lower_bytes,
                        "ms_per_step": te * 1e3, "api": "paper_2110_13042_b200.ata(host pinned A, C)"}
     if rank == 0 and world == 1 and not args.no_cpu:
-        cores = os.cpu_count() or 1
-        rate, dt, sample = cpu_sample_rate(args.config, cores)
-        line["cpu_baseline"] = {"value": rate, "unit": "GFLOP/s", "cores": cores, "kind": "port",
-                                "sample": sample, "seconds": dt}
+        rate, dt, cb = cpu_sample_rate(args.config, None)
+        line["cpu_baseline"] = {"value": rate, "unit": "GFLOP/s", "cores": cb.cores, "kind": cb.kind,
+                                "sample": cb.describe(), "seconds": dt}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

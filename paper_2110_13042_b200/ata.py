@@ -87,7 +87,7 @@ def ata(A, C, alpha=1.0, threshold=DEFAULT_THRESHOLD, ws: StrassenWorkspace | No
     plan = _plan_for(m, n, A_.ld, C_.ld, threshold, ws, auto_params,
                      round_tf32=(precision == "tf32" and C_.t.dtype == torch.float32))
     extra = plan.ws_scalars if (threshold == AUTO or not engine.reference_dfs()) else 0
-    wbuf = ws.ensure(C_.t.device, extra=extra) if plan.ws_scalars > 0 else None
+    wbuf = ws.ensure(C_.t.device, extra=extra, dtype=C_.t.dtype) if plan.ws_scalars > 0 else None
     args = (plan, nat.dtype_code(C_.t.dtype, precision), A_.ptr, A_.elems, C_.ptr, C_.elems, alpha)
     kw = dict(ws=int(wbuf.data_ptr()) if wbuf is not None else 0,
               ws_elems=int(wbuf.numel()) if wbuf is not None else 0)
@@ -259,10 +259,9 @@ def _pipelined_host_ata(a, c, m, n, alpha, ws, counter, auto_params, precision) 
     need = max(p.ws_scalars for (_, _, p) in blocks)
     if ws is None:
         ws = workspace_for_ata(m, n, AUTO, dtype=c.dtype)
-    wbuf = ws.ensure(dev, extra=need) if need > 0 else None
+    wbuf = ws.ensure(dev, extra=need, dtype=c.dtype) if need > 0 else None
     wptr = int(wbuf.data_ptr()) if wbuf is not None else 0
     wel = int(wbuf.numel()) if wbuf is not None else 0
-    copy.wait_stream(main)                 # dA / dC / scratch are free to overwrite
     # zero-start C pays one extra add pass but lets block 0 run without C; it
     # wins with the small first block of geometric row blocks (c4: 1680 -> 1642
     # ms e2e), not with two equal blocks (c3: 138.1 vs 139.2 ms)
@@ -281,6 +280,9 @@ def _pipelined_host_ata(a, c, m, n, alpha, ws, counter, auto_params, precision) 
             _PIPE_CIN.clear()
             dCin = _PIPE_CIN[key] = torch.empty((n, n), dtype=c.dtype, device=dev)
         dCin.zero_()
+    # dA / dC / scratch are free to overwrite, and the zero fills above are
+    # ordered before the copy stream's uploads into dCin
+    copy.wait_stream(main)
     with torch.cuda.stream(copy):
         for i, (r0, rows, _) in enumerate(blocks):
             dA[r0:r0 + rows].copy_(a[r0:r0 + rows], non_blocking=True)

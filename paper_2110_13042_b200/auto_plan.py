@@ -405,6 +405,13 @@ class _AutoPlanner:
             A = R
             self.ws_floor = self.ws_top
         self.budget = int(self.p.ws_budget_gb * 1e9 / 8)
+        self.ata_win(A, C)
+
+    def ata_win(self, A: Win, C: Win):
+        """lower(C) += A^T A for an A window (m x n) and the n x n C window at
+        its diagonal position: the column recursion of ata() on windows (the
+        multi-GPU unit planner runs it on row chunks and column halves)."""
+        m, n = A.rows, A.cols
         # the diagonal SYRK leaves depend only on A: they join the first
         # breadth-first leaf group (more tiles per launch), else run last
         diag, level = [], [(0, n)]
@@ -557,3 +564,175 @@ def plan_gemm_auto(m: int, n: int, k: int, lda: int, ldb: int, ldc: int,
     plan = ap.pb.finish()
     plan.ws_scalars = max(plan.ws_scalars, ap.ws_peak)
     return plan
+
+
+# --------------------------------------------------------------------------
+# Multi-GPU "units" partition (north star: the independent AtA sub-problems
+# and the seven Strassen sub-products of the top level on different ranks).
+#
+# The top level of plan_ata_auto is: C11 += A_L^T A_L, C22 += A_R^T A_R (two
+# AtA units, A_L / A_R the column halves) and C21 += A_R^T A_L, a Strassen
+# node whose seven products P_i = S_i^T T_i (S_i, T_i signed sums of the
+# quadrants of A_R and A_L, contraction = the top half's m1 rows) are
+# combined into the four quadrants of C21 (strassen.py:234-275).  All nine
+# units are sums over contraction rows, so any row range of a unit is an
+# independent piece of work whose result simply adds into C: ranks receive
+# contiguous row ranges of the unit sequence, balanced by the planner's own
+# executed-multiplication counts, and a sum of the ranks' C triangles (one
+# NCCL reduce) combines them -- each P_i is added with its sign into its C21
+# quadrants on the rank that computes it.
+
+UNITS = ("ata_l", "ata_r", "p1", "p2", "p3", "p4", "p5", "p6", "p7")
+# destinations of P_i among the C21 quadrants (0 = C11, 1 = C12, 2 = C21,
+# 3 = C22) with signs: C11 = P1+P4-P5+P7, C12 = P3+P5, C21 = P2+P4,
+# C22 = P1-P2+P3+P6
+_PDEST = [((0, 1.0), (3, 1.0)), ((2, 1.0), (3, -1.0)), ((1, 1.0), (3, 1.0)), ((0, 1.0), (2, 1.0)),
+          ((0, -1.0), (1, 1.0)), ((3, 1.0),), ((0, 1.0),)]
+
+
+def unit_geometry(m: int, n: int):
+    """(n1, n2, m1): column halves of the top AtA level (floor first, as
+    plan_ata_auto) and the ceil half of the contraction of the C21 node."""
+    n1 = n // 2
+    return n1, n - n1, _ceil2(m)
+
+
+def unit_rows(unit: str, m: int, n: int) -> int:
+    """Contraction rows of a unit: m for the AtA units, m1 for the products."""
+    return m if unit in ("ata_l", "ata_r") else unit_geometry(m, n)[2]
+
+
+def a_rows_needed(segments, m: int, n: int):
+    """Row ranges of A a rank's segments read (a product's row r of the top
+    half pairs with row m1 + r of the bottom half)."""
+    m1 = unit_geometry(m, n)[2]
+    out = []
+    for (u, r0, r1) in segments:
+        out.append((r0, r1))
+        if u not in ("ata_l", "ata_r"):
+            lo, hi = m1 + r0, min(m, m1 + r1)
+            if lo < hi:
+                out.append((lo, hi))
+    out.sort()
+    merged = []
+    for lo, hi in out:
+        if merged and lo <= merged[-1][1]:
+            merged[-1] = (merged[-1][0], max(merged[-1][1], hi))
+        else:
+            merged.append((lo, hi))
+    return merged
+
+
+class _UnitPlanner(_AutoPlanner):
+    def segment(self, unit: str, r0: int, r1: int, A: Win, C: Win, m: int, n: int):
+        n1, n2, m1 = unit_geometry(m, n)
+        rows = r1 - r0
+        if rows <= 0:
+            return
+        mark = self.ws_top
+        if unit == "ata_l":
+            self.ata_win(A.sub(r0, 0, rows, n1), C.sub(0, 0, n1, n1))
+        elif unit == "ata_r":
+            self.ata_win(A.sub(r0, n1, rows, n2), C.sub(n1, n1, n2, n2))
+        else:
+            i = UNITS.index(unit) - 2
+            a, b = A.sub(0, n1, m, n2), A.sub(0, 0, m, n1)          # C21 += A_R^T A_L
+            out = C.sub(n1, 0, n2, n1)
+            q1, k1 = _ceil2(n2), _ceil2(n1)
+            X = [_clip(w, r0, 0, rows, w.cols) for w in _quads(a, m1, q1)]
+            Y = [_clip(w, r0, 0, rows, w.cols) for w in _quads(b, m1, k1)]
+            S = self._operand(X, _S[i], rows, q1)
+            T = self._operand(Y, _T[i], rows, k1)
+            outq = [_clip(out, 0, 0, q1, k1), _clip(out, 0, k1, q1, k1), _clip(out, q1, 0, q1, k1),
+                    _clip(out, q1, k1, q1, k1)]
+            dests = [(outq[d], sg) for (d, sg) in _PDEST[i] if outq[d].rows and outq[d].cols]
+            if dests and not (_empty(S) or _empty(T)):
+                depth = self.p.max_depth - 1
+                if len(dests) == 1:
+                    self.node(S, T, rows, q1, k1, dests[0][0], dests[0][1], True, depth)
+                else:
+                    P = self.alloc(q1, k1)
+                    self.node(S, T, rows, q1, k1, P, 1.0, False, depth)
+                    self.pb.update(P, dests)
+        self.ws_top = mark
+
+    def _operand(self, quads, coef, rows, cols):
+        """S_i / T_i over the segment's rows: a quadrant view, or one combo4
+        pass writing the signed sum into scratch."""
+        if sorted(coef) == [0, 0, 0, 1]:
+            return quads[coef.index(1)]
+        buf = self.alloc(rows, cols)
+        self.pb.combo4(quads, [(buf, coef)])
+        return buf
+
+
+def plan_units(segments, m: int, n: int, lda: int, ldc: int, params: AutoParams = AutoParams()) -> Plan:
+    """One rank's plan of the units partition: lower(C) += the rank's
+    segments [(unit, r0, r1)] (contraction rows [r0, r1) of a UNITS entry).
+    Over all ranks' segments the sum is lower(A^T A)."""
+    if m < 2 or n < 2:
+        raise ShapeMismatchError("shape mismatch: the units partition needs m, n >= 2")
+    up = _UnitPlanner(params)
+    up.budget = int(params.ws_budget_gb * 1e9 / 8)
+    A = Win(nat.BASE_A, 0, lda, m, n)
+    C = Win(nat.BASE_C, 0, ldc, n, n)
+    for (u, r0, r1) in segments:
+        if u not in UNITS:
+            raise ValueError(f"unknown unit {u!r}")
+        up.segment(u, r0, r1, A, C, m, n)
+    plan = up.pb.finish()
+    plan.ws_scalars = max(plan.ws_scalars, up.ws_peak)
+    return plan
+
+
+def unit_costs(m: int, n: int, params: AutoParams = AutoParams()):
+    """Executed multiplications per contraction row of each unit (the
+    planner's own count at the unit's full row extent)."""
+    out = {}
+    for u in UNITS:
+        rows = unit_rows(u, m, n)
+        p = plan_units([(u, 0, rows)], m, n, n, n, params)
+        out[u] = p.mults / rows
+    return out
+
+
+def partition_units(m: int, n: int, procs: int, params: AutoParams = AutoParams(), align: int = 256,
+                    costs=None):
+    """Split the unit sequence (UNITS order, each unit's rows in order) into
+    `procs` contiguous pieces of equal executed multiplications.  Each cut is
+    rounded to `align` rows and snapped to the unit's edge when it would leave
+    a piece shorter than `align` rows.  Returns per rank [(unit, r0, r1)]."""
+    costs = costs or unit_costs(m, n, params)
+    ext = [(u, unit_rows(u, m, n), costs[u]) for u in UNITS]
+    total = sum(rows * c for (_, rows, c) in ext)
+
+    def position(work):
+        """(unit index, row) where the cumulative work reaches `work`."""
+        before = 0.0
+        for ui, (u, rows, c) in enumerate(ext):
+            span = rows * c
+            if work < before + span:
+                r = int(round((work - before) / c / align)) * align
+                if r < align:
+                    return (ui, 0)
+                if rows - r < align:
+                    return (ui + 1, 0)
+                return (ui, r)
+            before += span
+        return (len(ext), 0)
+
+    cuts = [(0, 0)] + [position(total * j / procs) for j in range(1, procs)] + [(len(ext), 0)]
+    for j in range(1, len(cuts)):                       # monotone after rounding
+        cuts[j] = max(cuts[j], cuts[j - 1])
+    ranks = []
+    for (u0, r0), (u1, r1) in zip(cuts, cuts[1:]):
+        segs = []
+        ui, r = u0, r0
+        while (ui, r) < (u1, r1):
+            u, rows, _ = ext[ui]
+            end = r1 if ui == u1 else rows
+            if end > r:
+                segs.append((u, r, end))
+            ui, r = ui + 1, 0
+        ranks.append(segs)
+    return ranks

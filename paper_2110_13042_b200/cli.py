@@ -111,47 +111,12 @@ def validate(args) -> None:
         args.m = args.n
 
 
-def _shared_leaf(task, a, C, threshold, counter, ws):
-    """One leaf of the shared tree, written into its own C cells; `ws` holds
-    this leaf's private workspaces (leaves run concurrently on their own
-    streams, so they never share scratch)."""
-    from .ata import ata, workspace_for_ata
-    from .strassen import fast_strassen, workspace_for
-    ar, cr = task.a_region, task.c_region
-    A = a[ar.row_offset:ar.row_offset + ar.rows, ar.col_offset:ar.col_offset + ar.cols]
-    Cb = C[cr.row_offset:cr.row_offset + cr.rows, cr.col_offset:cr.col_offset + cr.cols]
-    dt = np.float64 if C.dtype.itemsize == 8 else np.float32
-
-    def gemm(X, Y, out):
-        key = ("gemm", tuple(X.shape), int(Y.shape[1]))
-        if key not in ws:
-            ws[key] = workspace_for(int(X.shape[0]), int(X.shape[1]), int(Y.shape[1]), threshold, dt) \
-                if threshold != "auto" else workspace_for_ata(1, 1, "auto", dt)
-        fast_strassen(X, Y, out, 1.0, ws=ws[key], threshold=threshold, counter=counter)
-
-    if task.b_region is not None:
-        br = task.b_region
-        gemm(A, a[br.row_offset:br.row_offset + br.rows, br.col_offset:br.col_offset + br.cols], Cb)
-        return
-    # stripe: result rows [s, e) of the prefix Gram -- a rectangle left of
-    # the diagonal block plus the block's lower triangle
-    e = ar.cols
-    s = e - cr.rows
-    if s > 0:
-        gemm(A[:, s:], A[:, :s], Cb[:, :s])
-    key = ("ata", int(A.shape[0]), e - s)
-    if key not in ws:
-        ws[key] = workspace_for_ata(int(A.shape[0]), e - s, threshold, dt)
-    ata(A[:, s:], Cb[:, s:], 1.0, threshold, ws=ws[key], counter=counter)
-
-
 def run_bench(args) -> list[BenchRecord]:
     import torch
     from . import dist as pdist
     from .ata import ata
     from .matrix import MultCounter, mirror_lower_to_upper, naive_syrk_lower, read_matrix, write_matrix
     from .measure import check_tolerance, effective_gflops, gen_matrix
-    from .tasktree import build_tree_shared, leaf_task
 
     dtype = np.float64 if args.dtype == "f64" else np.float32
     if args.in_path:
@@ -177,18 +142,15 @@ def run_bench(args) -> list[BenchRecord]:
         def compute(C):
             naive_syrk_lower(a, C, 1.0, counter)
     elif args.mode == "shared":
-        tree = build_tree_shared(procs, args.m, n)
-        streams = [torch.cuda.Stream() for _ in range(procs)]
-        leaf_ws = [dict() for _ in range(procs)]
+        # the reference's bench drives SharedRunner (bench.py:170-176): leaves
+        # of the shared tree on concurrent CUDA streams (shared.py)
+        from .shared import SharedRunner
+        runner = SharedRunner(a, procs, thr)
+        runner.counters = [counter] * procs
+        runner.prepare()
 
         def compute(C):
-            cur = torch.cuda.current_stream()
-            for q in range(procs):
-                streams[q].wait_stream(cur)
-                with torch.cuda.stream(streams[q]):
-                    _shared_leaf(leaf_task(tree, q), a, C, thr, counter, leaf_ws[q])
-            for st in streams:
-                cur.wait_stream(st)
+            runner.run_into(C, mirror=False)
     else:   # dist
         leaf_thr = (1 << 62) if args.leaf_kernel == "naive" else thr
 

@@ -1,5 +1,6 @@
 // Shared device-side descriptors and helpers for the AtA kernels (sm_100a).
 #pragma once
+#include <atomic>
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -174,6 +175,38 @@ inline int periodic_workers(const int* tiles, const int* kinds, int n, long long
     return w * 10 >= (long long)slots * 9 ? (int)w : slots;
   }
   return slots;
+}
+
+// Host-side launch helpers.  The SM count and a kernel's max-dynamic-shared-
+// memory attribute belong to a device (context), so both are cached per device
+// ordinal: a process that drives several GPUs gets the attribute set on each.
+inline int current_device() {
+  int d = 0;
+  cudaGetDevice(&d);
+  return d;
+}
+
+inline int sm_count() {
+  static std::atomic<int> cache[64];
+  const int d = current_device();
+  int n = (d >= 0 && d < 64) ? cache[d].load(std::memory_order_relaxed) : 0;
+  if (n > 0) return n;
+  cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, d);
+  if (n <= 0) n = 148;
+  if (d >= 0 && d < 64) cache[d].store(n, std::memory_order_relaxed);
+  return n;
+}
+
+// `done` is one bit per device ordinal, owned by the caller (one static per
+// kernel instantiation); setting the attribute twice is harmless.
+template <typename Kernel>
+inline cudaError_t set_smem_attr(Kernel kern, size_t smem, std::atomic<unsigned long long>& done) {
+  const int d = current_device();
+  const unsigned long long bit = (d >= 0 && d < 64) ? (1ull << d) : 0ull;
+  if (bit && (done.load(std::memory_order_acquire) & bit)) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e == cudaSuccess && bit) done.fetch_or(bit, std::memory_order_release);
+  return e;
 }
 
 }  // namespace ata

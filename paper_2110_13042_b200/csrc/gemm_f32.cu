@@ -278,12 +278,8 @@ static cudaError_t launch_cfg_f32(const BatchArgs<float>& a, cudaStream_t s) {
   using namespace f32cfg;
   const size_t smem = (size_t)STAGES * (NS + NT) * BK * LDS * sizeof(float);
   auto kern = prod_f32_kernel<NS, NT, STAGES, SPLIT>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  static std::atomic<unsigned long long> attr_set{0};
+  if (cudaError_t e = ata::set_smem_attr(kern, smem, attr_set); e != cudaSuccess) return e;
   kern<<<a.total_tiles, THREADS, smem, s>>>(a);
   return cudaGetLastError();
 }

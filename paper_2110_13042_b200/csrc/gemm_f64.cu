@@ -282,12 +282,8 @@ static cudaError_t launch_cfg(BatchArgs<double> a, cudaStream_t s) {
   const size_t smem =
       (size_t)stages_for<CF, NS, NT>() * (NS * CF::BK * CF::LDA + NT * CF::BK * CF::LDB) * sizeof(double);
   auto kern = prod_f64_kernel<CF, NS, NT>;
-  static bool attr_set = false;  // per-instantiation; idempotent
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  static std::atomic<unsigned long long> attr_set{0};  // per instantiation, per device
+  if (cudaError_t e = ata::set_smem_attr(kern, smem, attr_set); e != cudaSuccess) return e;
   kern<<<a.total_tiles, CF::THREADS, smem, s>>>(a);
   return cudaGetLastError();
 }

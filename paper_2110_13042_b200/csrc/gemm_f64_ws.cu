@@ -538,16 +538,7 @@ __global__ void __launch_bounds__(ws64::THREADS, 1)
 }
 
 
-static int num_sms() {
-  static int n = 0;
-  if (n == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
-    if (n <= 0) n = 148;
-  }
-  return n;
-}
+static int num_sms() { return ata::sm_count(); }
 
 template <int BK, int NS, int NT, typename Args>
 static cudaError_t ws_kernel_launch(const Args& a, long long total, cudaStream_t s) {
@@ -559,12 +550,8 @@ static cudaError_t ws_kernel_launch(const Args& a, long long total, cudaStream_t
   const size_t smem = (size_t)STAGES * STAGE_BYTES + (2 * STAGES + 2 * TSLOTS) * sizeof(uint64_t) +
                       (TSLOTS + 2) * sizeof(int);
   auto kern = prod_f64_ws_kernel<BK, NS, NT, STAGES, Args>;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr_set = true;
-  }
+  static std::atomic<unsigned long long> attr_set{0};
+  if (cudaError_t e = ata::set_smem_attr(kern, smem, attr_set); e != cudaSuccess) return e;
   const int grid = (int)(total < num_sms() ? total : num_sms());
   kern<<<grid, THREADS, smem, s>>>(a);
   return cudaGetLastError();
@@ -666,6 +653,9 @@ struct DescEntry {
   std::vector<unsigned char> host;  // exact bytes (descriptors + tile table) for hit checks
   void* dev = nullptr;
   uint64_t last_use = 0;
+  // used by a launch recorded into a CUDA graph: the graph keeps the device
+  // pointer for as long as it lives, so the entry is never evicted
+  bool pinned = false;
 };
 struct DescCache {
   std::unordered_map<uint64_t, DescEntry> map;
@@ -723,21 +713,24 @@ cudaError_t launch_batch_f64_global(DProdT<double, kNarrowDests>* prods, int cou
   DescCache& cache = desc_cache();
   const uint64_t key = blob_hash(blob.data(), blob.size());
   auto it = cache.map.find(key);
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cs);
+  const bool capturing = cs != cudaStreamCaptureStatusNone;
   if (it == cache.map.end() || it->second.host != blob) {
-    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-    cudaStreamIsCapturing(s, &cs);
-    if (cs != cudaStreamCaptureStatusNone) return cudaErrorNotReady;  // no uploads inside a capture
+    if (capturing) return cudaErrorNotReady;  // no uploads inside a capture
     if (it != cache.map.end()) {  // hash collision: replace
+      if (it->second.pinned) return cudaErrorNotReady;  // a live graph holds the colliding entry: narrow batches
       cudaFree(it->second.dev);
       cache.bytes -= it->second.host.size();
       cache.map.erase(it);
     }
-    // evict least recently used entries beyond 256 MB
-    while (cache.bytes + blob.size() > (256u << 20) && !cache.map.empty()) {
-      auto lru = cache.map.begin();
+    // evict least recently used unpinned entries beyond 256 MB
+    while (cache.bytes + blob.size() > (256u << 20)) {
+      auto lru = cache.map.end();
       for (auto j = cache.map.begin(); j != cache.map.end(); ++j)
-        if (j->second.last_use < lru->second.last_use) lru = j;
-      cudaStreamSynchronize(s);  // the evicted buffer may be in use by queued work
+        if (!j->second.pinned && (lru == cache.map.end() || j->second.last_use < lru->second.last_use)) lru = j;
+      if (lru == cache.map.end()) break;  // everything left is held by graphs
+      cudaDeviceSynchronize();  // the evicted buffer may be in use by queued work on any stream  // the evicted buffer may be in use by queued work
       cudaFree(lru->second.dev);
       cache.bytes -= lru->second.host.size();
       cache.map.erase(lru);
@@ -752,6 +745,7 @@ cudaError_t launch_batch_f64_global(DProdT<double, kNarrowDests>* prods, int cou
     it = cache.map.emplace(key, std::move(ent)).first;
   }
   it->second.last_use = ++cache.clock;
+  if (capturing) it->second.pinned = true;
   BatchArgsGlobal64 a;
   std::memset(&a, 0, sizeof(a));
   a.count = count;

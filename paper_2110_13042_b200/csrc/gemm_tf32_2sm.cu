@@ -691,19 +691,10 @@ static bool t2_ring_setup(Tc2Args& a, const DProd<float>* prods, int n, const in
 
 cudaError_t launch_tf32_2sm(const DProd<float>* prods, int count, double alpha, cudaStream_t s) {
   using namespace tc2;
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int sms = ata::sm_count();
   const size_t smem = (size_t)STAGES * STAGE_BYTES + 1024 + 256;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(prod_tf32_2sm_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<unsigned long long> attr{0};
+  if (cudaError_t e = ata::set_smem_attr(prod_tf32_2sm_kernel, smem, attr); e != cudaSuccess) return e;
   for (int base = 0; base < count; base += kMax) {
     Tc2Args a;
     std::memset(&a, 0, sizeof(a));
@@ -754,8 +745,29 @@ cudaError_t launch_tf32_2sm(const DProd<float>* prods, int count, double alpha, 
       // the operands are raw fp32: without the ring they would be truncated -- fail loudly
       if (!three_d || !t2_ring_setup(a, prods + base, n, ptiles, clusters, s)) return cudaErrorNotSupported;
     }
-    prod_tf32_2sm_kernel<<<clusters * 2, THREADS, smem, s>>>(a);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e;
+    if (a.ring) {
+      // The L2 ring's static schedule has CTAs waiting on one another's
+      // rounding items and slot releases, so every CTA of the grid must be
+      // resident at once: a cooperative launch guarantees it (the launch waits
+      // for the SMs, or fails with cudaErrorCooperativeLaunchTooLarge, instead
+      // of leaving resident CTAs spinning on CTAs that never start).
+      cudaLaunchConfig_t cfg;
+      std::memset(&cfg, 0, sizeof(cfg));
+      cfg.gridDim = dim3(clusters * 2, 1, 1);
+      cfg.blockDim = dim3(THREADS, 1, 1);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = s;
+      cudaLaunchAttribute attrs[1];
+      attrs[0].id = cudaLaunchAttributeCooperative;
+      attrs[0].val.cooperative = 1;
+      cfg.attrs = attrs;
+      cfg.numAttrs = 1;
+      e = cudaLaunchKernelEx(&cfg, prod_tf32_2sm_kernel, a);
+    } else {
+      prod_tf32_2sm_kernel<<<clusters * 2, THREADS, smem, s>>>(a);
+      e = cudaGetLastError();
+    }
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;

@@ -384,19 +384,10 @@ bool tc_eligible(const DProd<float>& p) {
 
 cudaError_t launch_tf32_tc(const DProd<float>* prods, int count, double alpha, cudaStream_t s) {
   using namespace tc;
-  static int sms = 0;
-  if (sms == 0) {
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  }
+  const int sms = ata::sm_count();
   const size_t smem = (size_t)STAGES * STAGE_BYTES + 1024 + 256;
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(prod_tf32_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
+  static std::atomic<unsigned long long> attr{0};
+  if (cudaError_t e = ata::set_smem_attr(prod_tf32_tc_kernel, smem, attr); e != cudaSuccess) return e;
   for (int base = 0; base < count; base += kMax) {
     TcArgs a;
     std::memset(&a, 0, sizeof(a));

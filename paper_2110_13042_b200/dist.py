@@ -280,3 +280,116 @@ def tree_rows(tree, rank: int):
     from .tasktree import leaf_task
     t = leaf_task(tree, rank)
     return t.a_region.row_offset, t.a_region.row_offset + t.a_region.rows
+
+
+# --------------------------------------------------------------------------
+# Units partition (north star): the top level's two AtA sub-problems and the
+# seven Strassen products of its C21 node as row-range segments on the ranks
+# (auto_plan.partition_units / plan_units), combined region by region.
+#
+# A rank's segments write only some of the three regions of lower(C): C11
+# (lower triangle of the left diagonal block; "ata_l" segments), C22 (the
+# right diagonal block; "ata_r") and C21 (the rectangle; every product
+# segment, each adding its signed P_i into its C21 quadrants).  Each region
+# is summed to the root with one NCCL reduce over the group of ranks that
+# wrote it (plus the root): packed triangles for C11/C22, the rectangle for
+# C21.  Row shards reduce the whole packed triangle from every rank; here a
+# rank ships only what it computed.
+
+REGIONS = ("c11", "c22", "c21")
+
+
+def unit_regions(segments):
+    """The C regions a rank's segments write."""
+    out = set()
+    for (u, _, _) in segments:
+        out.add("c11" if u == "ata_l" else "c22" if u == "ata_r" else "c21")
+    return out
+
+
+def region_members(all_segments, root: int = 0):
+    """Per region, the sorted ranks that take part in its reduce."""
+    mem = {r: {root} for r in REGIONS}
+    for rank, segs in enumerate(all_segments):
+        for r in unit_regions(segs):
+            mem[r].add(rank)
+    return {r: sorted(v) for r, v in mem.items()}
+
+
+def region_windows(C, n: int):
+    """(kind, block view) of each region of an n x n C."""
+    n1 = n // 2
+    return {"c11": ("packed", C[:n1, :n1]), "c22": ("packed", C[n1:, n1:]), "c21": ("rect", C[n1:, :n1])}
+
+
+def make_region_groups(all_segments, root: int = 0):
+    """torch.distributed groups of the region reduces (every rank must call
+    this, in the same order: new_group is collective)."""
+    import torch.distributed as dist
+    mem = region_members(all_segments, root)
+    world = dist.get_world_size()
+    groups = {}
+    for r in REGIONS:
+        ranks = mem[r]
+        groups[r] = (None if len(ranks) == world else dist.new_group(ranks)) if len(ranks) > 1 else "solo"
+    return groups, mem
+
+
+def reduce_regions(C, n: int, rank: int, groups, members, ops, root: int = 0, bufs=None):
+    """Sum each region's contributions into the root's C: pack (triangles) or
+    copy (rectangle) this rank's block, NCCL reduce(SUM) to the root over the
+    region's group, and the root writes the sum back.  Regions in a fixed
+    order on every rank (no cross-communicator deadlock)."""
+    import torch.distributed as dist
+    wins = region_windows(C, n)
+    bufs = {} if bufs is None else bufs
+    for r in REGIONS:
+        if rank not in members[r] or groups[r] == "solo":
+            continue
+        kind, blk = wins[r]
+        data = ops.pack(blk) if kind == "packed" else ops.copy_rect(blk)
+        g = groups[r]
+        if ops.device.type == "cuda" and dist.get_backend(g) == "gloo":
+            host = data.cpu()
+            dist.reduce(host, dst=root, op=dist.ReduceOp.SUM, group=g)
+            data.copy_(host)
+        else:
+            dist.reduce(data, dst=root, op=dist.ReduceOp.SUM, group=g)
+        if rank == root:
+            ops.write(blk, kind, data)
+        bufs[r] = data
+    return C
+
+
+def ata_units(A, C, segments, all_segments=None, params=None, alpha: float = 1.0, groups=None,
+              root: int = 0, precision: str = "fp32"):
+    """lower(C) += alpha * A^T A over the ranks of the default process group
+    with the units partition.  `A` is the full m x n CUDA operand (only the
+    rows this rank's segments read must hold data: auto_plan.a_rows_needed),
+    `segments` this rank's (unit, r0, r1) list, `all_segments` every rank's
+    (for the region groups; built by partition_units when None).  The root's
+    C holds the result; other ranks' C hold their partial regions."""
+    import torch
+    import torch.distributed as dist
+    from . import _native as nat, auto_plan, engine
+    from .distsim import DeviceBlocks
+    m, n = int(A.shape[0]), int(A.shape[1])
+    params = params or auto_plan.AutoParams()
+    world = dist.get_world_size() if dist.is_initialized() else 1
+    rank = dist.get_rank() if dist.is_initialized() else 0
+    if all_segments is None:
+        all_segments = auto_plan.partition_units(m, n, world, params)
+    plan = engine.cached_plan(("units", m, n, A.stride(0), C.stride(0), tuple(segments), params),
+                              lambda: auto_plan.plan_units(segments, m, n, A.stride(0), C.stride(0), params))
+    ws = torch.empty(max(1, plan.ws_scalars), dtype=C.dtype, device=C.device)
+    if rank != root:
+        C.zero_()
+    engine.run_plan(plan, nat.dtype_code(C.dtype, precision), int(A.data_ptr()), A.numel(), int(C.data_ptr()),
+                    C.numel(), alpha, ws=int(ws.data_ptr()), ws_elems=ws.numel())
+    if world > 1:
+        if groups is None:
+            groups, members = make_region_groups(all_segments, root)
+        else:
+            groups, members = groups
+        reduce_regions(C, n, rank, groups, members, DeviceBlocks(C.device, C.dtype), root)
+    return C

@@ -55,3 +55,25 @@ def config_matrix(name: str, rows: int | None = None) -> np.ndarray:
     m = cfg["m"] if rows is None else rows
     dt = np.float64 if cfg["dtype"] == "f64" else np.float32
     return gen_matrix(m, cfg["n"], cfg["seed"], cfg["dist"], dt).a
+
+
+def bench_plan_params(name: str, rows: int, device, base=None, autotune: bool | None = None):
+    """(auto_params, precision) of the plan ``bench.py`` times on config
+    `name` for a shard of `rows` rows -- shared with the full-size parity
+    tests so they check exactly the benchmarked plan.  fp64 auto configs use
+    ``base`` (default AutoParams()); c3, whose BASELINE cutoff is
+    "auto-tuned", measures its rates and leaf width on `device`
+    (autotune.tune) unless autotune=False.  c5 computes in single-pass TF32."""
+    cfg = CONFIGS[name]
+    f64 = cfg["dtype"] == "f64"
+    precision = "fp32" if f64 else "tf32"
+    if cfg["threshold"] != "auto":
+        return None, precision
+    from . import auto_plan
+    params = base if base is not None else auto_plan.AutoParams()
+    if autotune is None:
+        autotune = name == "c3"
+    if autotune and f64:
+        from . import autotune as at
+        params = at.tune(rows, cfg["n"], device, base=params)
+    return params, precision

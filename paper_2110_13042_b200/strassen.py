@@ -62,7 +62,7 @@ def fast_strassen(A, B, C, alpha=1.0, ws: StrassenWorkspace | None = None,
         plan = engine.cached_plan(key, lambda: ref_bfs.plan_strassen_reference_bfs(
             m, n, k, A_.ld, B_.ld, C_.ld, threshold))
         extra = plan.ws_scalars
-    wbuf = ws.ensure(C_.t.device, extra=extra) if plan.ws_scalars > 0 else None
+    wbuf = ws.ensure(C_.t.device, extra=extra, dtype=C_.t.dtype) if plan.ws_scalars > 0 else None
     args = (plan, nat.dtype_code(C_.t.dtype), A_.ptr, A_.elems, C_.ptr, C_.elems, alpha)
     kw = dict(ws=int(wbuf.data_ptr()) if wbuf is not None else 0,
               ws_elems=int(wbuf.numel()) if wbuf is not None else 0, B=B_.ptr, b_elems=B_.elems)
@@ -84,7 +84,7 @@ def _fast_strassen_auto(A_, B_, C_, m, n, k, alpha, counter, auto_params, ws=Non
     plan = engine.cached_plan(key, lambda: auto_plan.plan_gemm_auto(m, n, k, A_.ld, B_.ld, C_.ld, params))
     wbuf = None
     if plan.ws_scalars > 0 and ws is not None:
-        wbuf = ws.ensure(C_.t.device, extra=plan.ws_scalars)
+        wbuf = ws.ensure(C_.t.device, extra=plan.ws_scalars, dtype=C_.t.dtype)
     elif plan.ws_scalars > 0:
         wbuf = _AUTO_WS.get((str(C_.t.device), str(C_.t.dtype)))
         if wbuf is None or wbuf.numel() < plan.ws_scalars:

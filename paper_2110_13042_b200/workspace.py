@@ -170,15 +170,23 @@ class StrassenWorkspace:
         a, l, r = self._base_sizes
         return bn * bk <= a and bm * bn <= l and bm * bk <= r
 
-    def ensure(self, device, extra: int = 0):
-        """Allocate (once) the arena on `device`; grow only if `extra` grows."""
-        import torch
+    def ensure(self, device, extra: int = 0, dtype=None):
+        """Allocate (once) the arena on `device`; grow only if `extra` grows.
+
+        The arena is always held in the dtype the call computes in (`dtype`,
+        default the workspace's own): the native executor counts scratch in
+        scalars of the plan's dtype, so a workspace built for f32 and handed
+        to an f64 call gets an f64 arena of the same scalar count (the
+        reference's NumPy buffers cast on assignment, so such a call is legal
+        there) instead of being overrun."""
+        from .matrix import _as_torch_dtype, _new_buffer
+        tdt = _as_torch_dtype(self.dtype if dtype is None else dtype)
         need = self.level_scalars + max(self.extra, extra)
-        if self.buffer is not None and self.buffer.device == device and self.buffer.numel() >= max(need, 1):
+        if (self.buffer is not None and self.buffer.device == device and self.buffer.dtype == tdt
+                and self.buffer.numel() >= max(need, 1)):
             return self.buffer
-        from .matrix import _new_buffer
         self.extra = max(self.extra, extra)
-        self.buffer = _new_buffer(max(need, 1), self.dtype, device)
+        self.buffer = _new_buffer(max(need, 1), tdt, device)
         self.device = device
         return self.buffer
 

@@ -104,6 +104,28 @@ def test_workspace_undersized_and_shape_errors():
         P.fast_strassen(np.zeros((8, 8)), np.zeros((8, 8)), np.zeros((8, 8)), 1.0, ws, threshold=1)
 
 
+def test_workspace_dtype_differs_from_c(rng):
+    """A workspace sized for f32 handed to an f64 call (legal in the
+    reference: NumPy casts on assignment) computes the f64 result in an f64
+    arena of the same scalar count -- no overrun of a half-sized buffer."""
+    import torch
+    import paper_2110_13042_b200 as P
+    a = rng.uniform(-1, 1, (301, 203))
+    ws = P.workspace_for_ata(301, 203, 4096, dtype=np.float32)
+    c = np.zeros((203, 203))
+    P.ata(a, c, 1.0, threshold=4096, ws=ws)
+    assert ws.buffer.dtype == torch.float64
+    assert ws.buffer.numel() * 8 >= ws.total_scalars * 8
+    ref = np.zeros((203, 203))
+    O.ata_lower(a, ref, 1.0, 4096)
+    assert O.rel_frobenius_lower(c, ref) <= 1e-13
+    b = rng.uniform(-1, 1, (301, 150))
+    ws2 = P.workspace_for(301, 203, 150, 4096, dtype=np.float32)
+    c2 = np.zeros((203, 150))
+    P.fast_strassen(a, b, c2, 1.0, ws2, threshold=4096)
+    assert np.allclose(c2, a.T @ b, rtol=0, atol=1e-11)
+
+
 def test_config_c1_golden(golden):
     """c1 (1024^2 U[-1,1], seed 0) at the parity cutoff t = 64^2: exact count,
     sampled entries and checksums against the reference's own run."""

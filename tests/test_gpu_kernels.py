@@ -232,3 +232,40 @@ def test_tf32_l2_ring_matches_rounding_pass():
     assert torch.equal(out[0], out[1])
     ref = O.gram_blas(A.double().cpu().numpy())
     assert O.rel_frobenius_lower(out[0].cpu().numpy(), ref) <= 1e-4
+
+
+def test_tf32_l2_ring_under_sm_contention():
+    """The L2-ring launch needs every CTA resident at once (CTAs wait on one
+    another's rounding items); it is a cooperative launch, so work on another
+    stream that holds SMs delays it instead of leaving resident CTAs spinning.
+    Run the ring plan while a second stream keeps the SMs busy with GEMMs and
+    check it completes with the same bits as on an idle GPU."""
+    import torch
+    from paper_2110_13042_b200 import auto_plan, engine, _native as nat
+    m, n = 1 << 17, 2048
+    g = torch.Generator(device="cuda").manual_seed(6)
+    A = torch.randn((m, n), device="cuda", generator=g)
+    plan = auto_plan.plan_ata_auto(m, n, n, n, auto_plan.AutoParams(tf32_ring=True), round_tf32=True)
+    assert int(plan.ops[0]["accumulate"]) == 2
+    ws = torch.empty(plan.ws_scalars, device="cuda")
+
+    def run(C, stream):
+        engine.run_plan(plan, nat.ATA_TF32, A.data_ptr(), A.numel(), C.data_ptr(), C.numel(), 1.0,
+                        ws=ws.data_ptr(), ws_elems=ws.numel(), stream=int(stream.cuda_stream))
+
+    main = torch.cuda.current_stream()
+    C0 = torch.zeros((n, n), device="cuda")
+    run(C0, main)
+    torch.cuda.synchronize()
+    hog = torch.cuda.Stream()
+    x = torch.randn((4096, 4096), device="cuda", dtype=torch.bfloat16)
+    C1 = torch.zeros((n, n), device="cuda")
+    with torch.cuda.stream(hog):
+        for _ in range(40):
+            x = (x @ x).clamp_(-1, 1)
+    run(C1, main)            # queued while the hog stream occupies SMs
+    with torch.cuda.stream(hog):
+        for _ in range(40):
+            x = (x @ x).clamp_(-1, 1)
+    torch.cuda.synchronize()
+    assert torch.equal(C0, C1)
