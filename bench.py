@@ -61,10 +61,12 @@ def parse():
     p.add_argument("--no-autotune", action="store_true")
     p.add_argument("--gain", type=float, default=None,
                    help="auto plan: split a Strassen node when saved time > gain x added time")
-    p.add_argument("--dist", choices=["auto", "rows", "tree"], default="auto",
-                   help="N>1 partition: row shards + one NCCL reduce (auto; the reference's tree for "
-                        "N <= 5), or the reference's distributed task tree (leaf per rank, blocks "
-                        "retrieved over NCCL point-to-point; its N >= 6 layout)")
+    p.add_argument("--dist", choices=["auto", "rows", "units", "tree"], default="auto",
+                   help="N>1 partition: row shards + one NCCL reduce of packed triangles; units = the "
+                        "top level's AtA sub-problems and seven Strassen products as balanced row-range "
+                        "segments per rank + one NCCL reduce per C region (auto picks the one with the "
+                        "smaller planned critical path); tree = the reference's distributed task tree "
+                        "(leaf per rank, blocks retrieved over NCCL point-to-point)")
     p.add_argument("--fuse-leaf-sums", action="store_true",
                    help="A/B: last Strassen level's operand sums summed in the product loads")
     p.add_argument("--dump-units", default=None, help="write per-launch timings (JSON) here")
@@ -288,19 +290,46 @@ def main():
     threshold = cfg["threshold"]
     from paper_2110_13042_b200.tasktree import build_tree_distributed, leaf_task
     tree = None
+    useg = None           # units partition: every rank's [(unit, r0, r1)] segments
+    dist_kind = "single"
     if world > 1:
         t_ref = build_tree_distributed(world, m, n)
+        dist_kind = args.dist
         if args.dist == "tree":
             tree = t_ref
+        elif args.dist in ("auto", "units") and threshold == "auto" and f64:
+            base = auto_plan.AutoParams()
+            parts = auto_plan.partition_units(m, n, world, base)
+            worst = max(auto_plan.plan_units(sg, m, n, n, n, base).mults for sg in parts)
+            rows_worst = auto_plan.plan_ata_auto(-(-m // world), n, n, n, base).mults
+            if args.dist == "units" or worst < 0.99 * rows_worst:
+                useg, dist_kind = parts, "units"
+            else:
+                dist_kind = "rows"
+        else:
+            dist_kind = "rows" if args.dist == "auto" else args.dist
     r0, r1 = pdist.tree_rows(tree, rank) if tree is not None else pdist.shard_rows(m, world, rank)
     # ---- inputs: seeded host draw of this rank's rows, then H2D ----
     t_gen = time.perf_counter()
-    if cfg["dist"] == "uniform":
+    if useg is not None:
+        # the full m x n operand in HBM, holding the row ranges this rank's
+        # segments read (auto_plan.a_rows_needed); other rows stay zero
+        r0, r1 = 0, m
+        A = torch.zeros((m, n), dtype=torch.float64 if f64 else torch.float32, device=dev)
+        host = None
+        for lo, hi in auto_plan.a_rows_needed(useg[rank], m, n):
+            if cfg["dist"] == "uniform":
+                blk = pdist.uniform_rows(m, n, cfg["seed"], lo, hi, np_dt)
+            else:
+                blk = np.random.default_rng(cfg["seed"]).standard_normal((m, n))[lo:hi].astype(np_dt)
+            A[lo:hi].copy_(torch.from_numpy(blk))
+    elif cfg["dist"] == "uniform":
         host = pdist.uniform_rows(m, n, cfg["seed"], r0, r1, np_dt)
     else:
         host = np.random.default_rng(cfg["seed"]).standard_normal((m, n))[r0:r1].astype(np_dt)
     t_gen = time.perf_counter() - t_gen
-    A = torch.from_numpy(host).to(dev)
+    if useg is None:
+        A = torch.from_numpy(host).to(dev)
     C = torch.zeros((n, n), dtype=A.dtype, device=dev)
     packed = torch.empty(n * (n + 1) // 2, dtype=A.dtype, device=dev) if world > 1 else None
     params = auto_plan.AutoParams(**{k: v for k, v in (("leaf_cols", args.leaf_cols),
@@ -341,6 +370,11 @@ def main():
             plan = ref_bfs.plan_strassen_reference_bfs(mloc, ar.cols, br.cols, n, n, cr.cols, threshold)
         wsbuf = torch.empty(max(1, plan.ws_scalars), dtype=A.dtype, device=dev) \
             if plan.ws_scalars else None
+    elif useg is not None:
+        plan = auto_plan.plan_units(useg[rank], m, n, n, n, params)
+        wsbuf = torch.empty(max(1, plan.ws_scalars), dtype=A.dtype, device=dev) \
+            if plan.ws_scalars else None
+        region_groups = pdist.make_region_groups(useg)
     elif threshold == "auto":
         plan = auto_plan.plan_ata_auto(mloc, n, n, n, params, round_tf32=not f64)
         wsbuf = torch.empty(max(1, plan.ws_scalars), dtype=A.dtype, device=dev) \
@@ -385,11 +419,17 @@ def main():
                                          leaf_block=C_out)
             if rank == 0:
                 pdist.add_lower_into(C, top)
+        elif useg is not None:   # one NCCL reduce per C region over the ranks that wrote it
+            pdist.reduce_regions(C, n, rank, region_groups[0], region_groups[1], region_ops)
         elif world > 1:
             P.pack_lower(C, out=packed)
             pdist.reduce_packed(packed, 0)
             if rank == 0:
                 P.unpack_lower(P.PackedLowerTriangular(n, packed), C)
+
+    if useg is not None:
+        from paper_2110_13042_b200.distsim import DeviceBlocks
+        region_ops = DeviceBlocks(dev, A.dtype)
 
     def barrier():
         if world > 1:
@@ -524,11 +564,14 @@ def main():
             "config": bench_config(args.config),
             "parallelism": (f"task-tree x{world} (reference build_tree_distributed; rank 0 "
                             f"leaf {leaf.computation.value} A{leaf.a_region})" if tree is not None
+                            else f"units x{world} (top-level AtA sub-problems + 7 Strassen products as "
+                                 f"balanced row-range segments; rank 0: {useg[0]})" if useg is not None
                             else f"row-shard x{world}" if world > 1 else "single GPU"),
             "a_bytes": A.numel() * A.element_size(),
             "plan": {"kind": plan.kind, "ops": len(plan.ops), "launches": n_launch,
                      "executed_mults": plan.mults,
                      "mults_over_classical": plan.mults / (
+                         m * n * (n + 1) / 2 / world if useg is not None else
                          mloc * n * (n + 1) / 2 if leaf is None else
                          mloc * leaf.a_region.cols * (leaf.a_region.cols + 1) / 2
                          if leaf.b_region is None else
@@ -537,9 +580,10 @@ def main():
             "effective_pct_of_peak": value / 1e3 / peak,
             "roofline": roofline,
             "clocks": clk.summary,
-            # our kernels in the timed region, counted by the native executor on a
-            # warm-up step (the graph replays the same launches) + pack/unpack at N>1
-            "gpu_launches": per_step_launches * args.steps + (2 * args.steps if world > 1 else 0),
+            # our kernels in the timed region, counted by the native library on a
+            # warm-up step (plan launches + pack / unpack / mirror kernels; the graph
+            # replays the same launches)
+            "gpu_launches": per_step_launches * args.steps,
             "cuda_graph": graph is not None,
             "input_gen_s": t_gen}
     # ---- e2e through the public API with pinned host buffers (N = 1) ----

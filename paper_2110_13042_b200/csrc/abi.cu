@@ -739,6 +739,7 @@ int ata_mirror_lower(int dtype, void* C, int64_t ldc, int32_t n, void* stream) {
   cudaError_t e = dtype == ATA_F64
                       ? ata::launch_mirror<double>(static_cast<double*>(C), ldc, n, (cudaStream_t)stream)
                       : ata::launch_mirror<float>(static_cast<float*>(C), ldc, n, (cudaStream_t)stream);
+  g_launches += 1;
   return e == cudaSuccess ? ATA_OK : cuda_fail(e, "mirror");
 }
 
@@ -750,6 +751,7 @@ int ata_pack_lower(int dtype, const void* C, int64_t ldc, int32_t n, void* packe
                                      (cudaStream_t)stream)
           : ata::launch_pack<float>(static_cast<const float*>(C), ldc, n, static_cast<float*>(packed),
                                     (cudaStream_t)stream);
+  g_launches += 1;
   return e == cudaSuccess ? ATA_OK : cuda_fail(e, "pack");
 }
 
@@ -763,6 +765,7 @@ int ata_unpack_lower(int dtype, const void* packed, int32_t n, void* C, int64_t 
                       : ata::launch_unpack<float>(static_cast<const float*>(packed), n,
                                                   static_cast<float*>(C), ldc, accumulate,
                                                   (cudaStream_t)stream);
+  g_launches += 1;
   return e == cudaSuccess ? ATA_OK : cuda_fail(e, "unpack");
 }
 

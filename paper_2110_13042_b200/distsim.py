@@ -399,6 +399,9 @@ class _GroupLink:
     def __init__(self, group, ops):
         import torch.distributed as dist
         self.dist, self.group, self.ops = dist, group, ops
+        # gloo has no point-to-point on CUDA tensors: stage through the host
+        # (CPU checks of the multi-rank path on one shared GPU)
+        self.stage = dist.get_backend(group) == "gloo" and getattr(ops.device, "type", "cpu") == "cuda"
 
     def _peer(self, r):
         return r if self.group is None else self.dist.get_global_rank(self.group, r)
@@ -407,12 +410,18 @@ class _GroupLink:
         import torch
         flat = torch.cat([pt.data.reshape(-1) for pt in msg.parts]) if len(msg.parts) > 1 \
             else msg.parts[0].data.reshape(-1)
-        self.dist.send(flat.contiguous(), dst=self._peer(msg.dst), group=self.group)
+        flat = flat.contiguous()
+        self.dist.send(flat.cpu() if self.stage else flat, dst=self._peer(msg.dst), group=self.group)
 
     def recv(self, src: int, dst: int, spec) -> Message:
         words = [_part_words(k, r) for k, r in spec]
         flat = self.ops.empty(sum(words))
-        self.dist.recv(flat, src=self._peer(src), group=self.group)
+        if self.stage:
+            host = flat.cpu()
+            self.dist.recv(host, src=self._peer(src), group=self.group)
+            flat.copy_(host)
+        else:
+            self.dist.recv(flat, src=self._peer(src), group=self.group)
         parts, o = [], 0
         for (k, r), w in zip(spec, words):
             parts.append(MessagePart(k, r, flat[o:o + w]))
@@ -443,6 +452,8 @@ def _gather_stats(stats: CommStats, group, device) -> CommStats:
     import torch
     import torch.distributed as dist
     P, r = stats.procs, dist.get_rank(group)
+    if dist.get_backend(group) == "gloo":
+        device = "cpu"
     mine = torch.tensor([stats.sent_messages[r], stats.sent_words[r], stats.recv_messages[r],
                          stats.recv_words[r]], dtype=torch.int64, device=device)
     out = [torch.zeros_like(mine) for _ in range(P)]
@@ -495,6 +506,8 @@ def ata_d(A, procs: int, threshold=DEFAULT_THRESHOLD, leaf_kernel: str = "fast",
     else:
         a, meta = None, torch.zeros(3, dtype=torch.int64, device=dev)
     if multi:
+        if dist.get_backend(group) == "gloo":
+            meta = meta.cpu()
         dist.broadcast(meta, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
     m, n, w = (int(x) for x in meta.tolist())
     dtype = torch.float64 if w == 8 else torch.float32

@@ -1,20 +1,66 @@
-"""Row-sharded multi-rank AtA (2 ranks, gloo, both on cuda:0): the packed
-lower-triangle sum equals the single-rank result (tools/dist_check.py)."""
+"""Multi-rank GPU paths, 2 and 3 ranks over gloo on cuda:0 (gpurun exposes
+one GPU): row shards, the units partition and the distribute-compute-
+retrieve executor ata_d, each checked on rank 0 against the CPU oracle's
+classical Gram (tests/dist_worker.py), plus the units partition's plans of
+all ranks run on one GPU against the oracle."""
 import os
 import subprocess
 import sys
 
+import numpy as np
 import pytest
+
+from oracle import atamul_oracle as O
 
 pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def test_row_sharded_two_ranks_shared_gpu():
-    env = dict(os.environ, ATA_DIST_BACKEND="gloo")
-    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-                        "--master-addr", "127.0.0.1", "--master-port", "29541",
-                        os.path.join(ROOT, "tools", "dist_check.py")],
-                       capture_output=True, text=True, env=env, timeout=600)
+@pytest.mark.parametrize("mode,world,m,n", [("rows", 2, 40000, 3000), ("units", 2, 9000, 3000),
+                                            ("units", 3, 8193, 2049), ("ata_d", 2, 3001, 2000),
+                                            ("ata_d", 3, 3001, 2000)])
+def test_multi_rank_vs_oracle(mode, world, m, n):
+    env = dict(os.environ)
+    port = str(29541 + world + 7 * ("rows", "units", "ata_d").index(mode))
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node",
+                        str(world), "--master-addr", "127.0.0.1", "--master-port", port,
+                        os.path.join(ROOT, "tests", "dist_worker.py"), mode, str(m), str(n)],
+                       capture_output=True, text=True, env=env, timeout=900)
     assert r.returncode == 0, r.stderr[-3000:]
     assert "OK" in r.stdout, r.stdout[-2000:]
+    print(r.stdout.strip().splitlines()[-1])
+
+
+@pytest.mark.parametrize("procs", [2, 4, 8])
+def test_units_partition_all_ranks_one_gpu(procs):
+    """Every rank's plan_units plan run on one GPU into one C: the segments
+    add up to lower(A^T A) (c4's aspect ratio, scaled down)."""
+    import torch
+    from paper_2110_13042_b200 import auto_plan, engine, _native as nat
+    m, n = 8192, 4096
+    params = auto_plan.AutoParams(leaf_cols=512, min_dim=256, hbm_gbs=1e9)
+    a = np.random.default_rng(procs).uniform(-1, 1, (m, n))
+    A = torch.from_numpy(a).cuda()
+    C = torch.zeros(n, n, dtype=torch.float64, device="cuda")
+    for segs in auto_plan.partition_units(m, n, procs, params):
+        plan = auto_plan.plan_units(segs, m, n, n, n, params)
+        ws = torch.empty(max(1, plan.ws_scalars), dtype=torch.float64, device="cuda")
+        engine.run_plan(plan, nat.ATA_F64, A.data_ptr(), A.numel(), C.data_ptr(), C.numel(), 1.0,
+                        ws=ws.data_ptr(), ws_elems=ws.numel())
+    torch.cuda.synchronize()
+    assert O.rel_frobenius_lower(C.cpu().numpy(), O.gram_blas(a)) <= 1e-13
+
+
+def test_bench_units_two_ranks_shared_gpu():
+    """bench.py's N>1 path with the units partition (2 ranks, gloo, one GPU):
+    the driver's JSON line names the partition and the per-rank plan."""
+    import json
+    env = dict(os.environ, ATA_DIST_BACKEND="gloo")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+                        "--master-addr", "127.0.0.1", "--master-port", "29611", os.path.join(ROOT, "bench.py"),
+                        "--gpus", "2", "--config", "c3", "--dist", "units", "--steps", "2", "--warmup", "1",
+                        "--no-autotune"], capture_output=True, text=True, env=env, timeout=900, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
+    assert line["n_gpus"] == 2 and line["parallelism"].startswith("units x2")
+    assert line["value"] > 0 and line["gpu_launches"] > 0
