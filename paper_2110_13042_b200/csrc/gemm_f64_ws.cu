@@ -370,6 +370,10 @@ __global__ void __launch_bounds__(ws64::THREADS, 1)
       for (int kt = 0; kt < KT; ++kt, ++kstep) {
         const int s = kstep % STAGES;
         if (kstep >= STAGES) mbar_wait(&empty[s], ((kstep / STAGES) - 1) & 1);
+#ifdef WS_AB_NOLOAD   // A/B probe: no operand traffic (stages publish stale data)
+        mbar_arrive(&full[s]);
+        continue;
+#endif
         issue(kt, kstep);
         if (!comb) {
           mbar_arrive_cpasync(&full[s]);
@@ -437,7 +441,9 @@ __global__ void __launch_bounds__(ws64::THREADS, 1)
     const double sb = same ? sa : (two_b ? P.t[1].sign : 0.0);
     for (int kt = 0; kt < KT; ++kt, ++kstep) {
       const int s = kstep % STAGES;
+#ifndef WS_AB_NOFULLWAIT   // A/B probe: consumers never wait for data
       mbar_wait(&full[s], (kstep / STAGES) & 1);
+#endif
       const double* As = smem + s * STAGE + aoff;
       const double* Bs = smem + s * STAGE + boff;
 #pragma unroll

@@ -187,17 +187,6 @@ def _wire(task, block):
     return block
 
 
-def _unwire(task, wire, dtype, device):
-    import torch
-    c = task.c_region
-    if task.b_region is None:
-        from .matrix import PackedLowerTriangular, unpack_lower
-        out = torch.zeros((c.rows, c.rows), dtype=dtype, device=device)
-        unpack_lower(PackedLowerTriangular(c.rows, wire), out)
-        return out
-    return wire.view(c.rows, c.cols)
-
-
 def run_tree_process(tree, p: int, get_block, link, alpha=1.0, threshold="auto", dtype=None,
                      device=None, counter=None, precision: str = "fp32", leaf_block=None):
     """Process p's part of the tree: its leaf (or the caller's `leaf_block`,
@@ -208,20 +197,27 @@ def run_tree_process(tree, p: int, get_block, link, alpha=1.0, threshold="auto",
     chain = path_to_root(tree, p)
     block = leaf_block if leaf_block is not None else \
         _leaf_block(chain[0].task, get_block, alpha, threshold, dtype, device, counter, precision)
+    from .matrix import PackedLowerTriangular, add_truncated, unpack_lower
     for prev, node in zip(chain, chain[1:]):
         import torch
         c = node.task.c_region
         out = torch.zeros((c.rows, c.cols), dtype=dtype, device=device)
+        # children's blocks accumulate in child order with the native kernels:
+        # packed AtA partials unpack-accumulate straight into their diagonal
+        # block (distsim.py:208-216), rectangles through the truncated add
         for child in tree.children_of(node):
-            if child.id == prev.id:
-                blk = block
-            else:
-                q = child.task.owner
-                wire = link.recv((_block_words(child.task), dtype, device), q, p, child)
-                blk = _unwire(child.task, wire, dtype, device)
             cc = child.task.c_region
             r0, c0 = cc.row_offset - c.row_offset, cc.col_offset - c.col_offset
-            out[r0:r0 + cc.rows, c0:c0 + cc.cols] += blk
+            view = out[r0:r0 + cc.rows, c0:c0 + cc.cols]
+            if child.id == prev.id:
+                add_truncated(view, block, 1.0)
+                continue
+            q = child.task.owner
+            wire = link.recv((_block_words(child.task), dtype, device), q, p, child)
+            if child.task.b_region is None:
+                unpack_lower(PackedLowerTriangular(cc.rows, wire), view, accumulate=True)
+            else:
+                add_truncated(view, wire.view(cc.rows, cc.cols), 1.0)
         block = out
     top = chain[-1]
     if top.parent_id is not None:

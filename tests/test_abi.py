@@ -61,3 +61,25 @@ def test_plan_validation_without_gpu():
     rc = lib.ata_run_plan(0, bad.ctypes.data_as(ctypes.c_void_p), len(bad), fake, 256,
                           fake, 256, fake, 256, fake, 10**6, None, 0, 1.0, None)
     assert rc == -1
+
+
+def test_python_surface_covers_reference_exports():
+    """Every name of the reference's atamul.__all__ (pkg/src/atamul/__init__.py:29-46)
+    is exported under the same name (import swap)."""
+    import paper_2110_13042_b200 as P
+    reference_all = [
+        "AtamulError", "CommStats", "ComputationType", "DEFAULT_THRESHOLD", "DenseMatrix",
+        "InvalidMeasurementError", "MatrixView", "MultCounter", "PackedLowerTriangular", "ProtocolError",
+        "Region", "ShapeMismatchError", "SharedRunner", "StrassenWorkspace", "Task", "TaskTree",
+        "TooManyWorkersError", "UnknownProcessError", "UnsplittableError", "UnsupportedSizeError",
+        "WorkspaceUndersizedError", "add_truncated", "ata", "ata_d", "ata_full", "ata_mult_count", "ata_s",
+        "build_tree_distributed", "build_tree_shared", "effective_gflops", "fast_strassen", "gen_matrix",
+        "leaf_task", "levels_distributed", "levels_shared", "mirror_lower_to_upper", "naive_gemm_atb",
+        "naive_syrk_lower", "pack_lower", "path_to_root", "read_matrix", "render_tree", "split4",
+        "strassen_mult_count", "unpack_lower", "verify_comm_bounds", "workspace_for", "workspace_for_ata",
+        "write_matrix"]
+    missing = [n for n in reference_all if not hasattr(P, n)]
+    assert not missing, missing
+    from paper_2110_13042_b200.execute import execute_leaf, workspace_for_leaf  # noqa: F401
+    from paper_2110_13042_b200.shared import MAX_WORKERS
+    assert MAX_WORKERS == 128
