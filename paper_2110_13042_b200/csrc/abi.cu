@@ -412,6 +412,31 @@ int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, int* sync, int64_t 
     if (!nb && last - first > ata::kMaxBatch) return fail(ATA_E_ARG, "internal: oversized product batch");
     if (nb) {
       if constexpr (std::is_same<T, double>::value) {
+        {
+          // single-term products with TMA-legal windows: the TMA-fed kernel, one
+          // persistent launch (descriptors and tensor maps in device memory)
+          struct {
+            int count;
+            double alpha;
+            int* sync;
+            int n_sync;
+            ata::DProdT<double, ata::kNarrowDests>* p;
+          } tb;
+          std::vector<ata::DProdT<double, ata::kNarrowDests>> prods(last - first);
+          std::memset(prods.data(), 0, sizeof(prods[0]) * prods.size());
+          tb.count = 0;
+          tb.p = prods.data();
+          fill_batch(tb, first, last);
+          if (ata::f64_tma_eligible(prods.data(), tb.count)) {
+            cudaError_t e = ata::launch_batch_f64_tma(prods.data(), tb.count, alpha, sync, sync_ints, s);
+            if (e == cudaSuccess) {
+              g_launches += 1;
+              return ATA_OK;
+            }
+            if (e != cudaErrorNotReady && e != cudaErrorNotSupported) return cuda_fail(e, "product launch (tma)");
+            cudaGetLastError();   // not resident while capturing / no map: the cp.async kernels below
+          }
+        }
         static const bool no_global = std::getenv("ATA_NO_GLOBAL_BATCH") != nullptr;  // A/B knob
         if (last - first > ata::kMaxBatchNarrow && !no_global) {
           // unbounded region-free batch: device-resident descriptors, one launch

@@ -106,6 +106,12 @@ cudaError_t launch_batch_f64_narrow(const BatchArgsNarrow64& a, cudaStream_t s);
 cudaError_t launch_batch_f64_global(DProdT<double, kNarrowDests>* prods, int count, double alpha, int* sync,
                                     cudaStream_t s);
 bool f64_narrow_supported();
+// single-term narrow products with TMA-legal windows (16-byte aligned, even
+// pitch, cols % 16 == 0): one persistent launch of the TMA-fed kernel;
+// cudaErrorNotReady while capturing with descriptors not yet resident
+bool f64_tma_eligible(const DProdT<double, kNarrowDests>* prods, int count);
+cudaError_t launch_batch_f64_tma(DProdT<double, kNarrowDests>* prods, int count, double alpha, int* sync,
+                                 long long sync_ints, cudaStream_t s);
 bool f64_supports_ordering();
 cudaError_t launch_batch_f32(const BatchArgs<float>& a, cudaStream_t s, bool split);
 template <typename T> cudaError_t launch_combo(const EwArgs<T>& a, cudaStream_t s);

@@ -35,6 +35,9 @@
 #include <cstring>
 #include <type_traits>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include "ata_common.cuh"
 
 namespace ata {
@@ -224,6 +227,84 @@ __device__ __forceinline__ TileInfo decode_tile(const Args& args, int tile) {
     t.tj = in / gsz;
   }
   return t;
+}
+
+// Epilogue of one output tile (shared by the cp.async- and TMA-fed kernels):
+// signed, truncated writes of every destination; a destination region shared
+// by several products of the launch is accumulated in product order through
+// per-tile turn counters.
+template <typename Args, typename PD>
+__device__ __forceinline__ void ws_epilogue(const Args& args, const PD& P, const TileInfo& tl,
+                                            const double (&acc)[ws64::WTM][ws64::WTN][2], int wm, int wn,
+                                            int g, int q, int ctid) {
+  using namespace ws64;
+  const bool syrk = P.kind == kSyrk;
+  const int i0 = tl.ti * BM, j0 = tl.tj * BN;
+  const int nd = P.nd;
+  const bool accumulate = P.accumulate != 0;
+  for (int d = 0; d < ((args.dbg & 2) ? 0 : nd); ++d) {
+    const DDest<double>& D = P.d[d];
+    const double scale = args.alpha * D.sign;
+    if (i0 >= D.rows || j0 >= D.cols) continue;  // tile entirely outside this window
+    int* sem = nullptr;
+    int turn = 0;
+    if (D.sem >= 0 && !(args.dbg & 1)) {
+      // turn = earlier products of the launch whose window in this region covers the tile
+      for (int q = 0; q < tl.pi; ++q)
+        for (int e = 0; e < prod_of(args, q).nd; ++e) {
+          const DDest<double>& E = prod_of(args, q).d[e];
+          if (E.sem == D.sem && i0 < E.rows && j0 < E.cols) ++turn;
+        }
+      sem = args.sync + D.sem + tl.ti * D.sem_ld + tl.tj;
+      if (ctid == 0) {
+        // bounded wait: a broken ordering invariant traps (launch error) instead of hanging
+        uint64_t t0;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+        while (ld_acquire(sem) != turn) {
+          __nanosleep(64);
+          uint64_t t1;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+          if (t1 - t0 > 20000000000ull) __trap();
+        }
+      }
+      named_sync(2, CONSUMERS * 32);
+    }
+#pragma unroll
+    for (int r = 0; r < WTM; ++r) {
+      const int row = i0 + wm * (WTM * 8) + r * 8 + g;
+      if (row >= D.rows) continue;
+      double* drow = D.p + (long long)row * D.ld;
+#pragma unroll
+      for (int c = 0; c < WTN; ++c) {
+        const int col = j0 + wn * (WTN * 8) + c * 8 + q * 2;
+        if (col + 1 < D.cols && (!syrk || col + 1 <= row) &&
+            ((reinterpret_cast<uintptr_t>(drow + col) & 15) == 0)) {
+          double2* p2 = reinterpret_cast<double2*>(drow + col);
+          double2 v = make_double2(scale * acc[r][c][0], scale * acc[r][c][1]);
+          if (accumulate) {
+            const double2 o = __ldcg(p2);  // L2: another SM may have written it this launch
+            v.x += o.x;
+            v.y += o.y;
+          }
+          __stcg(p2, v);
+        } else {
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int cc = col + e;
+            if (cc < D.cols && (!syrk || cc <= row)) {
+              const double v = scale * acc[r][c][e];
+              __stcg(drow + cc, accumulate ? __ldcg(drow + cc) + v : v);
+            }
+          }
+        }
+      }
+    }
+    if (sem != nullptr) {
+      __threadfence();
+      named_sync(2, CONSUMERS * 32);
+      if (ctid == 0) st_release(sem, turn + 1);
+    }
+  }
 }
 
 template <int BK, int NS, int NT, int STAGES, typename Args>
@@ -471,71 +552,7 @@ __global__ void __launch_bounds__(ws64::THREADS, 1)
     }
 
     // ---- epilogue: fused post-additions into up to four destinations ----
-    const int nd = P.nd;
-    const bool accumulate = P.accumulate != 0;
-    for (int d = 0; d < ((args.dbg & 2) ? 0 : nd); ++d) {
-      const DDest<double>& D = P.d[d];
-      const double scale = args.alpha * D.sign;
-      if (i0 >= D.rows || j0 >= D.cols) continue;  // tile entirely outside this window
-      int* sem = nullptr;
-      int turn = 0;
-      if (D.sem >= 0 && !(args.dbg & 1)) {
-        // turn = earlier products of the launch whose window in this region covers the tile
-        for (int q = 0; q < tl.pi; ++q)
-          for (int e = 0; e < prod_of(args, q).nd; ++e) {
-            const DDest<double>& E = prod_of(args, q).d[e];
-            if (E.sem == D.sem && i0 < E.rows && j0 < E.cols) ++turn;
-          }
-        sem = args.sync + D.sem + tl.ti * D.sem_ld + tl.tj;
-        if (ctid == 0) {
-          // bounded wait: a broken ordering invariant traps (launch error) instead of hanging
-          uint64_t t0;
-          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
-          while (ld_acquire(sem) != turn) {
-            __nanosleep(64);
-            uint64_t t1;
-            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
-            if (t1 - t0 > 20000000000ull) __trap();
-          }
-        }
-        named_sync(2, CONSUMERS * 32);
-      }
-#pragma unroll
-      for (int r = 0; r < WTM; ++r) {
-        const int row = i0 + wm * (WTM * 8) + r * 8 + g;
-        if (row >= D.rows) continue;
-        double* drow = D.p + (long long)row * D.ld;
-#pragma unroll
-        for (int c = 0; c < WTN; ++c) {
-          const int col = j0 + wn * (WTN * 8) + c * 8 + q * 2;
-          if (col + 1 < D.cols && (!syrk || col + 1 <= row) &&
-              ((reinterpret_cast<uintptr_t>(drow + col) & 15) == 0)) {
-            double2* p2 = reinterpret_cast<double2*>(drow + col);
-            double2 v = make_double2(scale * acc[r][c][0], scale * acc[r][c][1]);
-            if (accumulate) {
-              const double2 o = __ldcg(p2);  // L2: another SM may have written it this launch
-              v.x += o.x;
-              v.y += o.y;
-            }
-            __stcg(p2, v);
-          } else {
-#pragma unroll
-            for (int e = 0; e < 2; ++e) {
-              const int cc = col + e;
-              if (cc < D.cols && (!syrk || cc <= row)) {
-                const double v = scale * acc[r][c][e];
-                __stcg(drow + cc, accumulate ? __ldcg(drow + cc) + v : v);
-              }
-            }
-          }
-        }
-      }
-      if (sem != nullptr) {
-        __threadfence();
-        named_sync(2, CONSUMERS * 32);
-        if (ctid == 0) st_release(sem, turn + 1);
-      }
-    }
+    ws_epilogue(args, P, tl, acc, wm, wn, g, q, ctid);
     if (kSmemDesc) {    // the shared descriptor copy was read up to here
       __syncwarp();
       if (lane == 0) mbar_arrive(&tempty[slot]);
@@ -653,6 +670,236 @@ static cudaError_t launch_ws_any(const Args& a, cudaStream_t s) {
 
 cudaError_t launch_batch_f64_ws(const BatchArgs<double>& a, cudaStream_t s) { return launch_ws_any(a, s); }
 
+
+// ===========================================================================
+// TMA-fed variant (single-term operands).  Same warp roles, tiles, epilogue
+// and tile queue as prod_f64_ws_kernel, but the operand windows reach shared
+// memory through the tensor-memory accelerator: ONE producer thread issues,
+// per k-block, one 3-D bulk tensor copy per operand ([8 panels][BK rows][16
+// doubles], 128-byte swizzle) instead of 4096 16-byte cp.async per stage from
+// 128 threads (measured: removing the cp.async traffic alone lifts the c4 leaf
+// group from 33.3 to 35.2 TF/s, tools/f64_ab.py).  Rows / columns outside a
+// window are zero-filled by the TMA unit (the reference's zero-extension).
+//
+// Bank-conflict-free fragment reads of the swizzled layout: a DMMA m8n8k4
+// fragment lane (g, q) reads element (k = q, m/n = g); the k-slots of one DMMA
+// are mapped to smem rows {x, x+2, x+4, x+6} (x = k-step parity) of an 8-row
+// swizzle atom, whose 16-byte chunks the 128B swizzle spreads over all 32
+// banks.  The contraction order inside a k-block is permuted accordingly (the
+// same permutation for both operands).
+// ===========================================================================
+namespace wst {
+#ifndef WST_BK
+#define WST_BK 32
+#endif
+constexpr int BK = WST_BK;
+constexpr int PANELS = ws64::BM / 16;              // 16 doubles = one 128-byte swizzle row
+constexpr int BUF_BYTES = BK * 128 * PANELS;       // one operand k-block
+constexpr int STAGE_BYTES = 2 * BUF_BYTES;
+constexpr int STAGES = (ws64::SMEM_BUDGET - 2048) / STAGE_BYTES > 6 ? 6 : (ws64::SMEM_BUDGET - 2048) / STAGE_BYTES;
+static_assert(BK % 8 == 0 && STAGES >= 2, "TMA k-block");
+}  // namespace wst
+
+struct TmaBatch64 {
+  int count;
+  int total_tiles;
+  double alpha;
+  int* sync;
+  int n_sync;
+  int dynamic;
+  int dbg;
+  const CUtensorMap* maps;                      // device array [2 * count]: S, T of each product
+  const DProdT<double, kNarrowDests>* gp;       // device array [count]
+  const int* tile_prod;                         // device array [total_tiles]
+};
+__device__ __forceinline__ const DProdT<double, kNarrowDests>& prod_of(const TmaBatch64& a, int i) {
+  return a.gp[i];
+}
+
+__device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map, int c0, int c1, int c2,
+                                            uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
+      : "memory");
+}
+__device__ __forceinline__ double lds64(uint32_t addr) {
+  double v;
+  asm volatile("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+  return v;
+}
+
+__global__ void __launch_bounds__(ws64::THREADS, 1) prod_f64_tma_kernel(const __grid_constant__ TmaBatch64 args) {
+  using namespace ws64;
+  using wst::BK;
+  using wst::BUF_BYTES;
+  using wst::STAGE_BYTES;
+  using wst::STAGES;
+  using PD = DProdT<double, kNarrowDests>;
+  constexpr int kSlots = 3;
+  extern __shared__ uint8_t tma_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tma_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tfull = empty + STAGES;
+  uint64_t* tempty = tfull + kSlots;
+  int* tinfo = reinterpret_cast<int*>(tempty + kSlots);
+  __shared__ __align__(16) unsigned char pdesc_raw[kSlots * sizeof(PD)];
+  __shared__ int tdec[kSlots][3];
+  const int tid = threadIdx.x;
+  const int warp = tid >> 5;
+  const int lane = tid & 31;
+
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], CONSUMERS);
+    }
+    for (int s = 0; s < kSlots; ++s) {
+      mbar_init(&tfull[s], 1);
+      mbar_init(&tempty[s], CONSUMERS);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+  }
+  __syncthreads();
+
+  if (tid < PRODUCERS) {
+    // ===================== producer: one warp, one issuing thread =====================
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PRODUCER_REGS));
+    if (warp != 0) return;
+    int kstep = 0;
+    for (int it = 0;; ++it) {
+      int tile = 0;
+      if (lane == 0) tile = args.dynamic ? atomicAdd(args.sync, 1) : (int)(blockIdx.x + it * gridDim.x);
+      tile = __shfl_sync(0xffffffffu, tile, 0);
+      const int slot = it % kSlots;
+      if (lane == 0 && it >= kSlots) mbar_wait(&tempty[slot], ((it / kSlots) - 1) & 1);
+      __syncwarp();
+      if (tile >= args.total_tiles) {
+        if (lane == 0) {
+          tinfo[slot] = tile;
+          mbar_arrive(&tfull[slot]);
+        }
+        break;
+      }
+      const int pi = __ldg(args.tile_prod + tile);
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(args.gp + pi);
+      uint32_t* dst = reinterpret_cast<uint32_t*>(pdesc_raw) + slot * (sizeof(PD) / 4);
+      for (int i = lane; i < (int)(sizeof(PD) / 4); i += 32) dst[i] = __ldg(src + i);
+      __syncwarp();
+      const PD& P = *reinterpret_cast<const PD*>(dst);
+      const int local = tile - P.tile_begin;
+      int ti, tj;
+      if (P.kind == kSyrk) {
+        int r = (int)((sqrt(8.0 * (double)local + 1.0) - 1.0) * 0.5);
+        while ((r + 1) * (r + 2) / 2 <= local) ++r;
+        while (r * (r + 1) / 2 > local) --r;
+        ti = r;
+        tj = local - r * (r + 1) / 2;
+      } else {
+        const int per_group = 8 * P.tk;
+        const int grp = local / per_group;
+        const int first = grp * 8;
+        const int gsz = min(P.tn - first, 8);
+        const int in = local - grp * per_group;
+        ti = first + in % gsz;
+        tj = in / gsz;
+      }
+      const bool same = P.kind == kSyrk && ti == tj;
+      const int KT = (P.m + BK - 1) / BK;
+      if (lane == 0) {
+        tinfo[slot] = tile;
+        tdec[slot][0] = pi;
+        tdec[slot][1] = ti;
+        tdec[slot][2] = tj;
+        mbar_arrive(&tfull[slot]);   // release: descriptor copy and decoded tile
+        const CUtensorMap* ms = args.maps + 2 * pi;
+        const CUtensorMap* mt = P.kind == kSyrk ? ms : ms + 1;
+        const uint32_t bytes = same ? BUF_BYTES : 2 * BUF_BYTES;
+        for (int kt = 0; kt < KT; ++kt, ++kstep) {
+          const int s = kstep % STAGES;
+          if (kstep >= STAGES) mbar_wait(&empty[s], ((kstep / STAGES) - 1) & 1);
+          const uint32_t bar = smem_u32(&full[s]);
+          asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
+                       : "memory");
+          const uint32_t base = smem_u32(smem + s * STAGE_BYTES);
+          tma_load_3d(base, ms, 0, kt * BK, ti * (BM / 16), bar);
+          if (!same) tma_load_3d(base + BUF_BYTES, mt, 0, kt * BK, tj * (BN / 16), bar);
+        }
+      }
+      kstep = __shfl_sync(0xffffffffu, kstep, 0);
+    }
+    return;
+  }
+
+  // ===================== consumer warpgroups =====================
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(CONSUMER_REGS));
+  const int ctid = tid - PRODUCERS;
+  const int cw = warp - PRODUCERS / 32;
+  const int wm = cw >> 2, wn = cw & 3;
+  const int g = lane >> 2, q = lane & 3;
+  // per-lane fragment offsets inside an operand k-block (see the header note):
+  // [k-step parity][block parity]; the rest is compile-time
+  uint32_t aoff[2][2], boff[2][2];
+#pragma unroll
+  for (int jp = 0; jp < 2; ++jp)
+#pragma unroll
+    for (int rp = 0; rp < 2; ++rp) {
+      const int x = 2 * q + jp;
+      const int chunk = (rp * 4 + (g >> 1)) ^ x;
+      const uint32_t in_atom = x * 128 + chunk * 16 + (g & 1) * 8;
+      aoff[jp][rp] = (wm * (WTM / 2)) * BK * 128 + in_atom;
+      boff[jp][rp] = (wn * (WTN / 2)) * BK * 128 + in_atom;
+    }
+  const uint32_t smem0 = smem_u32(smem);
+  int kstep = 0;
+  for (int it = 0;; ++it) {
+    const int slot = it % kSlots;
+    mbar_wait(&tfull[slot], (it / kSlots) & 1);
+    const int tile = tinfo[slot];
+    if (tile >= args.total_tiles) break;
+    TileInfo tl;
+    tl.pi = tdec[slot][0];
+    tl.ti = tdec[slot][1];
+    tl.tj = tdec[slot][2];
+    const PD& P = *reinterpret_cast<const PD*>(pdesc_raw + slot * sizeof(PD));
+    const bool same = P.kind == kSyrk && tl.ti == tl.tj;
+    const int KT = (P.m + BK - 1) / BK;
+    double acc[WTM][WTN][2];
+#pragma unroll
+    for (int r = 0; r < WTM; ++r)
+#pragma unroll
+      for (int c = 0; c < WTN; ++c) acc[r][c][0] = acc[r][c][1] = 0.0;
+    const uint32_t bsel = same ? 0u : (uint32_t)BUF_BYTES;
+    for (int kt = 0; kt < KT; ++kt, ++kstep) {
+      const int s = kstep % STAGES;
+      mbar_wait(&full[s], (kstep / STAGES) & 1);
+      const uint32_t As = smem0 + s * STAGE_BYTES;
+      const uint32_t Bs = As + bsel;
+#pragma unroll
+      for (int j = 0; j < BK / 4; ++j) {
+        double a[WTM], b[WTN];
+#pragma unroll
+        for (int r = 0; r < WTM; ++r)
+          a[r] = lds64(As + aoff[j & 1][r & 1] + (r >> 1) * BK * 128 + (j >> 1) * 1024);
+#pragma unroll
+        for (int c = 0; c < WTN; ++c)
+          b[c] = lds64(Bs + boff[j & 1][c & 1] + (c >> 1) * BK * 128 + (j >> 1) * 1024);
+#pragma unroll
+        for (int r = 0; r < WTM; ++r)
+#pragma unroll
+          for (int c = 0; c < WTN; ++c) dmma_ws(acc[r][c], a[r], b[c]);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[s]);
+    }
+    ws_epilogue(args, P, tl, acc, wm, wn, g, q, ctid);
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&tempty[slot]);
+  }
+}
+
 // ---- device-resident descriptors (BatchArgsG) ----
 namespace {
 struct DescEntry {
@@ -689,6 +936,51 @@ uint64_t blob_hash(const unsigned char* p, size_t n) {  // 64-bit words (blobs a
 }
 }  // namespace
 
+// Device copy of a launch's descriptor blob, cached by content (repeated plans
+// hit it; entries used while a graph is captured are pinned for the graph's
+// lifetime).  cudaErrorNotReady: not resident and the stream is capturing.
+static cudaError_t resident_blob(std::vector<unsigned char>& blob, cudaStream_t s, void** dev) {
+  std::lock_guard<std::mutex> lock(desc_mutex());
+  DescCache& cache = desc_cache();
+  const uint64_t key = blob_hash(blob.data(), blob.size());
+  auto it = cache.map.find(key);
+  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+  cudaStreamIsCapturing(s, &cs);
+  const bool capturing = cs != cudaStreamCaptureStatusNone;
+  if (it == cache.map.end() || it->second.host != blob) {
+    if (capturing) return cudaErrorNotReady;  // no uploads inside a capture
+    if (it != cache.map.end()) {  // hash collision: replace
+      if (it->second.pinned) return cudaErrorNotReady;  // a live graph holds the colliding entry: narrow batches
+      cudaFree(it->second.dev);
+      cache.bytes -= it->second.host.size();
+      cache.map.erase(it);
+    }
+    // evict least recently used unpinned entries beyond 256 MB
+    while (cache.bytes + blob.size() > (256u << 20)) {
+      auto lru = cache.map.end();
+      for (auto j = cache.map.begin(); j != cache.map.end(); ++j)
+        if (!j->second.pinned && (lru == cache.map.end() || j->second.last_use < lru->second.last_use)) lru = j;
+      if (lru == cache.map.end()) break;  // everything left is held by graphs
+      cudaDeviceSynchronize();  // the evicted buffer may be in use by queued work on any stream
+      cudaFree(lru->second.dev);
+      cache.bytes -= lru->second.host.size();
+      cache.map.erase(lru);
+    }
+    DescEntry ent;
+    cudaError_t e = cudaMalloc(&ent.dev, blob.size());
+    if (e != cudaSuccess) return e;
+    e = cudaMemcpy(ent.dev, blob.data(), blob.size(), cudaMemcpyHostToDevice);
+    if (e != cudaSuccess) return e;
+    ent.host = std::move(blob);
+    cache.bytes += ent.host.size();
+    it = cache.map.emplace(key, std::move(ent)).first;
+  }
+  it->second.last_use = ++cache.clock;
+  if (capturing) it->second.pinned = true;
+  *dev = it->second.dev;
+  return cudaSuccess;
+}
+
 cudaError_t launch_batch_f64_global(DProdT<double, kNarrowDests>* prods, int count, double alpha, int* sync,
                                     cudaStream_t s) {
   using namespace ws64;
@@ -715,43 +1007,8 @@ cudaError_t launch_batch_f64_global(DProdT<double, kNarrowDests>* prods, int cou
     const long long nt_i = p.kind == kSyrk ? (long long)p.tn * (p.tn + 1) / 2 : (long long)p.tn * p.tk;
     for (long long t = 0; t < nt_i; ++t) tp[p.tile_begin + t] = i;
   }
-  std::lock_guard<std::mutex> lock(desc_mutex());
-  DescCache& cache = desc_cache();
-  const uint64_t key = blob_hash(blob.data(), blob.size());
-  auto it = cache.map.find(key);
-  cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-  cudaStreamIsCapturing(s, &cs);
-  const bool capturing = cs != cudaStreamCaptureStatusNone;
-  if (it == cache.map.end() || it->second.host != blob) {
-    if (capturing) return cudaErrorNotReady;  // no uploads inside a capture
-    if (it != cache.map.end()) {  // hash collision: replace
-      if (it->second.pinned) return cudaErrorNotReady;  // a live graph holds the colliding entry: narrow batches
-      cudaFree(it->second.dev);
-      cache.bytes -= it->second.host.size();
-      cache.map.erase(it);
-    }
-    // evict least recently used unpinned entries beyond 256 MB
-    while (cache.bytes + blob.size() > (256u << 20)) {
-      auto lru = cache.map.end();
-      for (auto j = cache.map.begin(); j != cache.map.end(); ++j)
-        if (!j->second.pinned && (lru == cache.map.end() || j->second.last_use < lru->second.last_use)) lru = j;
-      if (lru == cache.map.end()) break;  // everything left is held by graphs
-      cudaDeviceSynchronize();  // the evicted buffer may be in use by queued work on any stream  // the evicted buffer may be in use by queued work
-      cudaFree(lru->second.dev);
-      cache.bytes -= lru->second.host.size();
-      cache.map.erase(lru);
-    }
-    DescEntry ent;
-    cudaError_t e = cudaMalloc(&ent.dev, blob.size());
-    if (e != cudaSuccess) return e;
-    e = cudaMemcpy(ent.dev, blob.data(), blob.size(), cudaMemcpyHostToDevice);
-    if (e != cudaSuccess) return e;
-    ent.host = std::move(blob);
-    cache.bytes += ent.host.size();
-    it = cache.map.emplace(key, std::move(ent)).first;
-  }
-  it->second.last_use = ++cache.clock;
-  if (capturing) it->second.pinned = true;
+  void* dev_blob = nullptr;
+  if (cudaError_t e = resident_blob(blob, s, &dev_blob); e != cudaSuccess) return e;
   BatchArgsGlobal64 a;
   std::memset(&a, 0, sizeof(a));
   a.count = count;
@@ -766,8 +1023,8 @@ cudaError_t launch_batch_f64_global(DProdT<double, kNarrowDests>* prods, int cou
     if (e != cudaSuccess) return e;
   }
   { const char* e = std::getenv("ATA_DBG"); a.dbg = e ? std::atoi(e) : 0; }
-  a.gp = reinterpret_cast<const DProdT<double, kNarrowDests>*>(it->second.dev);
-  a.tile_prod = reinterpret_cast<const int*>(reinterpret_cast<const unsigned char*>(it->second.dev) + dbytes);
+  a.gp = reinterpret_cast<const DProdT<double, kNarrowDests>*>(dev_blob);
+  a.tile_prod = reinterpret_cast<const int*>(reinterpret_cast<const unsigned char*>(dev_blob) + dbytes);
 #ifndef WSG_BK
 #define WSG_BK 16   // k-block rows of single-term device-descriptor batches
 #endif
@@ -777,5 +1034,145 @@ cudaError_t launch_batch_f64_global(DProdT<double, kNarrowDests>* prods, int cou
   return ws_kernel_launch<WS2_BK, 2, 2>(a, total, s);
 }
 cudaError_t launch_batch_f64_ws_narrow(const BatchArgsNarrow64& a, cudaStream_t s) { return launch_ws_any(a, s); }
+
+// ---- TMA-fed launches (prod_f64_tma_kernel) ----
+static PFN_cuTensorMapEncodeTiled_v12000 f64_encoder() {
+  static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+  if (enc == nullptr) {
+    cudaDriverEntryPointQueryResult q;
+    void* p = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      return nullptr;
+    enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  }
+  return enc;
+}
+
+// A window as [panels][rows][16 doubles] (panel stride 128 B), boxes of
+// [BM/16 panels][BK rows][16] with the 128-byte swizzle; rows and panels
+// outside the window are zero-filled.
+static bool f64_map_term(CUtensorMap* map, const DTerm<double>& t) {
+  auto enc = f64_encoder();
+  if (enc == nullptr) return false;
+  cuuint64_t dims[3] = {16, (cuuint64_t)t.rows, (cuuint64_t)(t.cols / 16)};
+  cuuint64_t strides[2] = {(cuuint64_t)t.ld * 8, 128};
+  cuuint32_t box[3] = {16, wst::BK, wst::PANELS};
+  cuuint32_t estr[3] = {1, 1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(t.p), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static bool tma_term_ok(const DTerm<double>& t) {
+  return (reinterpret_cast<uintptr_t>(t.p) & 15) == 0 && (t.ld & 1) == 0 && t.cols % 16 == 0 && t.rows >= 1 &&
+         t.cols >= 16 && t.sign == 1.0;
+}
+
+bool f64_tma_eligible(const DProdT<double, kNarrowDests>* prods, int count) {
+  static const int mode = [] {
+    const char* e = std::getenv("ATA_F64_TMA");
+    return e ? std::atoi(e) : 1;
+  }();
+  if (mode == 0 || f64_encoder() == nullptr) return false;
+  for (int i = 0; i < count; ++i) {
+    const auto& p = prods[i];
+    if (p.ns != 1 || !tma_term_ok(p.s[0])) return false;
+    if (p.kind != kSyrk && (p.nt != 1 || !tma_term_ok(p.t[0]))) return false;
+  }
+  return true;
+}
+
+cudaError_t launch_batch_f64_tma(DProdT<double, kNarrowDests>* prods, int count, double alpha, int* sync,
+                                 long long sync_ints, cudaStream_t s) {
+  using namespace ws64;
+  long long total = 0;
+  for (int i = 0; i < count; ++i) {
+    auto& p = prods[i];
+    p.tn = (p.n + BM - 1) / BM;
+    p.tk = (p.k + BN - 1) / BN;
+    p.tile_begin = (int)total;
+    total += p.kind == kSyrk ? (long long)p.tn * (p.tn + 1) / 2 : (long long)p.tn * p.tk;
+  }
+  if (total <= 0) return cudaSuccess;
+  if (total > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
+  // destination regions (DDest.sem = batch-local region id, 1-based; 0 = none):
+  // per-tile turn counters at sync[1..], as in launch_ws
+  const int nreg = count * kNarrowDests;
+  std::vector<int> rbase(nreg, -1), rld(nreg, 0), rrows(nreg, 0), rseen(nreg, 0);
+  for (int i = 0; i < count; ++i)
+    for (int d = 0; d < prods[i].nd; ++d) {
+      const int rg = prods[i].d[d].sem;
+      if (rg <= 0 || rg > nreg) continue;
+      rld[rg - 1] = max(rld[rg - 1], prods[i].tk);
+      rrows[rg - 1] = max(rrows[rg - 1], prods[i].tn);
+    }
+  long long n_sync = 1;
+  for (int r = 0; r < nreg; ++r)
+    if (rld[r] > 0) {
+      rbase[r] = (int)n_sync;
+      n_sync += (long long)rld[r] * rrows[r];
+    }
+  for (int i = 0; i < count; ++i)
+    for (int d = 0; d < prods[i].nd; ++d) {
+      DDest<double>& D = prods[i].d[d];
+      const int rg = D.sem;
+      if (rg <= 0 || rg > nreg) {
+        D.sem = -1;
+        continue;
+      }
+      D.sem = rbase[rg - 1];
+      D.sem_ld = rld[rg - 1];
+      D.turn = rseen[rg - 1]++;
+    }
+  // dynamic tile queue (tiles still start in increasing order): groups mix
+  // tiles of very different contraction lengths (merged diagonal SYRKs, tail
+  // chunks); ATA_F64_TMA_STATIC=1 selects the static round-robin
+  static const bool force_static = std::getenv("ATA_F64_TMA_STATIC") != nullptr;
+  const bool dynamic = n_sync > 1 || (sync != nullptr && sync_ints >= 1 && !force_static);
+  if (dynamic && (sync == nullptr || n_sync > sync_ints)) return cudaErrorInvalidValue;
+  // blob: tensor maps (64-byte aligned), descriptors, tile -> product table
+  const size_t mbytes = sizeof(CUtensorMap) * 2 * (size_t)count;
+  const size_t dbytes = sizeof(DProdT<double, kNarrowDests>) * (size_t)count;
+  std::vector<unsigned char> blob(mbytes + dbytes + ((sizeof(int) * (size_t)total + 7) & ~size_t(7)), 0);
+  CUtensorMap* maps = reinterpret_cast<CUtensorMap*>(blob.data());
+  for (int i = 0; i < count; ++i) {
+    if (!f64_map_term(&maps[2 * i], prods[i].s[0])) return cudaErrorNotSupported;
+    if (prods[i].kind != kSyrk && !f64_map_term(&maps[2 * i + 1], prods[i].t[0])) return cudaErrorNotSupported;
+  }
+  std::memcpy(blob.data() + mbytes, prods, dbytes);
+  int* tp = reinterpret_cast<int*>(blob.data() + mbytes + dbytes);
+  for (int i = 0; i < count; ++i) {
+    const auto& p = prods[i];
+    const long long nt_i = p.kind == kSyrk ? (long long)p.tn * (p.tn + 1) / 2 : (long long)p.tn * p.tk;
+    for (long long t = 0; t < nt_i; ++t) tp[p.tile_begin + t] = i;
+  }
+  void* dev = nullptr;
+  if (cudaError_t e = resident_blob(blob, s, &dev); e != cudaSuccess) return e;
+  TmaBatch64 a;
+  std::memset(&a, 0, sizeof(a));
+  a.count = count;
+  a.total_tiles = (int)total;
+  a.alpha = alpha;
+  a.sync = sync;
+  a.n_sync = (int)n_sync;
+  a.dynamic = dynamic ? 1 : 0;
+  { const char* e = std::getenv("ATA_DBG"); a.dbg = e ? std::atoi(e) : 0; }
+  a.maps = reinterpret_cast<const CUtensorMap*>(dev);
+  a.gp = reinterpret_cast<const DProdT<double, kNarrowDests>*>(reinterpret_cast<const unsigned char*>(dev) + mbytes);
+  a.tile_prod = reinterpret_cast<const int*>(reinterpret_cast<const unsigned char*>(dev) + mbytes + dbytes);
+  if (dynamic) {
+    cudaError_t e = cudaMemsetAsync(sync, 0, (size_t)n_sync * sizeof(int), s);
+    if (e != cudaSuccess) return e;
+  }
+  const size_t smem = 1024 + (size_t)wst::STAGES * wst::STAGE_BYTES + (2 * wst::STAGES + 2 * 3) * sizeof(uint64_t) +
+                      4 * sizeof(int);
+  static std::atomic<unsigned long long> attr_set{0};
+  if (cudaError_t e = ata::set_smem_attr(prod_f64_tma_kernel, smem, attr_set); e != cudaSuccess) return e;
+  const int grid = (int)(total < num_sms() ? total : num_sms());
+  prod_f64_tma_kernel<<<grid, THREADS, smem, s>>>(a);
+  return cudaGetLastError();
+}
+
 
 }  // namespace ata
