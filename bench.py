@@ -557,6 +557,12 @@ def main():
                                              "share_of_step": l2_ms / unit_total_ms if unit_total_ms else None,
                                              "gbs": l2_elems * A.element_size() / (l2_ms * 1e-3) / 1e9
                                              if l2_ms > 0 else None}}
+    # the peaks are issue rates at the 1965 MHz boost clock; a power-capped run
+    # (sw_power_cap, c5) holds a lower clock: the same frac at the measured clock
+    sm_mhz, sm_max = clk.summary.get("sm_mhz"), clk.summary.get("sm_max_mhz")
+    if sm_mhz and sm_max:
+        roofline["frac_at_measured_clock"] = achieved / (peak * sm_mhz / sm_max)
+        roofline["measured_clock_mhz"] = sm_mhz
     line = {"metric": METRIC, "value": value, "unit": "GFLOP/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_step,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
