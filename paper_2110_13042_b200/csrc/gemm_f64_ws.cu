@@ -690,14 +690,21 @@ cudaError_t launch_batch_f64_ws(const BatchArgs<double>& a, cudaStream_t s) { re
 // ===========================================================================
 namespace wst {
 #ifndef WST_BK
-#define WST_BK 32
+#define WST_BK 32     // k-block rows, single-term launches
 #endif
-constexpr int BK = WST_BK;
+#ifndef WST_BK2
+#define WST_BK2 16    // k-block rows, launches with two-term (fused Strassen sum) operands
+#endif
 constexpr int PANELS = ws64::BM / 16;              // 16 doubles = one 128-byte swizzle row
-constexpr int BUF_BYTES = BK * 128 * PANELS;       // one operand k-block
-constexpr int STAGE_BYTES = 2 * BUF_BYTES;
-constexpr int STAGES = (ws64::SMEM_BUDGET - 2048) / STAGE_BYTES > 6 ? 6 : (ws64::SMEM_BUDGET - 2048) / STAGE_BYTES;
-static_assert(BK % 8 == 0 && STAGES >= 2, "TMA k-block");
+template <int BK>
+constexpr int buf_bytes() { return BK * 128 * PANELS; }   // one operand term, one k-block
+template <int BK, int NS, int NT>
+constexpr int stage_bytes() { return (NS + NT) * buf_bytes<BK>(); }
+template <int BK, int NS, int NT>
+constexpr int stages() {
+  return (ws64::SMEM_BUDGET - 2048) / stage_bytes<BK, NS, NT>() > 6 ? 6
+                                                                  : (ws64::SMEM_BUDGET - 2048) / stage_bytes<BK, NS, NT>();
+}
 }  // namespace wst
 
 struct TmaBatch64 {
@@ -730,12 +737,17 @@ __device__ __forceinline__ double lds64(uint32_t addr) {
   return v;
 }
 
+// NS / NT: operand terms per side (2: a Strassen operand sum X + s Y read as two
+// zero-extended windows and added as the fragments are loaded -- the pre-addition
+// fused into the product, no operand-sum buffer in HBM).  Products with fewer
+// terms than the launch's NS / NT run in the same launch.
+template <int BK, int NS, int NT>
 __global__ void __launch_bounds__(ws64::THREADS, 1) prod_f64_tma_kernel(const __grid_constant__ TmaBatch64 args) {
   using namespace ws64;
-  using wst::BK;
-  using wst::BUF_BYTES;
-  using wst::STAGE_BYTES;
-  using wst::STAGES;
+  constexpr int BUF_BYTES = wst::buf_bytes<BK>();
+  constexpr int STAGE_BYTES = wst::stage_bytes<BK, NS, NT>();
+  constexpr int STAGES = wst::stages<BK, NS, NT>();
+  static_assert(BK % 8 == 0 && STAGES >= 2, "TMA k-block");
   using PD = DProdT<double, kNarrowDests>;
   constexpr int kSlots = 3;
   extern __shared__ uint8_t tma_raw[];
@@ -814,9 +826,11 @@ __global__ void __launch_bounds__(ws64::THREADS, 1) prod_f64_tma_kernel(const __
         tdec[slot][1] = ti;
         tdec[slot][2] = tj;
         mbar_arrive(&tfull[slot]);   // release: descriptor copy and decoded tile
-        const CUtensorMap* ms = args.maps + 2 * pi;
-        const CUtensorMap* mt = P.kind == kSyrk ? ms : ms + 1;
-        const uint32_t bytes = same ? BUF_BYTES : 2 * BUF_BYTES;
+        // maps of product pi: [S0, S1, T0, T1] (4 per product)
+        const CUtensorMap* ms = args.maps + 4 * pi;
+        const CUtensorMap* mt = P.kind == kSyrk ? ms : ms + 2;
+        const int ns = NS == 2 ? P.ns : 1, nt = P.kind == kSyrk ? ns : (NT == 2 ? P.nt : 1);
+        const uint32_t bytes = (same ? ns : ns + nt) * BUF_BYTES;
         for (int kt = 0; kt < KT; ++kt, ++kstep) {
           const int s = kstep % STAGES;
           if (kstep >= STAGES) mbar_wait(&empty[s], ((kstep / STAGES) - 1) & 1);
@@ -825,7 +839,12 @@ __global__ void __launch_bounds__(ws64::THREADS, 1) prod_f64_tma_kernel(const __
                        : "memory");
           const uint32_t base = smem_u32(smem + s * STAGE_BYTES);
           tma_load_3d(base, ms, 0, kt * BK, ti * (BM / 16), bar);
-          if (!same) tma_load_3d(base + BUF_BYTES, mt, 0, kt * BK, tj * (BN / 16), bar);
+          if (NS == 2 && ns == 2) tma_load_3d(base + BUF_BYTES, ms + 1, 0, kt * BK, ti * (BM / 16), bar);
+          if (!same) {
+            tma_load_3d(base + NS * BUF_BYTES, mt, 0, kt * BK, tj * (BN / 16), bar);
+            if (NT == 2 && nt == 2)
+              tma_load_3d(base + (NS + 1) * BUF_BYTES, mt + 1, 0, kt * BK, tj * (BN / 16), bar);
+          }
         }
       }
       kstep = __shfl_sync(0xffffffffu, kstep, 0);
@@ -871,7 +890,12 @@ __global__ void __launch_bounds__(ws64::THREADS, 1) prod_f64_tma_kernel(const __
     for (int r = 0; r < WTM; ++r)
 #pragma unroll
       for (int c = 0; c < WTN; ++c) acc[r][c][0] = acc[r][c][1] = 0.0;
-    const uint32_t bsel = same ? 0u : (uint32_t)BUF_BYTES;
+    const uint32_t bsel = same ? 0u : (uint32_t)(NS * BUF_BYTES);
+    // second terms: S1 / T1 one buffer after S0 / T0, added with their signs
+    const bool two_a = NS == 2 && P.ns == 2;
+    const bool two_b = same ? two_a : (NT == 2 && P.kind != kSyrk && P.nt == 2);
+    const double sa = two_a ? P.s[1].sign : 0.0;
+    const double sb = same ? sa : (two_b ? P.t[1].sign : 0.0);
     for (int kt = 0; kt < KT; ++kt, ++kstep) {
       const int s = kstep % STAGES;
       mbar_wait(&full[s], (kstep / STAGES) & 1);
@@ -886,6 +910,16 @@ __global__ void __launch_bounds__(ws64::THREADS, 1) prod_f64_tma_kernel(const __
 #pragma unroll
         for (int c = 0; c < WTN; ++c)
           b[c] = lds64(Bs + boff[j & 1][c & 1] + (c >> 1) * BK * 128 + (j >> 1) * 1024);
+        if (NS == 2 && two_a) {
+#pragma unroll
+          for (int r = 0; r < WTM; ++r)
+            a[r] = fma(sa, lds64(As + BUF_BYTES + aoff[j & 1][r & 1] + (r >> 1) * BK * 128 + (j >> 1) * 1024), a[r]);
+        }
+        if ((NS == 2 || NT == 2) && two_b) {
+#pragma unroll
+          for (int c = 0; c < WTN; ++c)
+            b[c] = fma(sb, lds64(Bs + BUF_BYTES + boff[j & 1][c & 1] + (c >> 1) * BK * 128 + (j >> 1) * 1024), b[c]);
+        }
 #pragma unroll
         for (int r = 0; r < WTM; ++r)
 #pragma unroll
@@ -1052,21 +1086,21 @@ static PFN_cuTensorMapEncodeTiled_v12000 f64_encoder() {
 // A window as [panels][rows][16 doubles] (panel stride 128 B), boxes of
 // [BM/16 panels][BK rows][16] with the 128-byte swizzle; rows and panels
 // outside the window are zero-filled.
-static bool f64_map_term(CUtensorMap* map, const DTerm<double>& t) {
+static bool f64_map_term(CUtensorMap* map, const DTerm<double>& t, int bk) {
   auto enc = f64_encoder();
   if (enc == nullptr) return false;
   cuuint64_t dims[3] = {16, (cuuint64_t)t.rows, (cuuint64_t)(t.cols / 16)};
   cuuint64_t strides[2] = {(cuuint64_t)t.ld * 8, 128};
-  cuuint32_t box[3] = {16, wst::BK, wst::PANELS};
+  cuuint32_t box[3] = {16, (cuuint32_t)bk, wst::PANELS};
   cuuint32_t estr[3] = {1, 1, 1};
   return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 3, const_cast<double*>(t.p), dims, strides, box, estr,
              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-static bool tma_term_ok(const DTerm<double>& t) {
+static bool tma_term_ok(const DTerm<double>& t, bool first) {
   return (reinterpret_cast<uintptr_t>(t.p) & 15) == 0 && (t.ld & 1) == 0 && t.cols % 16 == 0 && t.rows >= 1 &&
-         t.cols >= 16 && t.sign == 1.0;
+         t.cols >= 16 && (!first || t.sign == 1.0);
 }
 
 bool f64_tma_eligible(const DProdT<double, kNarrowDests>* prods, int count) {
@@ -1077,10 +1111,27 @@ bool f64_tma_eligible(const DProdT<double, kNarrowDests>* prods, int count) {
   if (mode == 0 || f64_encoder() == nullptr) return false;
   for (int i = 0; i < count; ++i) {
     const auto& p = prods[i];
-    if (p.ns != 1 || !tma_term_ok(p.s[0])) return false;
-    if (p.kind != kSyrk && (p.nt != 1 || !tma_term_ok(p.t[0]))) return false;
+    if (p.ns < 1 || p.ns > 2 || !tma_term_ok(p.s[0], true) || (p.ns == 2 && !tma_term_ok(p.s[1], false)))
+      return false;
+    if (p.kind == kSyrk && p.ns != 1) return false;
+    if (p.kind != kSyrk && (p.nt < 1 || p.nt > 2 || !tma_term_ok(p.t[0], true) ||
+                            (p.nt == 2 && !tma_term_ok(p.t[1], false))))
+      return false;
   }
   return true;
+}
+
+template <int BK, int NS, int NT>
+static cudaError_t tma_kernel_launch(const TmaBatch64& a, long long total, cudaStream_t s) {
+  constexpr int STAGES = wst::stages<BK, NS, NT>();
+  const size_t smem = 1024 + (size_t)STAGES * wst::stage_bytes<BK, NS, NT>() + (2 * STAGES + 2 * 3) * sizeof(uint64_t) +
+                      4 * sizeof(int);
+  auto kern = prod_f64_tma_kernel<BK, NS, NT>;
+  static std::atomic<unsigned long long> attr_set{0};
+  if (cudaError_t e = ata::set_smem_attr(kern, smem, attr_set); e != cudaSuccess) return e;
+  const int grid = (int)(total < num_sms() ? total : num_sms());
+  kern<<<grid, ws64::THREADS, smem, s>>>(a);
+  return cudaGetLastError();
 }
 
 cudaError_t launch_batch_f64_tma(DProdT<double, kNarrowDests>* prods, int count, double alpha, int* sync,
@@ -1132,13 +1183,23 @@ cudaError_t launch_batch_f64_tma(DProdT<double, kNarrowDests>* prods, int count,
   const bool dynamic = n_sync > 1 || (sync != nullptr && sync_ints >= 1 && !force_static);
   if (dynamic && (sync == nullptr || n_sync > sync_ints)) return cudaErrorInvalidValue;
   // blob: tensor maps (64-byte aligned), descriptors, tile -> product table
-  const size_t mbytes = sizeof(CUtensorMap) * 2 * (size_t)count;
+  const size_t mbytes = sizeof(CUtensorMap) * 4 * (size_t)count;
   const size_t dbytes = sizeof(DProdT<double, kNarrowDests>) * (size_t)count;
   std::vector<unsigned char> blob(mbytes + dbytes + ((sizeof(int) * (size_t)total + 7) & ~size_t(7)), 0);
   CUtensorMap* maps = reinterpret_cast<CUtensorMap*>(blob.data());
+  int ns = 1, nt = 1;
   for (int i = 0; i < count; ++i) {
-    if (!f64_map_term(&maps[2 * i], prods[i].s[0])) return cudaErrorNotSupported;
-    if (prods[i].kind != kSyrk && !f64_map_term(&maps[2 * i + 1], prods[i].t[0])) return cudaErrorNotSupported;
+    ns = max(ns, prods[i].ns);
+    if (prods[i].kind != kSyrk) nt = max(nt, prods[i].nt);
+  }
+  const int bk = (ns == 1 && nt == 1) ? WST_BK : WST_BK2;   // the box rows of the kernel that runs
+  for (int i = 0; i < count; ++i) {
+    const auto& p = prods[i];
+    for (int j = 0; j < p.ns; ++j)
+      if (!f64_map_term(&maps[4 * i + j], p.s[j], bk)) return cudaErrorNotSupported;
+    if (p.kind != kSyrk)
+      for (int j = 0; j < p.nt; ++j)
+        if (!f64_map_term(&maps[4 * i + 2 + j], p.t[j], bk)) return cudaErrorNotSupported;
   }
   std::memcpy(blob.data() + mbytes, prods, dbytes);
   int* tp = reinterpret_cast<int*>(blob.data() + mbytes + dbytes);
@@ -1165,13 +1226,10 @@ cudaError_t launch_batch_f64_tma(DProdT<double, kNarrowDests>* prods, int count,
     cudaError_t e = cudaMemsetAsync(sync, 0, (size_t)n_sync * sizeof(int), s);
     if (e != cudaSuccess) return e;
   }
-  const size_t smem = 1024 + (size_t)wst::STAGES * wst::STAGE_BYTES + (2 * wst::STAGES + 2 * 3) * sizeof(uint64_t) +
-                      4 * sizeof(int);
-  static std::atomic<unsigned long long> attr_set{0};
-  if (cudaError_t e = ata::set_smem_attr(prod_f64_tma_kernel, smem, attr_set); e != cudaSuccess) return e;
-  const int grid = (int)(total < num_sms() ? total : num_sms());
-  prod_f64_tma_kernel<<<grid, THREADS, smem, s>>>(a);
-  return cudaGetLastError();
+  if (ns == 1 && nt == 1) return tma_kernel_launch<WST_BK, 1, 1>(a, total, s);
+  if (ns == 2 && nt == 1) return tma_kernel_launch<WST_BK2, 2, 1>(a, total, s);
+  if (ns == 1 && nt == 2) return tma_kernel_launch<WST_BK2, 1, 2>(a, total, s);
+  return tma_kernel_launch<WST_BK2, 2, 2>(a, total, s);
 }
 
 

@@ -67,7 +67,8 @@ def test_auto_plan_vs_oracle(shape, rng):
     from paper_2110_13042_b200.auto_plan import AutoParams
     a = rng.standard_normal(shape)
     n = shape[1]
-    for params in (AutoParams(), AutoParams(leaf_cols=256, min_dim=128, hbm_gbs=1e9)):
+    for params in (AutoParams(), AutoParams(leaf_cols=256, min_dim=128, hbm_gbs=1e9),
+                   AutoParams(leaf_cols=256, min_dim=128, hbm_gbs=1e9, fuse_leaf_sums=True)):
         A = torch.from_numpy(a).cuda()
         C = torch.triu(torch.full((n, n), 7.0, dtype=torch.float64, device="cuda"), 1)
         P.ata(A, C, 1.0, threshold="auto", auto_params=params)
@@ -215,3 +216,61 @@ def test_reference_plan_graph_replay():
     assert len(set(counts)) == 1
     ref = O.gram_blas(a.cpu().numpy())
     assert O.rel_frobenius_lower(outs[-1], ref) <= 1e-12
+
+
+@pytest.mark.parametrize("kernel", ["tma", "cp.async"])
+def test_fused_leaf_sums_vs_oracle(kernel, monkeypatch, rng):
+    """Last Strassen level's operand sums read as two zero-extended quadrant
+    terms inside the product kernel (AutoParams.fuse_leaf_sums), on the
+    TMA-fed and the cp.async-fed FP64 kernels (the latter also takes windows
+    TMA cannot: odd pitches), odd and even shapes, against the oracle."""
+    torch = pytest.importorskip("torch")
+    import paper_2110_13042_b200 as P
+    from paper_2110_13042_b200 import auto_plan, engine
+    from paper_2110_13042_b200.auto_plan import AutoParams
+    params = AutoParams(leaf_cols=512, min_dim=128, hbm_gbs=1e9, fuse_leaf_sums=True, max_depth=3)
+    for shape in ((3000, 2048), (2501, 1537), (4096, 3001)):
+        a = rng.uniform(-1, 1, shape)
+        n = shape[1]
+        plan = auto_plan.plan_ata_auto(shape[0], n, n, n, params)
+        assert (plan.ops["ns"] == 2).any() or (plan.ops["nt"] == 2).any()   # fused operands present
+        A = torch.from_numpy(a).cuda()
+        C = torch.triu(torch.full((n, n), 7.0, dtype=torch.float64, device="cuda"), 1)
+        # the native library reads ATA_F64_TMA once per process: select the
+        # cp.async kernel through an odd pitch instead (TMA needs an even one)
+        if kernel == "cp.async":
+            ld = n + 1 if n % 2 == 0 else n + 2          # odd pitch
+            big = torch.zeros((shape[0], ld), dtype=torch.float64, device="cuda")
+            big[:, :n] = A
+            A = big[:, :n]
+        P.ata(A, C, 1.0, threshold="auto", auto_params=params)
+        got = C.cpu().numpy()
+        assert np.all(got[np.triu_indices(n, 1)] == 7.0)
+        assert O.rel_frobenius_lower(got, O.gram_blas(a)) <= 1e-13, shape
+    engine._PLAN_CACHE.clear()
+
+
+def test_reference_depth_first_executor(golden, monkeypatch):
+    """ATA_REF_DFS=1: the reference's own depth-first order with its per-depth
+    scratch (planner._ReferencePlanner) on the golden cases -- same exact
+    counts and results within tolerance as the reference run."""
+    import paper_2110_13042_b200 as P
+    from paper_2110_13042_b200 import engine
+    monkeypatch.setenv("ATA_REF_DFS", "1")
+    engine._PLAN_CACHE.clear()
+    meta, arrays = golden
+    done = 0
+    for case in meta["cases"]:
+        if case.get("kind") != "ata" or case["m"] * case["n"] > 200000:
+            continue
+        a = arrays[case["key"] + "_A"]
+        c = np.zeros((case["n"], case["n"]), dtype=a.dtype)
+        cnt = P.MultCounter()
+        P.ata(a, c, case["alpha"], threshold=case["threshold"], counter=cnt)
+        ref = arrays[case["key"] + "_C"]
+        tol = 1e-10 if a.dtype == np.float64 else 1e-4
+        assert O.rel_frobenius_lower(c, ref) <= tol, case["key"]
+        assert cnt.scalar_mults == case["mults"], case["key"]
+        done += 1
+    assert done >= 5
+    engine._PLAN_CACHE.clear()
