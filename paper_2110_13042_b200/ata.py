@@ -13,6 +13,7 @@ or anything the reference accepts (staged through the device).
 """
 from __future__ import annotations
 
+import dataclasses
 import os
 
 import numpy as np
@@ -253,9 +254,12 @@ def _pipelined_host_ata(a, c, m, n, alpha, ws, counter, auto_params, precision) 
     params = auto_params or auto_plan.AutoParams()
     blocks = []
     for (r0, rows) in _row_blocks(m, n, es, round_tf32 or es == 4):
-        key = ("ata-auto", rows, n, n, n, params, round_tf32)
+        # each block's plan takes the Strassen tree of the whole A (cost model at m
+        # rows): the blocks together execute the single plan's multiplications
+        bp = dataclasses.replace(params, cost_row_scale=params.cost_row_scale * m / rows)
+        key = ("ata-auto", rows, n, n, n, bp, round_tf32)
         blocks.append((r0, rows, engine.cached_plan(
-            key, lambda rows=rows: auto_plan.plan_ata_auto(rows, n, n, n, params, round_tf32=round_tf32))))
+            key, lambda rows=rows, bp=bp: auto_plan.plan_ata_auto(rows, n, n, n, bp, round_tf32=round_tf32))))
     need = max(p.ws_scalars for (_, _, p) in blocks)
     if ws is None:
         ws = workspace_for_ata(m, n, AUTO, dtype=c.dtype)

@@ -77,6 +77,10 @@ class AutoParams:
                                    # combo4 pass for the last Strassen level).  Off: measured
                                    # 2.1-2.2x slower on c3/c4 (the two-term kernel configuration
                                    # runs at 14 TF/s vs 34 for plain operands)
+    cost_row_scale: float = 1.0    # the cost model sees m * this many contraction rows: a row
+                                   # block of a larger A (the pinned-host pipeline) gets the
+                                   # Strassen tree of the whole A, so the blocks' executed
+                                   # multiplications add up to the single plan's
     tail_split: bool = True        # FP64: K-split a group's trailing products (partial last wave)
     min_tail_rows: int = 1024      # ... only when every chunk keeps this many rows
 
@@ -149,6 +153,7 @@ class _AutoPlanner:
     def worth_split(self, m: int, n: int, k: int, depth_left: int) -> bool:
         if depth_left <= 0 or min(n, k) < 2 * self.p.min_dim or m < 2:
             return False
+        m = m * self.p.cost_row_scale
         saved_s = 2.0 * m * n * k / 8 / (self.rate * 1e12)
         # pre: read both operands, write 5 + 5 quarter sums; post: write 7 child
         # products (leaf epilogue), read them back, write (or RMW) 4 quadrants
