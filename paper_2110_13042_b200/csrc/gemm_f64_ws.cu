@@ -989,8 +989,11 @@ static cudaError_t resident_blob(std::vector<unsigned char>& blob, cudaStream_t 
       cache.bytes -= it->second.host.size();
       cache.map.erase(it);
     }
-    // evict least recently used unpinned entries beyond 256 MB
-    while (cache.bytes + blob.size() > (256u << 20)) {
+    // evict least recently used unpinned entries beyond the budget (256 MB;
+    // ATA_DESC_CACHE_KB overrides it, read on every miss)
+    const char* lim_env = std::getenv("ATA_DESC_CACHE_KB");
+    const size_t limit = lim_env ? (size_t)std::atoll(lim_env) << 10 : (size_t)256 << 20;
+    while (cache.bytes + blob.size() > limit) {
       auto lru = cache.map.end();
       for (auto j = cache.map.begin(); j != cache.map.end(); ++j)
         if (!j->second.pinned && (lru == cache.map.end() || j->second.last_use < lru->second.last_use)) lru = j;

@@ -269,3 +269,38 @@ def test_tf32_l2_ring_under_sm_contention():
             x = (x @ x).clamp_(-1, 1)
     torch.cuda.synchronize()
     assert torch.equal(C0, C1)
+
+
+def test_graph_replay_survives_descriptor_cache_churn(monkeypatch):
+    """A CUDA graph captured over TMA / device-descriptor launches keeps the
+    descriptor blobs it baked in: entries used under capture are pinned, so a
+    later flood of other launches (with a tiny cache budget forcing eviction)
+    cannot free them, and replays stay bit-identical to the eager run."""
+    import torch
+    from paper_2110_13042_b200 import auto_plan, engine, _native as nat
+    m, n = 4096, 2048
+    params = auto_plan.AutoParams(leaf_cols=512, min_dim=128, hbm_gbs=1e9)
+    plan = auto_plan.plan_ata_auto(m, n, n, n, params)
+    A = torch.rand(m, n, dtype=torch.float64, device="cuda")
+    C = torch.zeros(n, n, dtype=torch.float64, device="cuda")
+    ws = torch.empty(max(1, plan.ws_scalars), dtype=torch.float64, device="cuda")
+    args = (plan, nat.ATA_F64, A.data_ptr(), A.numel(), C.data_ptr(), C.numel(), 1.0)
+    kw = dict(ws=ws.data_ptr(), ws_elems=ws.numel())
+    engine.run_plan(*args, **kw)                 # eager: blobs uploaded
+    torch.cuda.synchronize()
+    ref = C.clone()
+    g = engine.PlanGraph(*args, **kw)            # captured: blobs pinned
+    monkeypatch.setenv("ATA_DESC_CACHE_KB", "1")
+    for i in range(12):                          # churn: new blobs evict everything unpinned
+        Ai = torch.rand(m + 16 * (i + 1), n, dtype=torch.float64, device="cuda")
+        Ci = torch.zeros(n, n, dtype=torch.float64, device="cuda")
+        pi = auto_plan.plan_ata_auto(Ai.shape[0], n, n, n, params)
+        wi = torch.empty(max(1, pi.ws_scalars), dtype=torch.float64, device="cuda")
+        engine.run_plan(pi, nat.ATA_F64, Ai.data_ptr(), Ai.numel(), Ci.data_ptr(), Ci.numel(), 1.0,
+                        ws=wi.data_ptr(), ws_elems=wi.numel())
+    torch.cuda.synchronize()
+    for _ in range(2):
+        C.zero_()
+        g.replay()
+    torch.cuda.synchronize()
+    assert torch.equal(C, ref)
