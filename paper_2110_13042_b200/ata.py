@@ -136,6 +136,10 @@ PIPELINE_MIN_BYTES = 1 << 30      # host A at least this large: copy/compute pip
 PIPELINE_BLOCK_BYTES = 4 << 30    # ~ bytes of A per row block (PCIe-bound TF32 plans)
 PIPELINE_GEOMETRIC = True         # compute-bound plans: geometric row blocks (_row_blocks)
 PIPELINE_ZERO_C = bool(int(os.environ.get("ATA_PIPE_ZERO_C", "1")))   # device C starts at zero (_pipelined_host_ata)
+# zero-start C: add the caller's C tile group by tile group right before each
+# group's download (its upload then overlaps the last block's compute) instead
+# of one whole-square add before the last block
+PIPELINE_LATE_C_ADD = bool(int(os.environ.get("ATA_PIPE_LATE_C_ADD", "1")))
 _PIPE_CIN: dict = {}   # the staged host-C buffer of the pipeline, one per (device, n, dtype)
 PIPELINE_GEOMETRIC_MIN_RATIO = 4.0    # PIPELINE_GEOMETRIC_BLOCKS geometric blocks from here
 PIPELINE_GEOMETRIC_MIN_RATIO2 = 2.0   # two geometric blocks from here
@@ -312,7 +316,7 @@ def _pipelined_host_ata(a, c, m, n, alpha, ws, counter, auto_params, precision) 
         if i == 0 and not zero_start:
             cuts.append(_first_c_writer(ops))
         if i == last:
-            if zero_start:
+            if zero_start and not PIPELINE_LATE_C_ADD:
                 main.wait_event(c_ready)
                 engine.run_plan(_add_plan(n), code, int(dCin.data_ptr()), dCin.numel(), int(dC.data_ptr()),
                                 dC.numel(), 1.0)
@@ -329,6 +333,12 @@ def _pipelined_host_ata(a, c, m, n, alpha, ws, counter, auto_params, precision) 
             if i == 0 and not zero_start and cut == cuts[0]:
                 main.wait_event(c_ready)
             if cut in downloads:
+                if zero_start and PIPELINE_LATE_C_ADD:
+                    # the caller's C joins these final tiles just before they go home
+                    # (its upload ran behind the last block's compute, not before it)
+                    main.wait_event(c_ready)
+                    engine.run_plan(_add_tiles_plan(n, downloads[cut]), code, int(dCin.data_ptr()), dCin.numel(),
+                                    int(dC.data_ptr()), dC.numel(), 1.0)
                 ev = torch.cuda.Event()
                 ev.record(main)
                 copy.wait_event(ev)
@@ -336,12 +346,35 @@ def _pipelined_host_ata(a, c, m, n, alpha, ws, counter, auto_params, precision) 
                     _copy_tiles(c, dC, downloads[cut])
         mults += plan.mults
     main.wait_event(c_ready)               # (a plan with no C writer: download after the upload)
-    _copy_tiles(c, dC, _download_schedule(blocks[last][2], n, remaining=True))
+    rest = _download_schedule(blocks[last][2], n, remaining=True)
+    if zero_start and PIPELINE_LATE_C_ADD:
+        engine.run_plan(_add_tiles_plan(n, rest), code, int(dCin.data_ptr()), dCin.numel(), int(dC.data_ptr()),
+                        dC.numel(), 1.0)
+    _copy_tiles(c, dC, rest)
     main.wait_stream(copy)                 # the early downloads
     main.synchronize()
     if counter is not None:
         counter.add(mults)
     return True
+
+
+def _add_tiles_plan(n: int, tiles):
+    """combo4 passes C += A over the given (block row, block col, step) tiles
+    (square tiles of the download grid; one multi-node launch per <= 104)."""
+    tiles = tuple(tiles)
+
+    def build():
+        pb = planner.PlanBuilder("add-tiles")
+        g = pb.new_group()
+        for (bi, bj, step) in tiles:
+            r0, c0 = bi * step, bj * step
+            rows, cols = min(step, n - r0), min(step, n - c0)
+            if rows <= 0 or cols <= 0:
+                continue
+            c = planner.Win(nat.BASE_C, r0 * n + c0, n, rows, cols)
+            pb.combo4([c, planner.Win(nat.BASE_A, r0 * n + c0, n, rows, cols)], [(c, (1, 1))], group=g)
+        return pb.finish()
+    return engine.cached_plan(("add-tiles", n, hash(tiles), len(tiles)), build)
 
 
 def _add_plan(n: int):

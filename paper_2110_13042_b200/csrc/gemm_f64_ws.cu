@@ -860,17 +860,23 @@ __global__ void __launch_bounds__(ws64::THREADS, 1) prod_f64_tma_kernel(const __
   const int g = lane >> 2, q = lane & 3;
   // per-lane fragment offsets inside an operand k-block (see the header note):
   // [k-step parity][block parity]; the rest is compile-time
-  uint32_t aoff[2][2], boff[2][2];
+  uint32_t in_atom[2][2];
 #pragma unroll
   for (int jp = 0; jp < 2; ++jp)
 #pragma unroll
     for (int rp = 0; rp < 2; ++rp) {
       const int x = 2 * q + jp;
       const int chunk = (rp * 4 + (g >> 1)) ^ x;
-      const uint32_t in_atom = x * 128 + chunk * 16 + (g & 1) * 8;
-      aoff[jp][rp] = (wm * (WTM / 2)) * BK * 128 + in_atom;
-      boff[jp][rp] = (wn * (WTN / 2)) * BK * 128 + in_atom;
+      in_atom[jp][rp] = x * 128 + chunk * 16 + (g & 1) * 8;
     }
+  // Diagonal SYRK tiles: only the 8x8 blocks on or below the diagonal are
+  // computed, and the warps take their 64x32 sub-tiles in a permuted order so
+  // the two warps sharing an SM sub-partition (cw, cw + 4) split the lower
+  // triangle's 136 blocks 32/32/36/36 instead of 64/64/64/64 (the DMMA pipe is
+  // per sub-partition): a diagonal tile costs ~56 % of a full one.
+  // (wm, wn) of consumer warp cw on diagonal tiles, packed: wm = {1,1,0,1,0,0,1,0},
+  // wn = {0,1,0,2,2,3,3,1}
+  const int dwm = (75 >> cw) & 1, dwn = (32388 >> (2 * cw)) & 3;
   const uint32_t smem0 = smem_u32(smem);
   int kstep = 0;
   for (int it = 0;; ++it) {
@@ -890,45 +896,63 @@ __global__ void __launch_bounds__(ws64::THREADS, 1) prod_f64_tma_kernel(const __
     for (int r = 0; r < WTM; ++r)
 #pragma unroll
       for (int c = 0; c < WTN; ++c) acc[r][c][0] = acc[r][c][1] = 0.0;
+    const int twm = same ? dwm : wm, twn = same ? dwn : wn;
+    uint32_t need = 0;   // diagonal tiles: blocks (r, c) on or below the diagonal
+#pragma unroll
+    for (int r = 0; r < WTM; ++r)
+#pragma unroll
+      for (int c = 0; c < WTN; ++c)
+        if (twn * (WTN * 8) + c * 8 < twm * (WTM * 8) + r * 8 + 8) need |= 1u << (r * WTN + c);
+    const uint32_t abase = (twm * (WTM / 2)) * BK * 128, bbase = (twn * (WTN / 2)) * BK * 128;
     const uint32_t bsel = same ? 0u : (uint32_t)(NS * BUF_BYTES);
     // second terms: S1 / T1 one buffer after S0 / T0, added with their signs
     const bool two_a = NS == 2 && P.ns == 2;
     const bool two_b = same ? two_a : (NT == 2 && P.kind != kSyrk && P.nt == 2);
     const double sa = two_a ? P.s[1].sign : 0.0;
     const double sb = same ? sa : (two_b ? P.t[1].sign : 0.0);
-    for (int kt = 0; kt < KT; ++kt, ++kstep) {
-      const int s = kstep % STAGES;
-      mbar_wait(&full[s], (kstep / STAGES) & 1);
-      const uint32_t As = smem0 + s * STAGE_BYTES;
-      const uint32_t Bs = As + bsel;
+    auto mainloop = [&](auto diag) {
+      constexpr bool DIAG = decltype(diag)::value;
+      for (int kt = 0; kt < KT; ++kt, ++kstep) {
+        const int s = kstep % STAGES;
+        mbar_wait(&full[s], (kstep / STAGES) & 1);
+        const uint32_t As = smem0 + s * STAGE_BYTES + abase;
+        const uint32_t Bs = smem0 + s * STAGE_BYTES + bsel + bbase;
 #pragma unroll
-      for (int j = 0; j < BK / 4; ++j) {
-        double a[WTM], b[WTN];
-#pragma unroll
-        for (int r = 0; r < WTM; ++r)
-          a[r] = lds64(As + aoff[j & 1][r & 1] + (r >> 1) * BK * 128 + (j >> 1) * 1024);
-#pragma unroll
-        for (int c = 0; c < WTN; ++c)
-          b[c] = lds64(Bs + boff[j & 1][c & 1] + (c >> 1) * BK * 128 + (j >> 1) * 1024);
-        if (NS == 2 && two_a) {
+        for (int j = 0; j < BK / 4; ++j) {
+          double a[WTM], b[WTN];
 #pragma unroll
           for (int r = 0; r < WTM; ++r)
-            a[r] = fma(sa, lds64(As + BUF_BYTES + aoff[j & 1][r & 1] + (r >> 1) * BK * 128 + (j >> 1) * 1024), a[r]);
-        }
-        if ((NS == 2 || NT == 2) && two_b) {
+            a[r] = lds64(As + in_atom[j & 1][r & 1] + (r >> 1) * BK * 128 + (j >> 1) * 1024);
 #pragma unroll
           for (int c = 0; c < WTN; ++c)
-            b[c] = fma(sb, lds64(Bs + BUF_BYTES + boff[j & 1][c & 1] + (c >> 1) * BK * 128 + (j >> 1) * 1024), b[c]);
+            b[c] = lds64(Bs + in_atom[j & 1][c & 1] + (c >> 1) * BK * 128 + (j >> 1) * 1024);
+          if (NS == 2 && two_a) {
+#pragma unroll
+            for (int r = 0; r < WTM; ++r)
+              a[r] = fma(sa, lds64(As + BUF_BYTES + in_atom[j & 1][r & 1] + (r >> 1) * BK * 128 + (j >> 1) * 1024),
+                         a[r]);
+          }
+          if ((NS == 2 || NT == 2) && two_b) {
+#pragma unroll
+            for (int c = 0; c < WTN; ++c)
+              b[c] = fma(sb, lds64(Bs + BUF_BYTES + in_atom[j & 1][c & 1] + (c >> 1) * BK * 128 + (j >> 1) * 1024),
+                         b[c]);
+          }
+#pragma unroll
+          for (int r = 0; r < WTM; ++r)
+#pragma unroll
+            for (int c = 0; c < WTN; ++c)
+              if (!DIAG || ((need >> (r * WTN + c)) & 1u)) dmma_ws(acc[r][c], a[r], b[c]);
         }
-#pragma unroll
-        for (int r = 0; r < WTM; ++r)
-#pragma unroll
-          for (int c = 0; c < WTN; ++c) dmma_ws(acc[r][c], a[r], b[c]);
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
       }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[s]);
-    }
-    ws_epilogue(args, P, tl, acc, wm, wn, g, q, ctid);
+    };
+    if (same)
+      mainloop(std::integral_constant<bool, true>());
+    else
+      mainloop(std::integral_constant<bool, false>());
+    ws_epilogue(args, P, tl, acc, twm, twn, g, q, ctid);
     __syncwarp();
     if (lane == 0) mbar_arrive(&tempty[slot]);
   }
