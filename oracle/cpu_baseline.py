@@ -12,10 +12,12 @@ timed instead (``kind: "port"``).  Only ``bench.py``'s CPU legs use this.
 Sampling: the full configs take minutes to hours on the CPU (c4 is 7.0e13
 algorithmic flops), so a step is a bounded sample of the same seeded input:
 the leading rows x columns block of the config's matrix with the config's
-aspect ratio (c4: 8192 x 4096, m = 2n like 65536 x 32768; c5: 262144 x 512, m = 512n).  The metric is the
+aspect ratio (c4: 16384 x 8192, m = 2n like 65536 x 32768; c3: 8192^2; c5:
+262144 x 512, m = 512n).  For scale: the full c4 on the B200 box's 16 host cores
+took 474 s = 148.5 GF/s at threshold 2^19 (profiles/r02_cpu_reference_c4_full.json).  The metric is the
 same effective GFLOP/s = m*n^2/t of the sample (reference bench.py:57-65).
-The reference's element-count ``threshold`` is swept over {2^15, 2^17, 2^19}
-once and the fastest is used ("use the CPU path's best
+The reference's element-count ``threshold`` is swept over {2^17, 2^19, 2^21,
+2^23} once and the fastest is used ("use the CPU path's best
 threshold, not the default").
 """
 from __future__ import annotations
@@ -30,9 +32,11 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 REF_DIR = os.path.join(HERE, "_ref")
 
 # (rows, cols) of the bounded sample per config: the config's own aspect ratio
-SAMPLE = {"c1": (1024, 1024), "c2": (6001, 4097), "c3": (4096, 4096), "c4": (8192, 4096),
+SAMPLE = {"c1": (1024, 1024), "c2": (6001, 4097), "c3": (8192, 8192), "c4": (16384, 8192),
           "c5": (262144, 512)}
-THRESHOLDS = (1 << 15, 1 << 17, 1 << 19)
+# element-count thresholds swept once (the reference default 2^15 is 4-5x slower
+# than these at sample sizes: 20 s vs 4 s on 8192 x 4096)
+THRESHOLDS = (1 << 17, 1 << 19, 1 << 21, 1 << 23)
 
 
 def reference_module():
