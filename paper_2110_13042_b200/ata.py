@@ -76,6 +76,8 @@ def ata(A, C, alpha=1.0, threshold=DEFAULT_THRESHOLD, ws: StrassenWorkspace | No
         if auto_params != "tune":
             raise ValueError(f"auto_params must be AutoParams, None or 'tune', not {auto_params!r}")
         auto_params = _tuned_params(a, c, m, n)
+    if threshold == AUTO:
+        auto_params = fit_workspace_budget(auto_params or auto_plan.AutoParams())
     if threshold == AUTO and _pipelined_host_ata(a, c, m, n, alpha, ws, counter, auto_params, precision):
         return
     C_ = DeviceOperand(c, writable=True, lower=True)   # kernels touch only lower(C)
@@ -103,6 +105,26 @@ def ata(A, C, alpha=1.0, threshold=DEFAULT_THRESHOLD, ws: StrassenWorkspace | No
 
 
 _WS_CACHE: dict = {}
+
+
+def fit_workspace_budget(params, device=None, headroom: float = 0.8):
+    """AutoParams whose breadth-first workspace budget (default 40 GB) fits the
+    HBM this process can still get: free device memory plus what torch's
+    caching allocator holds unused, times `headroom`.  Unchanged (same plans,
+    same cache keys) whenever the default budget fits -- e.g. c4 on a 180 GB
+    B200 -- and a smaller budget (depth-first Strassen subtrees, less scratch)
+    when the device is shared or nearly full."""
+    import dataclasses
+    import torch
+    if not torch.cuda.is_available():
+        return params
+    dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
+    free, _ = torch.cuda.mem_get_info(dev)
+    avail = free + torch.cuda.memory_reserved(dev) - torch.cuda.memory_allocated(dev)
+    cap_gb = avail * headroom / 1e9
+    if cap_gb >= params.ws_budget_gb:
+        return params
+    return dataclasses.replace(params, ws_budget_gb=max(0.5, round(cap_gb, 1)))
 
 
 def _tuned_params(a, c, m, n):

@@ -897,12 +897,6 @@ __global__ void __launch_bounds__(ws64::THREADS, 1) prod_f64_tma_kernel(const __
 #pragma unroll
       for (int c = 0; c < WTN; ++c) acc[r][c][0] = acc[r][c][1] = 0.0;
     const int twm = same ? dwm : wm, twn = same ? dwn : wn;
-    uint32_t need = 0;   // diagonal tiles: blocks (r, c) on or below the diagonal
-#pragma unroll
-    for (int r = 0; r < WTM; ++r)
-#pragma unroll
-      for (int c = 0; c < WTN; ++c)
-        if (twn * (WTN * 8) + c * 8 < twm * (WTM * 8) + r * 8 + 8) need |= 1u << (r * WTN + c);
     const uint32_t abase = (twm * (WTM / 2)) * BK * 128, bbase = (twn * (WTN / 2)) * BK * 128;
     const uint32_t bsel = same ? 0u : (uint32_t)(NS * BUF_BYTES);
     // second terms: S1 / T1 one buffer after S0 / T0, added with their signs
@@ -910,8 +904,12 @@ __global__ void __launch_bounds__(ws64::THREADS, 1) prod_f64_tma_kernel(const __
     const bool two_b = same ? two_a : (NT == 2 && P.kind != kSyrk && P.nt == 2);
     const double sa = two_a ? P.s[1].sign : 0.0;
     const double sb = same ? sa : (two_b ? P.t[1].sign : 0.0);
-    auto mainloop = [&](auto diag) {
-      constexpr bool DIAG = decltype(diag)::value;
+    // OFF: the warp's 8x8 block (r, c) is computed iff c < r + OFF (on or below the
+    // diagonal of a diagonal tile: OFF = 8 wm - 4 wn + 1); 99 = every block, -99 = none.
+    // A compile-time pattern per warp role: predicated-off DMMAs would still spend
+    // their issue slots, branch-free unrolled code skips them.
+    auto mainloop = [&](auto off_tag) {
+      constexpr int OFF = decltype(off_tag)::value;
       for (int kt = 0; kt < KT; ++kt, ++kstep) {
         const int s = kstep % STAGES;
         mbar_wait(&full[s], (kstep / STAGES) & 1);
@@ -942,16 +940,21 @@ __global__ void __launch_bounds__(ws64::THREADS, 1) prod_f64_tma_kernel(const __
           for (int r = 0; r < WTM; ++r)
 #pragma unroll
             for (int c = 0; c < WTN; ++c)
-              if (!DIAG || ((need >> (r * WTN + c)) & 1u)) dmma_ws(acc[r][c], a[r], b[c]);
+              if (c < r + OFF) dmma_ws(acc[r][c], a[r], b[c]);
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
       }
     };
-    if (same)
-      mainloop(std::integral_constant<bool, true>());
+    const int off = 8 * twm - 4 * twn + 1;
+    if (!same || off >= WTN)
+      mainloop(std::integral_constant<int, 99>());
+    else if (off <= 1 - WTM)
+      mainloop(std::integral_constant<int, -99>());
+    else if (off == 1)
+      mainloop(std::integral_constant<int, 1>());
     else
-      mainloop(std::integral_constant<bool, false>());
+      mainloop(std::integral_constant<int, -3>());   // the permuted map's only other pattern
     ws_epilogue(args, P, tl, acc, twm, twn, g, q, ctid);
     __syncwarp();
     if (lane == 0) mbar_arrive(&tempty[slot]);

@@ -274,3 +274,23 @@ def test_reference_depth_first_executor(golden, monkeypatch):
         done += 1
     assert done >= 5
     engine._PLAN_CACHE.clear()
+
+
+def test_workspace_budget_follows_free_memory():
+    """fit_workspace_budget keeps the default 40 GB budget when it fits and
+    shrinks it to the HBM the process can get when it does not; a plan made
+    with a small budget needs less scratch and gives the same result."""
+    import dataclasses
+    import torch
+    from paper_2110_13042_b200 import auto_plan
+    from paper_2110_13042_b200.ata import fit_workspace_budget
+    base = auto_plan.AutoParams()
+    assert fit_workspace_budget(base) == base                      # an idle 180 GB B200
+    huge = dataclasses.replace(base, ws_budget_gb=1e6)
+    fitted = fit_workspace_budget(huge)
+    free, total = torch.cuda.mem_get_info()
+    assert fitted.ws_budget_gb <= total / 1e9
+    m, n = 16384, 8192
+    big = auto_plan.plan_ata_auto(m, n, n, n, base)
+    small = auto_plan.plan_ata_auto(m, n, n, n, dataclasses.replace(base, ws_budget_gb=0.5))
+    assert small.ws_scalars < big.ws_scalars

@@ -324,3 +324,40 @@ def test_tma_syrk_diagonal_tiles(m, n):
     ref = np.zeros((n, n))
     O.syrk_lower(a, ref, 2.0)
     assert O.rel_frobenius_lower(got, ref) <= 1e-14
+
+
+_CFG_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, sys.argv[1])
+import paper_2110_13042_b200 as P
+from oracle import atamul_oracle as O
+from paper_2110_13042_b200.auto_plan import AutoParams
+rng = np.random.default_rng(3)
+for shape in ((700, 333), (1500, 1024)):
+    a = rng.uniform(-1, 1, shape)
+    n = shape[1]
+    for thr, kw in ((4096, {}), ("auto", {"auto_params": AutoParams(leaf_cols=256, min_dim=128, hbm_gbs=1e9)})):
+        C = torch.triu(torch.full((n, n), 7.0, dtype=torch.float64, device="cuda"), 1)
+        P.ata(torch.from_numpy(a).cuda(), C, 1.0, threshold=thr, **kw)
+        got = C.cpu().numpy()
+        assert np.all(got[np.triu_indices(n, 1)] == 7.0)
+        err = O.rel_frobenius_lower(got, O.gram_blas(a))
+        assert err <= 1e-13, (shape, thr, err)
+print("OK")
+"""
+
+
+@pytest.mark.parametrize("cfg", ["0", "1", "2", "3"])
+def test_legacy_f64_configurations(cfg):
+    """The non-default FP64 product-kernel configurations kept for A/B
+    comparison (ATA_F64_CFG = 0..3: CTA-per-tile kernels of gemm_f64.cu) give
+    the oracle's result on reference and auto plans (fresh process: the
+    configuration is read once)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    env = dict(os.environ, ATA_F64_CFG=cfg)
+    r = subprocess.run([sys.executable, "-c", _CFG_SCRIPT, root], capture_output=True, text=True, env=env,
+                       timeout=600, cwd=root)
+    assert r.returncode == 0 and "OK" in r.stdout, r.stderr[-3000:]
