@@ -258,6 +258,14 @@ def run_reference(args, world, rank):
                              "threshold_sweep_s": {str(k): v for k, v in sweep.items()}},
             "e2e": {"value": value, "unit": "GFLOP/s", "h2d_bytes_per_step": 0,
                     "d2h_bytes_per_step": 0}}
+    # context, not this run's measurement: the same CPU path on the whole config
+    # (committed one-off runs, tools/cpu_full_reference.py)
+    full = os.path.join(ROOT, "profiles", f"r02_cpu_reference_{args.config}_full_t21.json")
+    if os.path.exists(full):
+        ctx = json.load(open(full))
+        line["cpu_baseline"]["full_size_context"] = {
+            "value": ctx["eff_gflops"], "unit": "GFLOP/s", "seconds": ctx["run_s"],
+            "threshold": ctx["threshold"], "source": os.path.relpath(full, ROOT)}
     print(json.dumps(line), flush=True)
 
 

@@ -77,7 +77,12 @@ class CpuBaseline:
         self.a = sample_matrix(cfg_name)
         self.ref = reference_module()
         self.kind = "reference" if self.ref is not None else "port"
-        self.threshold = THRESHOLDS[-1]
+        m, n = self.a.shape
+        # the default 2^15 and 2^17 are several times slower than the larger
+        # thresholds on the big samples (c4: 28 s at 2^17 vs 9 s at 2^21); small
+        # samples keep the small end of the range
+        self.thresholds = THRESHOLDS if m * n < (1 << 26) else THRESHOLDS[1:]
+        self.threshold = self.thresholds[-1]
 
     def _run(self, threshold) -> float:
         if self.ref is not None:
@@ -93,7 +98,7 @@ class CpuBaseline:
 
     def tune(self) -> dict:
         """Sweep the reference threshold once; keep the fastest."""
-        times = {t: self._run(t) for t in THRESHOLDS}
+        times = {t: self._run(t) for t in self.thresholds}
         self.threshold = min(times, key=times.get)
         return times
 
@@ -109,4 +114,4 @@ class CpuBaseline:
         what = ("reference atamul.SharedRunner (oracle/_ref, unmodified)" if self.kind == "reference"
                 else "oracle port of the reference AtA-S executor")
         return (f"leading {m} x {n} block of {self.cfg}'s seeded A; {what}, procs={self.cores}, "
-                f"threshold={self.threshold} (best of {list(THRESHOLDS)}); CPU: {cpu_model()}")
+                f"threshold={self.threshold} (best of {list(self.thresholds)}); CPU: {cpu_model()}")
