@@ -163,6 +163,15 @@ PIPELINE_ZERO_C = bool(int(os.environ.get("ATA_PIPE_ZERO_C", "1")))   # device C
 # of one whole-square add before the last block
 PIPELINE_LATE_C_ADD = bool(int(os.environ.get("ATA_PIPE_LATE_C_ADD", "1")))
 _PIPE_CIN: dict = {}   # the staged host-C buffer of the pipeline, one per (device, n, dtype)
+PIPE_TRACE = None      # a list: the pipeline appends (label, stream, event) marks (tools/e2e_timeline.py)
+
+
+def _mark(label, stream):
+    if PIPE_TRACE is not None:
+        import torch
+        ev = torch.cuda.Event(enable_timing=True)
+        ev.record(stream)
+        PIPE_TRACE.append((label, ev))
 PIPELINE_GEOMETRIC_MIN_RATIO = 4.0    # PIPELINE_GEOMETRIC_BLOCKS geometric blocks from here
 PIPELINE_GEOMETRIC_MIN_RATIO2 = 2.0   # two geometric blocks from here
 PIPELINE_GEOMETRIC_BLOCKS = 3     # measured (tools/e2e_ab.py): c4 e2e 1718 -> 1683 ms at 3 blocks,
@@ -319,16 +328,20 @@ def _pipelined_host_ata(a, c, m, n, alpha, ws, counter, auto_params, precision) 
             ev = torch.cuda.Event()
             ev.record(copy)
             events.append(ev)
+            _mark(f"A block {i} uploaded", copy)
             if i == 0 and not zero_start:
                 _copy_lower(dC, c, to_device=True)
                 c_ready.record(copy)
         if zero_start:
             _copy_lower(dCin, c, to_device=True)
             c_ready.record(copy)
+            _mark("C uploaded", copy)
     mults = 0
     last = len(blocks) - 1
+    _mark("start", main)
     for i, (r0, rows, plan) in enumerate(blocks):
         main.wait_event(events[i])
+        _mark(f"block {i} starts", main)
         ops = plan.ops
         A_ptr = int(dA.data_ptr()) + r0 * n * es
         # segment boundaries: the first C writer of block 0 waits for C's upload
@@ -366,13 +379,16 @@ def _pipelined_host_ata(a, c, m, n, alpha, ws, counter, auto_params, precision) 
                 copy.wait_event(ev)
                 with torch.cuda.stream(copy):
                     _copy_tiles(c, dC, downloads[cut])
+                    _mark(f"download group at op {cut} done ({len(downloads[cut])} tiles)", copy)
         mults += plan.mults
     main.wait_event(c_ready)               # (a plan with no C writer: download after the upload)
     rest = _download_schedule(blocks[last][2], n, remaining=True)
     if zero_start and PIPELINE_LATE_C_ADD:
         engine.run_plan(_add_tiles_plan(n, rest), code, int(dCin.data_ptr()), dCin.numel(), int(dC.data_ptr()),
                         dC.numel(), 1.0)
+    _mark("last block done", main)
     _copy_tiles(c, dC, rest)
+    _mark(f"remaining {len(rest)} tiles downloaded", main)
     main.wait_stream(copy)                 # the early downloads
     main.synchronize()
     if counter is not None:

@@ -750,20 +750,13 @@ __global__ void __launch_bounds__(ws64::THREADS, 1) prod_f64_tma_kernel(const __
   static_assert(BK % 8 == 0 && STAGES >= 2, "TMA k-block");
   using PD = DProdT<double, kNarrowDests>;
   constexpr int kSlots = 3;
-  // two-term launches: producer warps 1-3 are "summers" -- once a stage's terms
-  // have landed they add the second term into the first in shared memory
-  // (S0 += s1 S1, T0 += t1 T1, once per stage), and the consumers wait for
-  // `summed` instead of `full` and load single-term fragments
-  constexpr bool kSum = NS == 2 || NT == 2;
-  constexpr int SUMMERS = kSum ? 3 : 0;
   extern __shared__ uint8_t tma_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(tma_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + STAGES * STAGE_BYTES);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;
   uint64_t* tempty = tfull + kSlots;
-  uint64_t* summed = tempty + kSlots;   // STAGES barriers (two-term launches)
-  int* tinfo = reinterpret_cast<int*>(summed + STAGES);
+  int* tinfo = reinterpret_cast<int*>(tempty + kSlots);
   __shared__ __align__(16) unsigned char pdesc_raw[kSlots * sizeof(PD)];
   __shared__ int tdec[kSlots][3];
   const int tid = threadIdx.x;
@@ -777,9 +770,8 @@ __global__ void __launch_bounds__(ws64::THREADS, 1) prod_f64_tma_kernel(const __
     }
     for (int s = 0; s < kSlots; ++s) {
       mbar_init(&tfull[s], 1);
-      mbar_init(&tempty[s], CONSUMERS + SUMMERS);
+      mbar_init(&tempty[s], CONSUMERS);
     }
-    for (int s = 0; s < STAGES; ++s) mbar_init(&summed[s], SUMMERS > 0 ? SUMMERS : 1);
     asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
   }
   __syncthreads();
@@ -787,47 +779,7 @@ __global__ void __launch_bounds__(ws64::THREADS, 1) prod_f64_tma_kernel(const __
   if (tid < PRODUCERS) {
     // ===================== producer: one warp, one issuing thread =====================
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PRODUCER_REGS));
-    if (warp != 0) {
-      if (!kSum || warp > SUMMERS) return;
-      // ---------------- summers (two-term launches) ----------------
-      const int st = tid - 32;   // 0 .. 32 * SUMMERS - 1
-      int kstep = 0;
-      for (int it = 0;; ++it) {
-        const int slot = it % kSlots;
-        mbar_wait(&tfull[slot], (it / kSlots) & 1);
-        const int tile = tinfo[slot];
-        if (tile >= args.total_tiles) break;
-        const PD& P = *reinterpret_cast<const PD*>(pdesc_raw + slot * sizeof(PD));
-        const bool two_a = NS == 2 && P.ns == 2;
-        const bool two_b = NT == 2 && P.kind != kSyrk && P.nt == 2;
-        const double sa = two_a ? P.s[1].sign : 0.0, sb = two_b ? P.t[1].sign : 0.0;
-        const int KT = (P.m + BK - 1) / BK;
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&tempty[slot]);
-        for (int kt = 0; kt < KT; ++kt, ++kstep) {
-          const int s = kstep % STAGES;
-          mbar_wait(&full[s], (kstep / STAGES) & 1);
-          uint8_t* base = smem + s * STAGE_BYTES;
-          auto add = [&](uint8_t* x, const uint8_t* y, double sg) {
-            double2* px = reinterpret_cast<double2*>(x);
-            const double2* py = reinterpret_cast<const double2*>(y);
-#pragma unroll 4
-            for (int i = st; i < BUF_BYTES / 16; i += 32 * SUMMERS) {
-              double2 v = px[i];
-              const double2 w = py[i];
-              v.x = fma(sg, w.x, v.x);
-              v.y = fma(sg, w.y, v.y);
-              px[i] = v;
-            }
-          };
-          if (two_a) add(base, base + BUF_BYTES, sa);
-          if (two_b) add(base + NS * BUF_BYTES, base + (NS + 1) * BUF_BYTES, sb);
-          __syncwarp();
-          if (lane == 0) mbar_arrive(&summed[s]);
-        }
-      }
-      return;
-    }
+    if (warp != 0) return;
     int kstep = 0;
     for (int it = 0;; ++it) {
       int tile = 0;
@@ -947,6 +899,11 @@ __global__ void __launch_bounds__(ws64::THREADS, 1) prod_f64_tma_kernel(const __
     const int twm = same ? dwm : wm, twn = same ? dwn : wn;
     const uint32_t abase = (twm * (WTM / 2)) * BK * 128, bbase = (twn * (WTN / 2)) * BK * 128;
     const uint32_t bsel = same ? 0u : (uint32_t)(NS * BUF_BYTES);
+    // second terms: S1 / T1 one buffer after S0 / T0, added with their signs
+    const bool two_a = NS == 2 && P.ns == 2;
+    const bool two_b = same ? two_a : (NT == 2 && P.kind != kSyrk && P.nt == 2);
+    const double sa = two_a ? P.s[1].sign : 0.0;
+    const double sb = same ? sa : (two_b ? P.t[1].sign : 0.0);
     // OFF: the warp's 8x8 block (r, c) is computed iff c < r + OFF (on or below the
     // diagonal of a diagonal tile: OFF = 8 wm - 4 wn + 1); 99 = every block, -99 = none.
     // A compile-time pattern per warp role: predicated-off DMMAs would still spend
@@ -955,7 +912,7 @@ __global__ void __launch_bounds__(ws64::THREADS, 1) prod_f64_tma_kernel(const __
       constexpr int OFF = decltype(off_tag)::value;
       for (int kt = 0; kt < KT; ++kt, ++kstep) {
         const int s = kstep % STAGES;
-        mbar_wait(kSum ? &summed[s] : &full[s], (kstep / STAGES) & 1);
+        mbar_wait(&full[s], (kstep / STAGES) & 1);
         const uint32_t As = smem0 + s * STAGE_BYTES + abase;
         const uint32_t Bs = smem0 + s * STAGE_BYTES + bsel + bbase;
 #pragma unroll
@@ -967,6 +924,18 @@ __global__ void __launch_bounds__(ws64::THREADS, 1) prod_f64_tma_kernel(const __
 #pragma unroll
           for (int c = 0; c < WTN; ++c)
             b[c] = lds64(Bs + in_atom[j & 1][c & 1] + (c >> 1) * BK * 128 + (j >> 1) * 1024);
+          if (NS == 2 && two_a) {
+#pragma unroll
+            for (int r = 0; r < WTM; ++r)
+              a[r] = fma(sa, lds64(As + BUF_BYTES + in_atom[j & 1][r & 1] + (r >> 1) * BK * 128 + (j >> 1) * 1024),
+                         a[r]);
+          }
+          if ((NS == 2 || NT == 2) && two_b) {
+#pragma unroll
+            for (int c = 0; c < WTN; ++c)
+              b[c] = fma(sb, lds64(Bs + BUF_BYTES + in_atom[j & 1][c & 1] + (c >> 1) * BK * 128 + (j >> 1) * 1024),
+                         b[c]);
+          }
 #pragma unroll
           for (int r = 0; r < WTM; ++r)
 #pragma unroll
@@ -1185,7 +1154,7 @@ bool f64_tma_eligible(const DProdT<double, kNarrowDests>* prods, int count) {
 template <int BK, int NS, int NT>
 static cudaError_t tma_kernel_launch(const TmaBatch64& a, long long total, cudaStream_t s) {
   constexpr int STAGES = wst::stages<BK, NS, NT>();
-  const size_t smem = 1024 + (size_t)STAGES * wst::stage_bytes<BK, NS, NT>() + (3 * STAGES + 2 * 3) * sizeof(uint64_t) +
+  const size_t smem = 1024 + (size_t)STAGES * wst::stage_bytes<BK, NS, NT>() + (2 * STAGES + 2 * 3) * sizeof(uint64_t) +
                       4 * sizeof(int);
   auto kern = prod_f64_tma_kernel<BK, NS, NT>;
   static std::atomic<unsigned long long> attr_set{0};
