@@ -362,6 +362,7 @@ def main():
     leaf = leaf_task(tree, rank) if tree is not None else None
     A_ptr, B_ptr, C_out = int(A.data_ptr()), None, C
     a_elems = A.numel()
+    A_src = None          # the caller's operand when A is an even-pitch copy of it
     if leaf is not None:
         ar, br, cr = leaf.a_region, leaf.b_region, leaf.c_region
         C_out = torch.zeros((cr.rows, cr.cols), dtype=A.dtype, device=dev)
@@ -389,11 +390,20 @@ def main():
             if plan.ws_scalars else None
     else:
         ws = P.workspace_for_ata(mloc, n, threshold, dtype=np_dt)
+        if f64 and n % 2 and not engine.reference_dfs():
+            # odd pitch (c2: 4097 columns): like ata(), the operand is re-laid out
+            # with an even pitch (ata.even_pitch) for the TMA-fed leaf kernel; the
+            # copy is part of every timed step
+            A_src = A
+            A = torch.empty((mloc, n + 1), dtype=A_src.dtype, device=dev)[:, :n]
+            A.copy_(A_src)
+            A_ptr, a_elems = int(A.data_ptr()), (mloc - 1) * (n + 1) + n
+        lda = int(A.stride(0))
         if engine.reference_dfs():
-            plan = planner.plan_ata_reference(mloc, n, n, n, threshold, ws.level_offsets())
+            plan = planner.plan_ata_reference(mloc, n, lda, n, threshold, ws.level_offsets())
             wsbuf = ws.ensure(dev)
         else:   # the reference recursion tree executed breadth first
-            plan = ref_bfs.plan_ata_reference_bfs(mloc, n, n, n, threshold)
+            plan = ref_bfs.plan_ata_reference_bfs(mloc, n, lda, n, threshold)
             wsbuf = ws.ensure(dev, extra=plan.ws_scalars)
     units, n_launch = launch_units(plan)
     code = nat.dtype_code(A.dtype, precision)
@@ -411,7 +421,12 @@ def main():
 
     sub = [SubPlan(np.ascontiguousarray(plan.ops[i:j])) for (i, j, _, _) in units]
 
+    def repitch():
+        if A_src is not None:
+            A.copy_(A_src)
+
     def step(events=None):
+        repitch()
         C.zero_()
         if C_out is not C:
             C_out.zero_()
@@ -472,6 +487,7 @@ def main():
         e0.record(stream)
         for s in range(args.steps):
             if graph is not None:
+                repitch()
                 C.zero_()
                 graph.replay()
             else:

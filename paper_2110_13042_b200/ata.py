@@ -81,7 +81,7 @@ def ata(A, C, alpha=1.0, threshold=DEFAULT_THRESHOLD, ws: StrassenWorkspace | No
     if threshold == AUTO and _pipelined_host_ata(a, c, m, n, alpha, ws, counter, auto_params, precision):
         return
     C_ = DeviceOperand(c, writable=True, lower=True)   # kernels touch only lower(C)
-    A_ = DeviceOperand(a, dtype=C_.t.dtype, device=C_.t.device)
+    A_ = even_pitch(DeviceOperand(a, dtype=C_.t.dtype, device=C_.t.device))
     if ws is None:
         ws = _default_workspace(m, n, threshold, C_.t.dtype)
     elif threshold != AUTO:
@@ -105,6 +105,34 @@ def ata(A, C, alpha=1.0, threshold=DEFAULT_THRESHOLD, ws: StrassenWorkspace | No
 
 
 _WS_CACHE: dict = {}
+_PITCH_CACHE: dict = {}
+EVEN_PITCH_MIN_ELEMS = 1 << 20
+
+
+def even_pitch(op, slot: int = 0):
+    """An fp64 device operand with an odd row pitch, re-laid out with an even
+    one (one device copy, into a buffer kept per shape so repeated calls --
+    and captured graphs -- see the same pointer): the TMA-fed FP64 leaf kernel
+    needs 16-byte row pitches (config c2's 4097 columns).  Small operands, f32
+    and even pitches pass through."""
+    import torch
+    t = op.t
+    if t.dtype != torch.float64 or op.ld % 2 == 0 or op.rows < 2 or op.rows * op.cols < EVEN_PITCH_MIN_ELEMS:
+        return op
+    if os.environ.get("ATA_F64_TMA", "1") == "0":
+        return op
+    ld = op.cols + (op.cols & 1)
+    key = (str(t.device), op.rows, ld, slot)   # slot: distinct buffers for the operands of one call
+    buf = _PITCH_CACHE.get(key)
+    if buf is None:
+        if len(_PITCH_CACHE) >= 4:
+            _PITCH_CACHE.pop(next(iter(_PITCH_CACHE)))
+        buf = _PITCH_CACHE[key] = torch.empty((op.rows, ld), dtype=t.dtype, device=t.device)
+    view = buf[:, :op.cols]
+    view.copy_(t)
+    op.t, op.ld = view, ld
+    op.keep = buf
+    return op
 
 
 def fit_workspace_budget(params, device=None, headroom: float = 0.8):

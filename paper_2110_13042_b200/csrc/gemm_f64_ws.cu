@@ -715,7 +715,8 @@ struct TmaBatch64 {
   int n_sync;
   int dynamic;
   int dbg;
-  const CUtensorMap* maps;                      // device array [2 * count]: S, T of each product
+  int map3d;                                    // 1: 3-D maps (one box per operand); 0: 2-D maps, 8 boxes
+  const CUtensorMap* maps;                      // device array [4 * count]: S0, S1, T0, T1 of each product
   const DProdT<double, kNarrowDests>* gp;       // device array [count]
   const int* tile_prod;                         // device array [total_tiles]
 };
@@ -730,6 +731,26 @@ __device__ __forceinline__ void tma_load_3d(uint32_t dst, const CUtensorMap* map
       " [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(dst),
       "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(c2), "r"(bar)
       : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint32_t bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(c0), "r"(c1), "r"(bar)
+      : "memory");
+}
+// one operand term's k-block: a 3-D box, or eight 2-D boxes of [BK rows][16 doubles]
+// (2-D maps start 0 or 1 element before the window: col0 = its 8-byte misalignment)
+template <int BK>
+__device__ __forceinline__ void tma_term(uint32_t dst, const CUtensorMap* map, const DTerm<double>& t, bool map3d,
+                                         int kt, int c0, uint32_t bar) {
+  if (map3d) {
+    tma_load_3d(dst, map, 0, kt * BK, c0 / 16, bar);
+  } else {
+    const int col0 = (int)((reinterpret_cast<uintptr_t>(t.p) >> 3) & 1);
+#pragma unroll
+    for (int p = 0; p < wst::PANELS; ++p) tma_load_2d(dst + p * BK * 128, map, col0 + c0 + 16 * p, kt * BK, bar);
+  }
 }
 __device__ __forceinline__ double lds64(uint32_t addr) {
   double v;
@@ -838,12 +859,13 @@ __global__ void __launch_bounds__(ws64::THREADS, 1) prod_f64_tma_kernel(const __
           asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes)
                        : "memory");
           const uint32_t base = smem_u32(smem + s * STAGE_BYTES);
-          tma_load_3d(base, ms, 0, kt * BK, ti * (BM / 16), bar);
-          if (NS == 2 && ns == 2) tma_load_3d(base + BUF_BYTES, ms + 1, 0, kt * BK, ti * (BM / 16), bar);
+          const bool m3 = args.map3d != 0;
+          const DTerm<double>* tt = P.kind == kSyrk ? P.s : P.t;
+          tma_term<BK>(base, ms, P.s[0], m3, kt, ti * BM, bar);
+          if (NS == 2 && ns == 2) tma_term<BK>(base + BUF_BYTES, ms + 1, P.s[1], m3, kt, ti * BM, bar);
           if (!same) {
-            tma_load_3d(base + NS * BUF_BYTES, mt, 0, kt * BK, tj * (BN / 16), bar);
-            if (NT == 2 && nt == 2)
-              tma_load_3d(base + (NS + 1) * BUF_BYTES, mt + 1, 0, kt * BK, tj * (BN / 16), bar);
+            tma_term<BK>(base + NS * BUF_BYTES, mt, tt[0], m3, kt, tj * BN, bar);
+            if (NT == 2 && nt == 2) tma_term<BK>(base + (NS + 1) * BUF_BYTES, mt + 1, tt[1], m3, kt, tj * BN, bar);
           }
         }
       }
@@ -1128,9 +1150,31 @@ static bool f64_map_term(CUtensorMap* map, const DTerm<double>& t, int bk) {
              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 2-D map of a window with an even pitch and any 8-byte alignment: based at
+// the window start rounded down to 16 bytes (col0 = 0 or 1 element before it),
+// extent [col0 + cols][rows], boxes [BK rows][16 doubles], 128-byte swizzle;
+// everything past the window's last row / column is zero-filled
+static bool f64_map_term2d(CUtensorMap* map, const DTerm<double>& t, int bk) {
+  auto enc = f64_encoder();
+  if (enc == nullptr) return false;
+  const uintptr_t p = reinterpret_cast<uintptr_t>(t.p);
+  const uintptr_t base = p & ~uintptr_t(15);
+  const cuuint64_t col0 = (p - base) / 8;
+  cuuint64_t dims[2] = {col0 + (cuuint64_t)t.cols, (cuuint64_t)t.rows};
+  cuuint64_t strides[1] = {(cuuint64_t)t.ld * 8};
+  cuuint32_t box[2] = {16, (cuuint32_t)bk};
+  cuuint32_t estr[2] = {1, 1};
+  return enc(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, reinterpret_cast<void*>(base), dims, strides, box, estr,
+             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+static bool tma_term3d(const DTerm<double>& t) {
+  return (reinterpret_cast<uintptr_t>(t.p) & 15) == 0 && (t.ld & 1) == 0 && t.cols % 16 == 0 && t.cols >= 16;
+}
 static bool tma_term_ok(const DTerm<double>& t, bool first) {
-  return (reinterpret_cast<uintptr_t>(t.p) & 15) == 0 && (t.ld & 1) == 0 && t.cols % 16 == 0 && t.rows >= 1 &&
-         t.cols >= 16 && (!first || t.sign == 1.0);
+  return (reinterpret_cast<uintptr_t>(t.p) & 7) == 0 && (t.ld & 1) == 0 && t.rows >= 1 && t.cols >= 1 &&
+         (!first || t.sign == 1.0);
 }
 
 bool f64_tma_eligible(const DProdT<double, kNarrowDests>* prods, int count) {
@@ -1223,13 +1267,23 @@ cudaError_t launch_batch_f64_tma(DProdT<double, kNarrowDests>* prods, int count,
     if (prods[i].kind != kSyrk) nt = max(nt, prods[i].nt);
   }
   const int bk = (ns == 1 && nt == 1) ? WST_BK : WST_BK2;   // the box rows of the kernel that runs
+  bool map3d = true;   // every term a whole number of 16-column panels, 16-byte aligned
+  for (int i = 0; i < count && map3d; ++i) {
+    const auto& p = prods[i];
+    for (int j = 0; j < p.ns; ++j) map3d = map3d && tma_term3d(p.s[j]);
+    if (p.kind != kSyrk)
+      for (int j = 0; j < p.nt; ++j) map3d = map3d && tma_term3d(p.t[j]);
+  }
+  auto map_term = [&](CUtensorMap* m, const DTerm<double>& t) {
+    return map3d ? f64_map_term(m, t, bk) : f64_map_term2d(m, t, bk);
+  };
   for (int i = 0; i < count; ++i) {
     const auto& p = prods[i];
     for (int j = 0; j < p.ns; ++j)
-      if (!f64_map_term(&maps[4 * i + j], p.s[j], bk)) return cudaErrorNotSupported;
+      if (!map_term(&maps[4 * i + j], p.s[j])) return cudaErrorNotSupported;
     if (p.kind != kSyrk)
       for (int j = 0; j < p.nt; ++j)
-        if (!f64_map_term(&maps[4 * i + 2 + j], p.t[j], bk)) return cudaErrorNotSupported;
+        if (!map_term(&maps[4 * i + 2 + j], p.t[j])) return cudaErrorNotSupported;
   }
   std::memcpy(blob.data() + mbytes, prods, dbytes);
   int* tp = reinterpret_cast<int*>(blob.data() + mbytes + dbytes);
@@ -1248,6 +1302,7 @@ cudaError_t launch_batch_f64_tma(DProdT<double, kNarrowDests>* prods, int count,
   a.sync = sync;
   a.n_sync = (int)n_sync;
   a.dynamic = dynamic ? 1 : 0;
+  a.map3d = map3d ? 1 : 0;
   { const char* e = std::getenv("ATA_DBG"); a.dbg = e ? std::atoi(e) : 0; }
   a.maps = reinterpret_cast<const CUtensorMap*>(dev);
   a.gp = reinterpret_cast<const DProdT<double, kNarrowDests>*>(reinterpret_cast<const unsigned char*>(dev) + mbytes);

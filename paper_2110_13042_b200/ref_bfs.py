@@ -79,8 +79,11 @@ class _RefBFS:
 
     # ------------------------------------------------------------ scratch
     def alloc(self, rows: int, cols: int) -> Win:
-        w = Win(nat.BASE_WS, self.ws_top, max(cols, 1), rows, cols)
-        self.ws_top += rows * cols
+        # even pitch (16-byte rows): the TMA-fed FP64 leaf kernel's 2-D tensor maps
+        # need it; one padding column per odd-width buffer, never read
+        ld = max(cols + (cols & 1), 2)
+        w = Win(nat.BASE_WS, self.ws_top, ld, rows, cols)
+        self.ws_top += rows * ld
         self.ws_peak = max(self.ws_peak, self.ws_top)
         return w
 

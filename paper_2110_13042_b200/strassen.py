@@ -40,8 +40,9 @@ def fast_strassen(A, B, C, alpha=1.0, ws: StrassenWorkspace | None = None,
     if tuple(c.shape) != (n, k):
         raise ShapeMismatchError(f"shape mismatch: C {tuple(c.shape)} != {(n, k)}")
     C_ = DeviceOperand(c, writable=True)
-    A_ = DeviceOperand(a, dtype=C_.t.dtype, device=C_.t.device)
-    B_ = DeviceOperand(b, dtype=C_.t.dtype, device=C_.t.device)
+    from .ata import even_pitch
+    A_ = even_pitch(DeviceOperand(a, dtype=C_.t.dtype, device=C_.t.device), slot=0)
+    B_ = even_pitch(DeviceOperand(b, dtype=C_.t.dtype, device=C_.t.device), slot=1)
     if threshold == "auto":
         _fast_strassen_auto(A_, B_, C_, m, n, k, alpha, counter, auto_params, ws)
         return
