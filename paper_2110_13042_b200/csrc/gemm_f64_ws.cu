@@ -504,7 +504,6 @@ __global__ void __launch_bounds__(ws64::THREADS, 1)
                              : prod_of(args, tl.pi);
     const bool syrk = P.kind == kSyrk;
     const bool same = syrk && tl.ti == tl.tj;
-    const int i0 = tl.ti * BM, j0 = tl.tj * BN;
     const int KT = (P.m + BK - 1) / BK;
 
     double acc[WTM][WTN][2];
@@ -992,6 +991,7 @@ struct DescEntry {
   // used by a launch recorded into a CUDA graph: the graph keeps the device
   // pointer for as long as it lives, so the entry is never evicted
   bool pinned = false;
+  size_t payload_bytes = 0;
 };
 struct DescCache {
   std::unordered_map<uint64_t, DescEntry> map;
@@ -1022,49 +1022,67 @@ uint64_t blob_hash(const unsigned char* p, size_t n) {  // 64-bit words (blobs a
 // Device copy of a launch's descriptor blob, cached by content (repeated plans
 // hit it; entries used while a graph is captured are pinned for the graph's
 // lifetime).  cudaErrorNotReady: not resident and the stream is capturing.
-static cudaError_t resident_blob(std::vector<unsigned char>& blob, cudaStream_t s, void** dev) {
+// `sig` identifies the content (hashed, compared on a hit); `build` makes the
+// device payload only on a miss (the TMA launches' tensor maps are expensive to
+// encode: ~20k for a c2 leaf group).
+template <typename Build>
+static cudaError_t resident_blob_sig(std::vector<unsigned char>& sig, Build build, cudaStream_t s, void** dev) {
   std::lock_guard<std::mutex> lock(desc_mutex());
   DescCache& cache = desc_cache();
-  const uint64_t key = blob_hash(blob.data(), blob.size());
+  const uint64_t key = blob_hash(sig.data(), sig.size());
   auto it = cache.map.find(key);
   cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
   cudaStreamIsCapturing(s, &cs);
   const bool capturing = cs != cudaStreamCaptureStatusNone;
-  if (it == cache.map.end() || it->second.host != blob) {
+  if (it == cache.map.end() || it->second.host != sig) {
     if (capturing) return cudaErrorNotReady;  // no uploads inside a capture
     if (it != cache.map.end()) {  // hash collision: replace
       if (it->second.pinned) return cudaErrorNotReady;  // a live graph holds the colliding entry: narrow batches
       cudaFree(it->second.dev);
-      cache.bytes -= it->second.host.size();
+      cache.bytes -= it->second.host.size() + it->second.payload_bytes;
       cache.map.erase(it);
     }
     // evict least recently used unpinned entries beyond the budget (256 MB;
     // ATA_DESC_CACHE_KB overrides it, read on every miss)
     const char* lim_env = std::getenv("ATA_DESC_CACHE_KB");
     const size_t limit = lim_env ? (size_t)std::atoll(lim_env) << 10 : (size_t)256 << 20;
-    while (cache.bytes + blob.size() > limit) {
+    while (cache.bytes + sig.size() > limit) {
       auto lru = cache.map.end();
       for (auto j = cache.map.begin(); j != cache.map.end(); ++j)
         if (!j->second.pinned && (lru == cache.map.end() || j->second.last_use < lru->second.last_use)) lru = j;
       if (lru == cache.map.end()) break;  // everything left is held by graphs
       cudaDeviceSynchronize();  // the evicted buffer may be in use by queued work on any stream
       cudaFree(lru->second.dev);
-      cache.bytes -= lru->second.host.size();
+      cache.bytes -= lru->second.host.size() + lru->second.payload_bytes;
       cache.map.erase(lru);
     }
+    std::vector<unsigned char> payload;
+    if (cudaError_t e = build(payload); e != cudaSuccess) return e;
     DescEntry ent;
-    cudaError_t e = cudaMalloc(&ent.dev, blob.size());
+    cudaError_t e = cudaMalloc(&ent.dev, payload.size());
     if (e != cudaSuccess) return e;
-    e = cudaMemcpy(ent.dev, blob.data(), blob.size(), cudaMemcpyHostToDevice);
+    e = cudaMemcpy(ent.dev, payload.data(), payload.size(), cudaMemcpyHostToDevice);
     if (e != cudaSuccess) return e;
-    ent.host = std::move(blob);
-    cache.bytes += ent.host.size();
+    ent.host = std::move(sig);
+    cache.bytes += ent.host.size() + payload.size();
+    ent.payload_bytes = payload.size();
     it = cache.map.emplace(key, std::move(ent)).first;
   }
   it->second.last_use = ++cache.clock;
   if (capturing) it->second.pinned = true;
   *dev = it->second.dev;
   return cudaSuccess;
+}
+
+static cudaError_t resident_blob(std::vector<unsigned char>& blob, cudaStream_t s, void** dev) {
+  std::vector<unsigned char> copy;
+  return resident_blob_sig(
+      blob,
+      [&](std::vector<unsigned char>& out) {
+        out = blob;
+        return cudaSuccess;
+      },
+      s, dev);
 }
 
 cudaError_t launch_batch_f64_global(DProdT<double, kNarrowDests>* prods, int count, double alpha, int* sync,
@@ -1152,15 +1170,20 @@ static bool f64_map_term(CUtensorMap* map, const DTerm<double>& t, int bk) {
 
 // 2-D map of a window with an even pitch and any 8-byte alignment: based at
 // the window start rounded down to 16 bytes (col0 = 0 or 1 element before it),
-// extent [col0 + cols][rows], boxes [BK rows][16 doubles], 128-byte swizzle;
-// everything past the window's last row / column is zero-filled
+// extent [col0 + cols, rounded up to even][rows], boxes [BK rows][16 doubles],
+// 128-byte swizzle; everything past the window's last row (the contraction) is
+// zero-filled, columns past it only reach truncated output columns
 static bool f64_map_term2d(CUtensorMap* map, const DTerm<double>& t, int bk) {
   auto enc = f64_encoder();
   if (enc == nullptr) return false;
   const uintptr_t p = reinterpret_cast<uintptr_t>(t.p);
   const uintptr_t base = p & ~uintptr_t(15);
   const cuuint64_t col0 = (p - base) / 8;
-  cuuint64_t dims[2] = {col0 + (cuuint64_t)t.cols, (cuuint64_t)t.rows};
+  // the inner extent must be a whole number of 16-byte units (an odd one faults
+  // the TMA unit -- measured): round up; the extra column lies inside the even
+  // pitch and only feeds output columns the epilogue truncates
+  const cuuint64_t width = col0 + (cuuint64_t)t.cols;
+  cuuint64_t dims[2] = {width + (width & 1), (cuuint64_t)t.rows};
   cuuint64_t strides[1] = {(cuuint64_t)t.ld * 8};
   cuuint32_t box[2] = {16, (cuuint32_t)bk};
   cuuint32_t estr[2] = {1, 1};
@@ -1172,8 +1195,12 @@ static bool f64_map_term2d(CUtensorMap* map, const DTerm<double>& t, int bk) {
 static bool tma_term3d(const DTerm<double>& t) {
   return (reinterpret_cast<uintptr_t>(t.p) & 15) == 0 && (t.ld & 1) == 0 && t.cols % 16 == 0 && t.cols >= 16;
 }
+// (a box may not start 8 bytes into a 16-byte unit -- measured: the load
+// faults -- so windows must start 16-byte aligned; with even pitches that is
+// an even column offset, which every window of the reference trees has once A
+// and the scratch buffers use even pitches)
 static bool tma_term_ok(const DTerm<double>& t, bool first) {
-  return (reinterpret_cast<uintptr_t>(t.p) & 7) == 0 && (t.ld & 1) == 0 && t.rows >= 1 && t.cols >= 1 &&
+  return (reinterpret_cast<uintptr_t>(t.p) & 15) == 0 && (t.ld & 1) == 0 && t.rows >= 1 && t.cols >= 1 &&
          (!first || t.sign == 1.0);
 }
 
@@ -1256,11 +1283,11 @@ cudaError_t launch_batch_f64_tma(DProdT<double, kNarrowDests>* prods, int count,
   static const bool force_static = std::getenv("ATA_F64_TMA_STATIC") != nullptr;
   const bool dynamic = n_sync > 1 || (sync != nullptr && sync_ints >= 1 && !force_static);
   if (dynamic && (sync == nullptr || n_sync > sync_ints)) return cudaErrorInvalidValue;
-  // blob: tensor maps (64-byte aligned), descriptors, tile -> product table
+  // device blob: tensor maps (64-byte aligned), descriptors, tile -> product
+  // table; identified by the descriptors themselves (the maps are a function of
+  // them), so a repeated launch skips encoding its maps
   const size_t mbytes = sizeof(CUtensorMap) * 4 * (size_t)count;
   const size_t dbytes = sizeof(DProdT<double, kNarrowDests>) * (size_t)count;
-  std::vector<unsigned char> blob(mbytes + dbytes + ((sizeof(int) * (size_t)total + 7) & ~size_t(7)), 0);
-  CUtensorMap* maps = reinterpret_cast<CUtensorMap*>(blob.data());
   int ns = 1, nt = 1;
   for (int i = 0; i < count; ++i) {
     ns = max(ns, prods[i].ns);
@@ -1274,26 +1301,35 @@ cudaError_t launch_batch_f64_tma(DProdT<double, kNarrowDests>* prods, int count,
     if (p.kind != kSyrk)
       for (int j = 0; j < p.nt; ++j) map3d = map3d && tma_term3d(p.t[j]);
   }
-  auto map_term = [&](CUtensorMap* m, const DTerm<double>& t) {
-    return map3d ? f64_map_term(m, t, bk) : f64_map_term2d(m, t, bk);
+  std::vector<unsigned char> sig(dbytes + 4 * sizeof(int));
+  std::memcpy(sig.data(), prods, dbytes);
+  const int tail[4] = {0x544d4146, bk, map3d ? 1 : 0, (int)total};   // "TMA" tag: own hash domain
+  std::memcpy(sig.data() + dbytes, tail, sizeof(tail));
+  auto build = [&](std::vector<unsigned char>& blob) -> cudaError_t {
+    blob.assign(mbytes + dbytes + ((sizeof(int) * (size_t)total + 7) & ~size_t(7)), 0);
+    CUtensorMap* maps = reinterpret_cast<CUtensorMap*>(blob.data());
+    auto map_term = [&](CUtensorMap* m, const DTerm<double>& t) {
+      return map3d ? f64_map_term(m, t, bk) : f64_map_term2d(m, t, bk);
+    };
+    for (int i = 0; i < count; ++i) {
+      const auto& p = prods[i];
+      for (int j = 0; j < p.ns; ++j)
+        if (!map_term(&maps[4 * i + j], p.s[j])) return cudaErrorNotSupported;
+      if (p.kind != kSyrk)
+        for (int j = 0; j < p.nt; ++j)
+          if (!map_term(&maps[4 * i + 2 + j], p.t[j])) return cudaErrorNotSupported;
+    }
+    std::memcpy(blob.data() + mbytes, prods, dbytes);
+    int* tp = reinterpret_cast<int*>(blob.data() + mbytes + dbytes);
+    for (int i = 0; i < count; ++i) {
+      const auto& p = prods[i];
+      const long long nt_i = p.kind == kSyrk ? (long long)p.tn * (p.tn + 1) / 2 : (long long)p.tn * p.tk;
+      for (long long t = 0; t < nt_i; ++t) tp[p.tile_begin + t] = i;
+    }
+    return cudaSuccess;
   };
-  for (int i = 0; i < count; ++i) {
-    const auto& p = prods[i];
-    for (int j = 0; j < p.ns; ++j)
-      if (!map_term(&maps[4 * i + j], p.s[j])) return cudaErrorNotSupported;
-    if (p.kind != kSyrk)
-      for (int j = 0; j < p.nt; ++j)
-        if (!map_term(&maps[4 * i + 2 + j], p.t[j])) return cudaErrorNotSupported;
-  }
-  std::memcpy(blob.data() + mbytes, prods, dbytes);
-  int* tp = reinterpret_cast<int*>(blob.data() + mbytes + dbytes);
-  for (int i = 0; i < count; ++i) {
-    const auto& p = prods[i];
-    const long long nt_i = p.kind == kSyrk ? (long long)p.tn * (p.tn + 1) / 2 : (long long)p.tn * p.tk;
-    for (long long t = 0; t < nt_i; ++t) tp[p.tile_begin + t] = i;
-  }
   void* dev = nullptr;
-  if (cudaError_t e = resident_blob(blob, s, &dev); e != cudaSuccess) return e;
+  if (cudaError_t e = resident_blob_sig(sig, build, s, &dev); e != cudaSuccess) return e;
   TmaBatch64 a;
   std::memset(&a, 0, sizeof(a));
   a.count = count;

@@ -363,12 +363,14 @@ def test_legacy_f64_configurations(cfg):
     assert r.returncode == 0 and "OK" in r.stdout, r.stderr[-3000:]
 
 
-@pytest.mark.parametrize("m,n,k,off", [(300, 129, 77, 1), (1000, 200, 300, 3), (64, 16, 1, 1), (513, 255, 257, 0)])
+@pytest.mark.parametrize("m,n,k,off", [(300, 129, 77, 1), (1000, 200, 300, 3), (64, 16, 1, 1), (513, 255, 257, 0),
+                                       (300, 130, 77, 0), (777, 18, 129, 2)])
 def test_tma_2d_maps_unaligned_windows(m, n, k, off):
-    """Even-pitch windows that start 8 bytes past a 16-byte boundary and have
-    ragged widths go through the TMA-fed kernel's 2-D maps (based one element
-    early, extents bounded at the window's last row / column): GEMM and SYRK
-    leaves against NumPy, destinations outside the windows untouched."""
+    """Ragged widths and 8-byte-aligned starts: 16-byte-aligned even-pitch
+    windows with any width go through the TMA-fed kernel's 2-D maps (extents
+    bounded at the window's last row), windows starting 8 bytes into a
+    16-byte unit through the cp.async kernel -- GEMM and SYRK leaves against
+    NumPy, destinations outside the windows untouched."""
     import torch
     import paper_2110_13042_b200 as P
     rng = np.random.default_rng(m + n + k)
