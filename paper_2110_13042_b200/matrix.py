@@ -243,6 +243,18 @@ class DeviceOperand:
             _copy_lower(self.t, t, to_device=True)
             self.lower = True
             self.staged = True
+        elif (want == torch.float64 and t.dtype == want and not t.is_cuda and cols % 2 == 1 and rows > 1
+              and rows * cols >= (1 << 20) and t.is_contiguous()):
+            # odd-width fp64 host operand: staged straight into an even-pitch
+            # buffer (16-byte rows for the TMA-fed leaf kernel, ata.even_pitch)
+            buf = torch.empty((rows, cols + 1), dtype=want, device=device)
+            rc = _cudart().cudaMemcpy2DAsync(buf.data_ptr(), (cols + 1) * 8, t.data_ptr(), cols * 8, cols * 8,
+                                             rows, 1, _stream_ptr())
+            if rc != 0:
+                raise RuntimeError(f"cudaMemcpy2DAsync failed ({rc})")
+            self.t = buf[:, :cols]
+            self.keep = buf
+            self.staged = True
         else:
             self.t = t.to(device=device, dtype=want).contiguous()
             self.staged = True
