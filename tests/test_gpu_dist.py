@@ -51,16 +51,19 @@ def test_units_partition_all_ranks_one_gpu(procs):
     assert O.rel_frobenius_lower(C.cpu().numpy(), O.gram_blas(a)) <= 1e-13
 
 
-def test_bench_units_two_ranks_shared_gpu():
-    """bench.py's N>1 path with the units partition (2 ranks, gloo, one GPU):
-    the driver's JSON line names the partition and the per-rank plan."""
+@pytest.mark.parametrize("dist,prefix,port", [("units", "units x2", 29611), ("rows", "row-shard x2", 29613),
+                                               ("tree", "task-tree x2", 29615)])
+def test_bench_two_ranks_shared_gpu(dist, prefix, port):
+    """bench.py's N>1 paths (2 ranks, gloo, one GPU): units partition, row
+    shards and the reference's task tree; the driver's JSON line names the
+    partition."""
     import json
     env = dict(os.environ, ATA_DIST_BACKEND="gloo")
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
-                        "--master-addr", "127.0.0.1", "--master-port", "29611", os.path.join(ROOT, "bench.py"),
-                        "--gpus", "2", "--config", "c3", "--dist", "units", "--steps", "2", "--warmup", "1",
+                        "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
+                        "--gpus", "2", "--config", "c3", "--dist", dist, "--steps", "2", "--warmup", "1",
                         "--no-autotune"], capture_output=True, text=True, env=env, timeout=900, cwd=ROOT)
     assert r.returncode == 0, r.stderr[-3000:]
     line = json.loads([ln for ln in r.stdout.splitlines() if ln.startswith("{")][-1])
-    assert line["n_gpus"] == 2 and line["parallelism"].startswith("units x2")
+    assert line["n_gpus"] == 2 and line["parallelism"].startswith(prefix)
     assert line["value"] > 0 and line["gpu_launches"] > 0
