@@ -272,6 +272,9 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
         const Tc2Prod& P = args.p[t.pi];
         const CUtensorMap* mt = P.kind == kSyrk ? &P.ts : &P.tt;
         const int i0 = t.ti * BM + rank * HALF, j0 = t.tj * BN + rank * HALF;
+        // diagonal SYRK tile: each CTA's B half is its A half (same rows of the
+        // same panel) -- loaded once, the MMA reads it as both operands
+        const bool same = P.kind == kSyrk && t.ti == t.tj;
         const int KT = (P.m + BK - 1) / BK;
         const int rc = args.ring ? args.rg.chunk[t.pi] : 0, rr = rc & 1;
         const int rs = args.ring ? (args.rg.col_s[t.pi] + i0) / 32 : 0;
@@ -302,7 +305,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
           const uint32_t bar = t2_smem(&full[s]) & 0xFEFFFFFFu;  // the leader's barrier
           if (leader)
             asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(t2_smem(&full[s])),
-                         "r"(2 * STAGE_BYTES)
+                         "r"(same ? 2 * A_BYTES : 2 * STAGE_BYTES)
                          : "memory");
           if (args.ring) {
 #if TC2_RING_HINT & 2
@@ -315,6 +318,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
                 "l"(reinterpret_cast<uint64_t>(&args.rg.rmap[rr])), "r"(bar), "r"(0), "r"(ring_row), "r"(rs),
                 "l"(pol)
                 : "memory");
+            if (!same)
             asm volatile(
                 "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
                 ".L2::cache_hint [%0], [%1, {%3, %4, %5}], [%2], %6;" ::"r"(t2_smem(sb)),
@@ -327,6 +331,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
                 " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(t2_smem(sa)),
                 "l"(reinterpret_cast<uint64_t>(&args.rg.rmap[rr])), "r"(bar), "r"(0), "r"(ring_row), "r"(rs)
                 : "memory");
+            if (!same)
             asm volatile(
                 "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
                 " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(t2_smem(sb)),
@@ -340,6 +345,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
                 " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(t2_smem(sa)),
                 "l"(reinterpret_cast<uint64_t>(&P.ts)), "r"(bar), "r"(0), "r"(kb * BK), "r"(i0 / 32)
                 : "memory");
+            if (!same)
             asm volatile(
                 "cp.async.bulk.tensor.3d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
                 " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(t2_smem(sb)),
@@ -355,6 +361,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
                   : "memory");
 #pragma unroll
             for (int g = 0; g < HALF / 32; ++g)
+              if (!same)
               asm volatile(
                   "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
                   " [%0], [%1, {%3, %4}], [%2];" ::"r"(t2_smem(sb + g * BK * 128)),
@@ -372,6 +379,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
         const Tc2Tile t = t2_decode(args, tile);
         const Tc2Prod& P = args.p[t.pi];
         const int KT = (P.m + BK - 1) / BK;
+        const bool same = P.kind == kSyrk && t.ti == t.tj;
        for (int k0 = 0; k0 < KT; k0 += KSUB, ++it) {
         const int k1 = min(KT, k0 + KSUB);
         const int buf = it & 1;
@@ -384,7 +392,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(tc2::THREADS, 1)
           asm volatile("tcgen05.fence::after_thread_sync;");
           if (lane == 0) {
             const uint32_t sa = t2_smem(smem + s * STAGE_BYTES);
-            const uint32_t sb = sa + A_BYTES;
+            const uint32_t sb = same ? sa : sa + A_BYTES;
 #pragma unroll
             for (int kk = 0; kk < BK / 8; ++kk)
               asm volatile(
