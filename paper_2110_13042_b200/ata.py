@@ -80,6 +80,8 @@ def ata(A, C, alpha=1.0, threshold=DEFAULT_THRESHOLD, ws: StrassenWorkspace | No
         auto_params = fit_workspace_budget(auto_params or auto_plan.AutoParams())
     if threshold == AUTO and _pipelined_host_ata(a, c, m, n, alpha, ws, counter, auto_params, precision):
         return
+    if threshold != AUTO and _pipelined_host_ref(a, c, m, n, threshold, alpha, ws, counter):
+        return
     C_ = DeviceOperand(c, writable=True, lower=True)   # kernels touch only lower(C)
     A_ = even_pitch(DeviceOperand(a, dtype=C_.t.dtype, device=C_.t.device))
     if ws is None:
@@ -421,6 +423,96 @@ def _pipelined_host_ata(a, c, m, n, alpha, ws, counter, auto_params, precision) 
     main.synchronize()
     if counter is not None:
         counter.add(mults)
+    return True
+
+
+PIPELINE_REF_MIN_BYTES = 64 << 20    # integer-threshold pipeline: host A at least this large
+_PIPE_BUFS: dict = {}
+
+
+def _pipe_buffer(dev, shape, tag):
+    import torch
+    key = (str(dev), tuple(shape), tag)
+    buf = _PIPE_BUFS.get(key)
+    if buf is None:
+        for k in [k for k in _PIPE_BUFS if k[2] == tag]:
+            _PIPE_BUFS.pop(k)
+        buf = _PIPE_BUFS[key] = torch.empty(shape, dtype=torch.float64, device=dev)
+    return buf
+
+
+def _pipelined_host_ref(a, c, m, n, threshold, alpha, ws, counter) -> bool:
+    """Integer-threshold plans (the reference recursion tree, breadth first)
+    on pinned host fp64 A and C: A crosses PCIe first (straight into an
+    even-pitch device buffer), C's lower block-trapezoids follow on the copy
+    stream while the plan's operand-sum phase runs (the first op that writes C
+    waits for them), and C tiles go home as soon as their last writer has run.
+    The plan runs as a few CUDA-graph segments split at those points.  Returns
+    False when not applicable (the caller stages A and C itself)."""
+    import torch
+    if engine.reference_dfs():
+        return False
+    if not (isinstance(a, torch.Tensor) and isinstance(c, torch.Tensor)) or a.is_cuda or c.is_cuda:
+        return False
+    if a.dtype != torch.float64 or c.dtype != torch.float64 or m < 2:
+        return False
+    if not (a.is_contiguous() and c.is_contiguous() and a.is_pinned() and c.is_pinned()):
+        return False
+    if m * n * 8 < PIPELINE_REF_MIN_BYTES:
+        return False
+    from .matrix import _cudart, _stream_ptr
+    dev = torch.device("cuda", torch.cuda.current_device())
+    main = torch.cuda.current_stream(dev)
+    copy = _copy_stream(dev)
+    ld = n + (n & 1)
+    dA = _pipe_buffer(dev, (m, ld), "ref-A")
+    dC = _pipe_buffer(dev, (n, n), "ref-C")
+    if ws is None:
+        ws = _default_workspace(m, n, threshold, torch.float64)
+    else:
+        check_ata_workspace(ws, m, n, threshold)
+    plan = _plan_for(m, n, ld, n, threshold, ws)
+    wbuf = ws.ensure(dev, extra=plan.ws_scalars, dtype=torch.float64) if plan.ws_scalars > 0 else None
+    wkw = dict(ws=int(wbuf.data_ptr()) if wbuf is not None else 0,
+               ws_elems=int(wbuf.numel()) if wbuf is not None else 0)
+    a_ready, c_ready = torch.cuda.Event(), torch.cuda.Event()
+    copy.wait_stream(main)                 # the buffers are free to overwrite
+    with torch.cuda.stream(copy):
+        rc = _cudart().cudaMemcpy2DAsync(dA.data_ptr(), ld * 8, a.data_ptr(), n * 8, n * 8, m, 1, _stream_ptr())
+        if rc != 0:
+            raise RuntimeError(f"cudaMemcpy2DAsync failed ({rc})")
+        a_ready.record(copy)
+        _copy_lower(dC, c, to_device=True)
+        c_ready.record(copy)
+    ops = plan.ops
+    first_c = _first_c_writer(ops)
+    downloads = dict(_download_schedule(plan, n))
+    cuts = sorted({first_c} | set(downloads))
+    code = nat.ATA_F64
+    A_ptr, a_elems = int(dA.data_ptr()), (m - 1) * ld + n
+    main.wait_event(a_ready)
+    prev, c_waited = 0, False
+    for cut in cuts + [len(ops)]:
+        if cut > prev:
+            key = ("ata-ref-pipe", m, n, ld, threshold, prev, cut)
+            engine.run_plan_graphed(key, _SubPlan(ops[prev:cut]), code, A_ptr, a_elems, int(dC.data_ptr()),
+                                    dC.numel(), alpha, **wkw)
+            prev = cut
+        if cut == first_c and not c_waited:
+            main.wait_event(c_ready)
+            c_waited = True
+        if cut in downloads:
+            ev = torch.cuda.Event()
+            ev.record(main)
+            copy.wait_event(ev)
+            with torch.cuda.stream(copy):
+                _copy_tiles(c, dC, downloads[cut])
+    main.wait_event(c_ready)
+    _copy_tiles(c, dC, _download_schedule(plan, n, remaining=True))
+    main.wait_stream(copy)
+    main.synchronize()
+    if counter is not None:
+        counter.add(plan.mults)
     return True
 
 

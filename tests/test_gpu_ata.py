@@ -294,3 +294,33 @@ def test_workspace_budget_follows_free_memory():
     big = auto_plan.plan_ata_auto(m, n, n, n, base)
     small = auto_plan.plan_ata_auto(m, n, n, n, dataclasses.replace(base, ws_budget_gb=0.5))
     assert small.ws_scalars < big.ws_scalars
+
+
+def test_pipelined_host_reference_plan():
+    """Integer threshold on pinned host A and C (ata._pipelined_host_ref):
+    A's upload first, C's behind the operand-sum phase, tiles home as their
+    last writer finishes, the plan as CUDA-graph segments -- exact count, the
+    oracle's result added to the caller's C, the strict upper triangle
+    untouched, repeat calls (graph replay) bit-identical."""
+    import torch
+    import paper_2110_13042_b200 as P
+    rng = np.random.default_rng(23)
+    m, n, t = 6001, 1401, 65536
+    a = rng.standard_normal((m, n))
+    c0 = rng.uniform(-1, 1, (n, n))
+    hA = torch.from_numpy(a).pin_memory()
+    outs = []
+    for _ in range(3):
+        hC = torch.from_numpy(c0.copy()).pin_memory()
+        cnt = P.MultCounter()
+        P.ata(hA, hC, 1.5, threshold=t, counter=cnt)
+        outs.append(hC.numpy().copy())
+    got = outs[0]
+    iu = np.triu_indices(n, 1)
+    assert np.array_equal(got[iu], c0[iu])
+    ref = c0.copy()
+    want = [0]
+    O.ata_lower(a, ref, 1.5, t, want)
+    assert cnt.scalar_mults == want[0]
+    assert O.rel_frobenius_lower(got, ref) <= 1e-13
+    assert np.array_equal(outs[0], outs[1]) and np.array_equal(outs[1], outs[2])
