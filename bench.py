@@ -67,6 +67,10 @@ def parse():
                         "segments per rank + one NCCL reduce per C region (auto picks the one with the "
                         "smaller planned critical path); tree = the reference's distributed task tree "
                         "(leaf per rank, blocks retrieved over NCCL point-to-point)")
+    p.add_argument("--ws-budget", type=float, default=None,
+                   help="auto plan: breadth-first workspace budget in GB (smaller: depth-first Strassen "
+                        "subtrees, whose operand sums ride on the previous subtree's product launch)")
+    p.add_argument("--no-ride", action="store_true", help="A/B: plan without riding operand sums")
     p.add_argument("--fuse-leaf-sums", action="store_true",
                    help="A/B: last Strassen level's operand sums summed in the product loads")
     p.add_argument("--dump-units", default=None, help="write per-launch timings (JSON) here")
@@ -143,6 +147,9 @@ class ClockSampler:
         return False
 
 
+RIDE_ELEMS = {}   # unit index -> elements moved by the operand sums riding on that product launch
+
+
 def launch_units(plan):
     """Split a plan into the launches the native executor issues (consecutive
     same-group products form one launch), with algorithmic flops per unit."""
@@ -150,9 +157,29 @@ def launch_units(plan):
     ops = plan.ops
     units = []
     i = 0
+    RIDE_ELEMS.clear()
     while i < len(ops):
         t = int(ops[i]["type"])
         j = i + 1
+        if t == nat.OP_COMBO4 and int(ops[i]["flags"]) & nat.OPF_RIDE:
+            # riding operand sums: one unit with the product group they precede (the
+            # executor runs them inside that group's launch, on the kernel's spare warps)
+            while j < len(ops) and int(ops[j]["type"]) == nat.OP_COMBO4 and int(ops[j]["flags"]) & nat.OPF_RIDE:
+                j += 1
+            r1 = j
+            if j < len(ops) and int(ops[j]["type"]) in (nat.OP_GEMM, nat.OP_SYRK) and int(ops[j]["group"]) >= 0:
+                g = int(ops[j]["group"])
+                while j < len(ops) and int(ops[j]["type"]) in (nat.OP_GEMM, nat.OP_SYRK) \
+                        and int(ops[j]["group"]) == g:
+                    j += 1
+                flops = sum(2 * int(o["m"]) * int(o["n"]) * int(o["k"]) if int(o["type"]) == nat.OP_GEMM
+                            else int(o["m"]) * int(o["n"]) * (int(o["n"]) + 1) for o in ops[r1:j])
+                RIDE_ELEMS[len(units)] = sum(int(r["rows"]) * int(r["cols"]) for o in ops[i:r1]
+                                             for r in list(o["s"][:int(o["ns"])]) + list(o["d"][:int(o["nd"])]))
+                units.append((i, j, True, flops))
+                i = j
+                continue
+            j = i + 1      # no product group follows: ordinary passes
         if (t == nat.OP_ROUND and int(ops[i]["group"]) >= 0 and j < len(ops)
                 and int(ops[j]["group"]) == int(ops[i]["group"])):
             t = int(ops[j]["type"])     # fused rounding: part of the product launch that follows
@@ -344,6 +371,8 @@ def main():
                                                         ("max_depth", args.max_depth),
                                                         ("min_dim", args.min_dim),
                                                         ("gain", args.gain),
+                                                        ("ws_budget_gb", args.ws_budget),
+                                                        ("ride_sums", False if args.no_ride else None),
                                                         ("fuse_leaf_sums", args.fuse_leaf_sums or None))
                                                      if v is not None})
     mloc = r1 - r0
@@ -462,11 +491,13 @@ def main():
 
     lib = nat.load()
     per_step_launches = 0
+    rides_per_step = 0
     for w in range(args.warmup):
-        lc0 = lib.ata_launch_count()
+        lc0, rc0 = lib.ata_launch_count(), lib.ata_ride_count()
         step()
         if w == 0:
             per_step_launches = lib.ata_launch_count() - lc0   # executor launches of one step
+            rides_per_step = lib.ata_ride_count() - rc0
     barrier()
     # Reference-faithful plans (integer threshold: c1, c2) issue thousands of small
     # launches: the timed steps replay one captured CUDA graph of the plan, and the
@@ -573,6 +604,12 @@ def main():
                              "achieved": ew_gbs, "peak": hbm_peak, "unit": "GB/s",
                              "frac": ew_gbs / hbm_peak if ew_gbs else None,
                              "share_of_step": ew_ms / unit_total_ms if unit_total_ms else None,
+                             "riding": {"note": "operand sums executed inside the product launches (spare "
+                                                "warps of the FP64 leaf kernel), not in the achieved/share "
+                                                "figures of this block",
+                                        "launches_with_ride_per_step": len(RIDE_ELEMS),
+                                        "bytes_per_step": sum(RIDE_ELEMS.values()) * A.element_size(),
+                                        "executor_rides_per_step": rides_per_step},
                              "bytes_counted": "8 or 4 B x (elements of every source window read once + every "
                                               "output written once; lower-triangular passes count the "
                                               "lower part only)",

@@ -77,6 +77,14 @@ extern "C" {
  * chip just before its TMA loads them (auto_plan._ringify decides when the group
  * fits: equal row chunks, two chunks per wave of the persistent grid). */
 #define ATA_OP_ROUND 7
+/* ata_op.flags.  ATA_OPF_RIDE (COMBO4 only): the op is independent of the product
+ * group that follows it in the list -- it neither writes anything those products
+ * read or write nor reads anything they write -- so the executor may run it INSIDE
+ * that group's launch, on the FP64 leaf kernel's spare warps, instead of as its own
+ * HBM pass (the Strassen operand sums of the next leaf group hidden behind this
+ * group's tensor-core work).  The executor re-checks the independence and runs the
+ * op as an ordinary pass, in list order, whenever it cannot ride. */
+#define ATA_OPF_RIDE 1
 #define ATA_MAX_TERMS 4
 #define ATA_MAX_DESTS 8
 
@@ -103,7 +111,7 @@ typedef struct ata_op {
   int32_t ns, nt, nd;    /* term / destination counts */
   int32_t accumulate;    /* GEMM/SYRK: 1 = D += ..., 0 = D = ... */
   int32_t group;         /* consecutive GEMM/SYRK ops with equal group>=0 share one launch */
-  int32_t _pad;
+  int32_t flags;         /* ATA_OPF_* */
   ata_ref s[ATA_MAX_TERMS];
   ata_ref t[ATA_MAX_TERMS];
   ata_ref d[ATA_MAX_DESTS];
@@ -164,6 +172,8 @@ int64_t ata_sync_ints_needed(int dtype, const ata_op* ops, int32_t n_ops);
 /* Kernel launches the executor has issued since the library was loaded
  * (benchmark accounting; a captured graph replays without new calls). */
 int64_t ata_launch_count(void);
+/* Product launches that carried riding operand sums (ATA_OPF_RIDE) so far. */
+int64_t ata_ride_count(void);
 
 #ifdef __cplusplus
 }

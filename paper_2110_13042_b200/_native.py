@@ -25,20 +25,21 @@ OP_GEMM, OP_SYRK, OP_COMBO, OP_UPDATE, OP_FILL, OP_COMBO4, OP_POSTADD7, OP_ROUND
 BASE_A, BASE_C, BASE_WS, BASE_B = 0, 1, 2, 3
 MAX_TERMS, MAX_DESTS = 4, 8
 PROD_MAX_TERMS = 2
+OPF_RIDE = 1
 
 # numpy mirrors of ata_ref / ata_op (include/atamul_b200.h)
 REF_DTYPE = np.dtype([("base", "<i4"), ("rows", "<i4"), ("off", "<i8"), ("ld", "<i8"),
                       ("cols", "<i4"), ("region", "<i4"), ("sign", "<f8")], align=True)
 OP_DTYPE = np.dtype([("type", "<i4"), ("m", "<i4"), ("n", "<i4"), ("k", "<i4"),
                      ("ns", "<i4"), ("nt", "<i4"), ("nd", "<i4"), ("accumulate", "<i4"),
-                     ("group", "<i4"), ("_pad", "<i4"),
+                     ("group", "<i4"), ("flags", "<i4"),
                      ("s", REF_DTYPE, (MAX_TERMS,)), ("t", REF_DTYPE, (MAX_TERMS,)),
                      ("d", REF_DTYPE, (MAX_DESTS,))], align=True)
 
 EXPORTS = [
     "ata_last_error", "ata_strerror", "ata_version", "ata_abi_op_size",
     "ata_syrk_lower", "ata_gemm_atb", "ata_add_truncated", "ata_mirror_lower",
-    "ata_pack_lower", "ata_unpack_lower", "ata_run_plan", "ata_sync_ints_needed", "ata_launch_count",
+    "ata_pack_lower", "ata_unpack_lower", "ata_run_plan", "ata_sync_ints_needed", "ata_launch_count", "ata_ride_count",
 ]
 
 _CODE_TO_EXC = {
@@ -84,6 +85,8 @@ def load() -> ctypes.CDLL:
     lib.ata_sync_ints_needed.restype = ctypes.c_int64
     lib.ata_launch_count.restype = ctypes.c_int64
     lib.ata_launch_count.argtypes = []
+    lib.ata_ride_count.restype = ctypes.c_int64
+    lib.ata_ride_count.argtypes = []
     for name in EXPORTS:
         getattr(lib, name).restype = getattr(lib, name).restype or ctypes.c_int
     if lib.ata_abi_op_size() != OP_DTYPE.itemsize:

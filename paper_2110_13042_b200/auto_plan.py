@@ -39,6 +39,8 @@ from __future__ import annotations
 import os
 from dataclasses import dataclass
 
+import numpy as np
+
 from . import _native as nat
 from .errors import ShapeMismatchError
 from .planner import Plan, PlanBuilder, Win
@@ -81,6 +83,10 @@ class AutoParams:
                                    # block of a larger A (the pinned-host pipeline) gets the
                                    # Strassen tree of the whole A, so the blocks' executed
                                    # multiplications add up to the single plan's
+    ride_sums: bool = True         # FP64: the operand sums of the NEXT leaf group ride on the current
+                                   # group's product launch (ATA_OPF_RIDE, executed by the leaf kernel's
+                                   # spare warps while the DMMAs run): scratch of successive leaf groups
+                                   # alternates between two regions and _hoist_sums reorders / flags the ops
     tail_split: bool = True        # FP64: K-split a group's trailing products (partial last wave)
     min_tail_rows: int = 1024      # ... only when every chunk keeps this many rows
 
@@ -141,6 +147,9 @@ class _AutoPlanner:
         self.fill_waves = params.fill_waves
         self.tile = (TILE, TILE)
         self.defer_sums = None   # breadth-first trees: [(depth_left, quadrants, outputs)] emitted by emit()
+        self.flip_tree = 0       # ride_sums: successive breadth-first subtrees / depth-first operand
+        self.flip_sums = 0       # sums alternate between two scratch regions
+        self.flip_extra = 0      # elements below ws_top that are second copies of alternating regions
 
     # ---------------------------------------------------------------- workspace
     def alloc(self, rows: int, cols: int) -> Win:
@@ -369,24 +378,48 @@ class _AutoPlanner:
             for (srcs, outs, lower) in level:
                 self.pb.combo4(srcs, outs, lower=lower, group=g)
 
-    def node(self, a, b, m, n, k, out, sign, accumulate, depth):
+    def _riding(self) -> bool:
+        return self.p.ride_sums and self.esize == 8
+
+    def node(self, a, b, m, n, k, out, sign, accumulate, depth, level=0):
         """Depth-first at this node when its breadth-first workspace exceeds the budget."""
         need = self._dry_ws(a, b, m, n, k, depth)
-        if self.ws_top + need <= self.budget or not self.worth_split(m, n, k, depth):
+        # (the budget decides breadth- vs depth-first as without riding sums: the
+        # second copies of alternating regions do not count against it)
+        if self.ws_top - self.flip_extra + need <= self.budget or not self.worth_split(m, n, k, depth):
             leaves, posts = [], []
             mark = self.ws_top
+            if self._riding() and need > 0:
+                # the next subtree's operand sums are computed while this one's
+                # products run: successive subtrees use alternate scratch regions
+                self.ws_top = mark + self.flip_tree * need
+                self.ws_peak = max(self.ws_peak, mark + 2 * need)
+                self.flip_tree ^= 1
             self.defer_sums = []
             self.tree(a, b, m, n, k, out, sign, accumulate, depth, leaves, posts)
             self.emit(leaves, posts)
             self.ws_top = mark
             return
         mark = self.ws_top
-        S, T, m1, n1, k1 = self._sums(a, b, m, n, k)
+        if self._riding() and level >= 1:
+            # likewise the operand sums of successive depth-first nodes below the top
+            # (the products still running may read the previous node's sums through views)
+            ext = 5 * _ceil2(m) * (_ceil2(n) + _ceil2(k))
+            self.ws_top = mark + self.flip_sums * ext
+            self.flip_sums ^= 1
+            S, T, m1, n1, k1 = self._sums(a, b, m, n, k)
+            self.ws_top = mark + 2 * ext
+            self.ws_peak = max(self.ws_peak, self.ws_top)
+            self.flip_extra += ext
+        else:
+            ext = 0
+            S, T, m1, n1, k1 = self._sums(a, b, m, n, k)
         kids = [self.alloc(n1, k1) for _ in range(7)]
         for i in range(7):
-            self.node(S[i], T[i], m1, n1, k1, kids[i], 1.0, False, depth - 1)
+            self.node(S[i], T[i], m1, n1, k1, kids[i], 1.0, False, depth - 1, level + 1)
         self._post(kids, out, sign, n1, k1, accumulate)
         self.ws_top = mark
+        self.flip_extra -= ext
 
     def _dry_ws(self, a, b, m, n, k, depth) -> int:
         probe = _AutoPlanner(self.p)
@@ -448,6 +481,11 @@ class _AutoPlanner:
                            for (a, b, _) in blocks)
                 if need <= self.budget:
                     leaves, posts = [], []
+                    if self._riding() and 0 < need <= self.budget // 4:
+                        # alternate scratch regions for successive levels (see node())
+                        self.ws_top = self.ws_floor + self.flip_tree * need
+                        self.ws_peak = max(self.ws_peak, self.ws_floor + 2 * need)
+                        self.flip_tree ^= 1
                     self.defer_sums = []
                     for (a, b, c) in blocks:
                         self.tree(a, b, a.rows, a.cols, b.cols, c, 1.0, True, self.p.max_depth,
@@ -460,6 +498,91 @@ class _AutoPlanner:
                         self.node(a, b, a.rows, a.cols, b.cols, c, 1.0, True, self.p.max_depth)
             level = nxt
         self.emit_products(diag_prods)
+
+
+def _op_spans(ops, idx):
+    """(read intervals, write intervals) of ops[idx] as int64 arrays [k, 3] of
+    (base, first element, one past the last element): bounding intervals of the
+    windows (exact for dense blocks, conservative for strided views)."""
+    def spans(refs):
+        refs = refs[(refs["rows"] > 0) & (refs["cols"] > 0)]
+        lo = refs["off"].astype(np.int64)
+        hi = lo + (refs["rows"].astype(np.int64) - 1) * refs["ld"].astype(np.int64) + refs["cols"]
+        return np.stack([refs["base"].astype(np.int64), lo, hi], axis=1) if len(refs) else np.zeros((0, 3), np.int64)
+    op = ops[idx]
+    ns, nt, nd = int(op["ns"]), int(op["nt"]), int(op["nd"])
+    reads = [spans(op["s"][:ns])]
+    if int(op["type"]) in (nat.OP_GEMM, nat.OP_POSTADD7):
+        reads.append(spans(op["t"][:nt]))
+    return np.concatenate(reads), spans(op["d"][:nd])
+
+
+def _hit(a, b) -> bool:
+    """Any interval of a overlaps any interval of b (same base)."""
+    if not len(a) or not len(b):
+        return False
+    return bool(((a[:, None, 0] == b[None, :, 0]) & (a[:, None, 1] < b[None, :, 2]) &
+                 (b[None, :, 1] < a[:, None, 2])).any())
+
+
+def _hoist_sums(ops):
+    """Reorder a plan for riding operand sums (AutoParams.ride_sums).
+
+    Between the end of a product group G and the start of the next one lie G's
+    post-additions and the operand sums (COMBO4) of the next group.  Every such
+    COMBO4 that is independent of G and of the ops between G and itself -- it
+    writes nothing they read or write and reads nothing they write -- is moved
+    directly in front of G and flagged ATA_OPF_RIDE: the executor then runs it
+    inside G's launch, on the FP64 leaf kernel's spare warps, instead of as an HBM
+    pass of its own between the two product launches.  The sequential meaning of
+    the op list is unchanged (only independent ops are reordered)."""
+    n = len(ops)
+    types, groups = ops["type"], ops["group"]
+    prod = (types == nat.OP_GEMM) | (types == nat.OP_SYRK)
+    spans, i = [], 0
+    while i < n:
+        if prod[i] and groups[i] >= 0:
+            j = i + 1
+            while j < n and prod[j] and groups[j] == groups[i]:
+                j += 1
+            spans.append((i, j))
+            i = j
+        else:
+            i += 1
+    if len(spans) < 2:
+        return ops
+    order, ride = list(range(spans[0][0])), set()
+    for si, (g0, g1) in enumerate(spans):
+        nxt = spans[si + 1][0] if si + 1 < len(spans) else n
+        # blockers so far: the group itself; interval sets grow with the ops that stay
+        rw = [_op_spans(ops, q) for q in range(g0, g1)]
+        reads = np.concatenate([r for r, _ in rw])
+        writes = np.concatenate([w for _, w in rw])
+        moved, stay = [], []
+        for q in range(g1, nxt):
+            r, w = _op_spans(ops, q)
+            free = (int(types[q]) == nat.OP_COMBO4 and int(ops[q]["accumulate"]) == 0 and
+                    not _hit(w, reads) and not _hit(w, writes) and not _hit(r, writes))
+            if free:
+                moved.append(q)
+            else:
+                stay.append(q)
+                reads = np.concatenate([reads, r])
+                writes = np.concatenate([writes, w])
+        order += moved + list(range(g0, g1)) + stay
+        ride.update(moved)
+    out = ops[np.asarray(order, dtype=np.int64)].copy()
+    flag = np.asarray([q in ride for q in order])
+    out["flags"][flag] |= nat.OPF_RIDE
+    return out
+
+
+def _finish(ap) -> Plan:
+    plan = ap.pb.finish()
+    plan.ws_scalars = max(plan.ws_scalars, ap.ws_peak)
+    if ap.p.ride_sums and ap.esize == 8:
+        plan.ops = _hoist_sums(plan.ops)
+    return plan
 
 
 RING_PIECE_ROWS = 192    # scratch sized for pieces of up to 192 rows (tc2::PR, gemm_tf32_2sm.cu)
@@ -545,8 +668,7 @@ def plan_ata_auto(m: int, n: int, lda: int, ldc: int, params: AutoParams = AutoP
         raise ShapeMismatchError("shape mismatch: empty operand")
     ap = _AutoPlanner(params)
     ap.ata(m, n, lda, ldc, round_tf32)
-    plan = ap.pb.finish()
-    plan.ws_scalars = max(plan.ws_scalars, ap.ws_peak)
+    plan = _finish(ap)
     if round_tf32 and params.tf32_ring:
         plan = _ringify(plan, m, n, lda)
     return plan
@@ -566,9 +688,7 @@ def plan_gemm_auto(m: int, n: int, k: int, lda: int, ldb: int, ldc: int,
     B = Win(nat.BASE_B, 0, ldb, m, k)
     C = Win(nat.BASE_C, 0, ldc, n, k)
     ap.node(A, B, m, n, k, C, 1.0, True, params.max_depth)
-    plan = ap.pb.finish()
-    plan.ws_scalars = max(plan.ws_scalars, ap.ws_peak)
-    return plan
+    return _finish(ap)
 
 
 # --------------------------------------------------------------------------
@@ -685,9 +805,7 @@ def plan_units(segments, m: int, n: int, lda: int, ldc: int, params: AutoParams 
         if u not in UNITS:
             raise ValueError(f"unknown unit {u!r}")
         up.segment(u, r0, r1, A, C, m, n)
-    plan = up.pb.finish()
-    plan.ws_scalars = max(plan.ws_scalars, up.ws_peak)
-    return plan
+    return _finish(up)
 
 
 def unit_costs(m: int, n: int, params: AutoParams = AutoParams()):

@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <functional>
 #include <string>
 #include <algorithm>
 #include <atomic>
@@ -22,6 +23,8 @@
 
 // kernel launches issued through the executor (reported by ata_launch_count)
 static std::atomic<long long> g_launches{0};
+// product launches that carried riding operand sums (reported by ata_ride_count)
+static std::atomic<long long> g_rides{0};
 
 namespace {
 
@@ -209,9 +212,11 @@ bool supports_ordering<float>() { return false; }
 // on_batch(first, last, cont): cont = the group continues in the next launch
 // (the batch was cut at kMaxBatch products), so the two may run concurrently
 // when neither orders shared destinations.
-template <typename F1, typename F2, typename F3>
+// on_ride(first, last): a run of COMBO4 ops flagged ATA_OPF_RIDE (independent of
+// the product group that follows; they may execute inside its launch).
+template <typename F1, typename F2, typename F3, typename F4>
 int walk_batches(const ata_op* ops, int n_ops, bool ordering, bool narrow, F1 on_batch, F2 on_ew,
-                 F3 on_ew_run) {
+                 F3 on_ew_run, F4 on_ride) {
   int first = -1, group = -1, count = 0;
   bool all_narrow = true;  // every product of the open batch has <= kNarrowDests destinations
   std::vector<int> regions;
@@ -260,6 +265,13 @@ int walk_batches(const ata_op* ops, int n_ops, bool ordering, bool narrow, F1 on
       continue;
     }
     if ((rc = flush(i))) return rc;
+    if (op.type == ATA_OP_COMBO4 && (op.flags & ATA_OPF_RIDE)) {
+      int j = i + 1;
+      while (j < n_ops && ops[j].type == ATA_OP_COMBO4 && (ops[j].flags & ATA_OPF_RIDE)) ++j;
+      if ((rc = on_ride(i, j))) return rc;
+      i = j - 1;
+      continue;
+    }
     if ((op.type == ATA_OP_COMBO4 || op.type == ATA_OP_POSTADD7) && op.group >= 0) {
       // consecutive combo4 / postadd7 ops of one group: independent nodes, one launch
       int j = i + 1;
@@ -401,7 +413,21 @@ int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, int* sync, int64_t 
       }
     }
   };
-  auto launch_one = [&](int first, int last, cudaStream_t s) -> int {
+  // riding operand sums waiting for the next product launch: ops [ride_first, ride_last)
+  int ride_first = 0, ride_last = 0;
+  static const bool ride_enabled = [] {
+    const char* e = std::getenv("ATA_RIDE");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  std::function<int(int, int)> run_ew_range;   // ops [first, last) as ordinary elementwise launches
+  auto flush_ride = [&]() -> int {             // pending sums that cannot ride: ordinary launches, now
+    if (ride_last <= ride_first) return ATA_OK;
+    const int f = ride_first, l = ride_last;
+    ride_first = ride_last = 0;
+    return run_ew_range(f, l);
+  };
+  auto launch_one = [&](int first, int last, cudaStream_t ls) -> int {
+    cudaStream_t s = ls;
     const int64_t need = batch_sync_ints(ops, first, last);
     if (ordering && need > 1 && (sync == nullptr || need > sync_ints))
       return fail(ATA_E_WORKSPACE, "workspace undersized: sync buffer needs " +
@@ -428,7 +454,27 @@ int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, int* sync, int64_t 
           tb.p = prods.data();
           fill_batch(tb, first, last);
           if (ata::f64_tma_eligible(prods.data(), tb.count)) {
-            cudaError_t e = ata::launch_batch_f64_tma(prods.data(), tb.count, alpha, sync, sync_ints, s);
+            cudaError_t e = cudaErrorNotSupported;
+            if (ride_last > ride_first && ride_enabled) {
+              // the launch carries the pending operand sums on its spare warps
+              std::vector<ata::EwArgs<double>> ride;
+              for (int i = ride_first; i < ride_last; ++i) ride.push_back(combo4_args<double>(ops[i], b));
+              // (on a copy: the launcher rewrites the descriptors' region fields, and a
+              // refused ride falls through to the plain launch below)
+              auto with_ride = prods;
+              e = ata::launch_batch_f64_tma(with_ride.data(), tb.count, alpha, sync, sync_ints, s, ride.data(),
+                                            (int)ride.size());
+              if (e == cudaSuccess) {
+                ride_first = ride_last = 0;
+                g_launches += 1;
+                g_rides += 1;
+                return ATA_OK;
+              }
+              if (e != cudaErrorNotReady && e != cudaErrorNotSupported) return cuda_fail(e, "product launch (tma+ride)");
+              cudaGetLastError();
+            }
+            if (int rc = flush_ride()) return rc;
+            e = ata::launch_batch_f64_tma(prods.data(), tb.count, alpha, sync, sync_ints, s);
             if (e == cudaSuccess) {
               g_launches += 1;
               return ATA_OK;
@@ -437,6 +483,7 @@ int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, int* sync, int64_t 
             cudaGetLastError();   // not resident while capturing / no map: the cp.async kernels below
           }
         }
+        if (int rc = flush_ride()) return rc;
         static const bool no_global = std::getenv("ATA_NO_GLOBAL_BATCH") != nullptr;  // A/B knob
         if (last - first > ata::kMaxBatchNarrow && !no_global) {
           // unbounded region-free batch: device-resident descriptors, one launch
@@ -476,6 +523,7 @@ int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, int* sync, int64_t 
         return ATA_OK;
       }
     }
+    if (int rc = flush_ride()) return rc;
     std::memset(&batch, 0, sizeof(batch));
     fill_batch(batch, first, last);
     cudaError_t e = launch_batch<T>(batch, s, dtype);
@@ -532,6 +580,7 @@ int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, int* sync, int64_t 
     return ATA_OK;
   };
   auto on_ew = [&](int i) -> int {
+    if (int rc = flush_ride()) return rc;
     if (int rc = join_all()) return rc;
     ata::set_tf32_ring(nullptr);   // a ring belongs to the product group right after its ROUND op
     g_launches += 1;
@@ -587,6 +636,7 @@ int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, int* sync, int64_t 
     return ATA_OK;
   };
   auto on_ew_run = [&](int first, int last) -> int {
+    if (int rc = flush_ride()) return rc;
     if (int rc = join_all()) return rc;
     ata::set_tf32_ring(nullptr);
     std::vector<ata::EwArgs<T>> args;
@@ -615,7 +665,27 @@ int run_plan_t(const ata_op* ops, int n_ops, const Bases& b, int* sync, int64_t 
     if (e != cudaSuccess) return cuda_fail(e, "elementwise launch");
     return ATA_OK;
   };
-  int rc = walk_batches(ops, n_ops, ordering, narrow, on_batch, on_ew, on_ew_run);
+  run_ew_range = [&](int first, int last) -> int {
+    for (int i = first; i < last;) {
+      int j = i + 1;
+      if (ops[i].group >= 0) {
+        while (j < last && ops[j].group == ops[i].group) ++j;
+        if (int rc = on_ew_run(i, j)) return rc;
+      } else if (int rc = on_ew(i)) {
+        return rc;
+      }
+      i = j;
+    }
+    return ATA_OK;
+  };
+  auto on_ride = [&](int first, int last) -> int {
+    if (int rc = flush_ride()) return rc;
+    ride_first = first;
+    ride_last = last;
+    return ATA_OK;
+  };
+  int rc = walk_batches(ops, n_ops, ordering, narrow, on_batch, on_ew, on_ew_run, on_ride);
+  if (rc == ATA_OK) rc = flush_ride();
   int rj = join_all();
   ata::set_tf32_ring(nullptr);
   return rc ? rc : rj;
@@ -643,6 +713,7 @@ const char* ata_strerror(int code) {
 
 int ata_version(void) { return 100; }
 int64_t ata_launch_count(void) { return (int64_t)g_launches.load(); }
+int64_t ata_ride_count(void) { return (int64_t)g_rides.load(); }
 int ata_abi_op_size(void) { return (int)sizeof(ata_op); }
 
 int64_t ata_sync_ints_needed(int dtype, const ata_op* ops, int32_t n_ops) {
@@ -650,14 +721,20 @@ int64_t ata_sync_ints_needed(int dtype, const ata_op* ops, int32_t n_ops) {
   const bool ordering = dtype == ATA_F64 ? ata::f64_supports_ordering() : false;
   const bool narrow = dtype == ATA_F64 && ata::f64_narrow_supported();
   int64_t need = 1;
+  bool rides = false;
   walk_batches(
       ops, n_ops, ordering, narrow,
       [&](int first, int last, bool) -> int {
         need = std::max(need, batch_sync_ints(ops, first, last));
         return ATA_OK;
       },
-      [](int) -> int { return ATA_OK; }, [](int, int) -> int { return ATA_OK; });
-  return need;
+      [](int) -> int { return ATA_OK; }, [](int, int) -> int { return ATA_OK; },
+      [&](int, int) -> int {
+        rides = true;
+        return ATA_OK;
+      });
+  // riding operand sums: a chunk queue and one count per phase behind the turn counters
+  return need + (rides ? 1 + ata::kMaxRidePhases : 0);
 }
 
 int ata_run_plan(int dtype, const ata_op* ops, int32_t n_ops, const void* A, int64_t a_elems,

@@ -110,8 +110,14 @@ bool f64_narrow_supported();
 // pitch, cols % 16 == 0): one persistent launch of the TMA-fed kernel;
 // cudaErrorNotReady while capturing with descriptors not yet resident
 bool f64_tma_eligible(const DProdT<double, kNarrowDests>* prods, int count);
+// `ride` (may be null): Strassen operand-sum nodes (combo4) of a LATER product
+// group, independent of this launch's products, executed by the kernel's three
+// spare producer warps per SM while the DMMAs run (f64_ride_eligible nodes only).
 cudaError_t launch_batch_f64_tma(DProdT<double, kNarrowDests>* prods, int count, double alpha, int* sync,
-                                 long long sync_ints, cudaStream_t s);
+                                 long long sync_ints, cudaStream_t s, const EwArgs<double>* ride = nullptr,
+                                 int n_ride = 0);
+bool f64_ride_eligible(const EwArgs<double>& node);
+constexpr int kMaxRidePhases = 32;
 bool f64_supports_ordering();
 cudaError_t launch_batch_f32(const BatchArgs<float>& a, cudaStream_t s, bool split);
 template <typename T> cudaError_t launch_combo(const EwArgs<T>& a, cudaStream_t s);

@@ -695,6 +695,12 @@ namespace wst {
 #define WST_BK2 16    // k-block rows, launches with two-term (fused Strassen sum) operands
 #endif
 constexpr int PANELS = ws64::BM / 16;              // 16 doubles = one 128-byte swizzle row
+// register split of the launch allocation (384 x 168 = 64512; setmaxnreg.inc can only
+// draw what the CTA itself released): 128 producer threads x 56 (the spare warps run
+// the riding operand sums) + 256 consumer threads x 224
+constexpr int PRODUCER_REGS = 56, CONSUMER_REGS = 224;
+static_assert(PRODUCER_REGS * ws64::PRODUCERS + CONSUMER_REGS * ws64::CONSUMERS * 32 <= 168 * ws64::THREADS,
+              "setmaxnreg split exceeds the launch allocation: the consumers' inc would block forever");
 template <int BK>
 constexpr int buf_bytes() { return BK * 128 * PANELS; }   // one operand term, one k-block
 template <int BK, int NS, int NT>
@@ -705,6 +711,33 @@ constexpr int stages() {
                                                                   : (ws64::SMEM_BUDGET - 2048) / stage_bytes<BK, NS, NT>();
 }
 }  // namespace wst
+
+// ---- riding operand sums ------------------------------------------------
+// The Strassen pre-additions (strassen.py:195-203, one combo4 node = the five
+// operand sums of one Strassen node's operand) of the NEXT leaf group are
+// HBM-bound and independent of this launch's products, which are DMMA-bound and
+// leave three of the four producer warps idle.  A launch may therefore carry a
+// "ride": a list of combo4 nodes cut into chunks of kRideChunk column pairs
+// that the spare warps claim from a global queue.  Nodes are ordered by phase;
+// a node of phase p > 0 reads outputs of earlier phases and waits until every
+// chunk of phase p - 1 is finished.  Chunks are claimed in increasing order and
+// a chunk only ever waits for lower-numbered chunks (already claimed by running
+// warps that never wait on later ones), so the wait is deadlock-free without
+// any co-residency assumption.
+struct RideNode {
+  const double* src[4];
+  double* dst[5];
+  int sld[4], srows[4], scols[4];
+  int dld[5], drows[5], dcols[5];
+  int code[5];          // base-4 coefficient digits over the sources (1: +, 2: -)
+  int nsrc, ndst, rows, cp;   // iteration extent: rows x cp column pairs
+  int chunk_begin;      // first chunk of this node in the ride's chunk space
+  int phase;
+  int wait_chunks;      // chunks of phase - 1 that must be finished first (0: none)
+  int _pad;
+};
+static_assert(sizeof(RideNode) % 8 == 0, "RideNode is copied as 32-bit words and stored in 8-byte blobs");
+constexpr int kRideChunk = 2048;   // column pairs (16 bytes each) per chunk
 
 struct TmaBatch64 {
   int count;
@@ -718,7 +751,105 @@ struct TmaBatch64 {
   const CUtensorMap* maps;                      // device array [4 * count]: S0, S1, T0, T1 of each product
   const DProdT<double, kNarrowDests>* gp;       // device array [count]
   const int* tile_prod;                         // device array [total_tiles]
+  int ride_nodes, ride_chunks;                  // riding operand sums (0: none)
+  const RideNode* ride;                         // device array [ride_nodes]
+  int* ride_sync;                               // [0] chunk queue, [1 + p] finished chunks of phase p
 };
+
+__device__ __forceinline__ double2 ride_ld(const double* p) {
+  double2 v;
+  asm volatile("ld.global.cs.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ void ride_st(double* p, double2 v) {
+  asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+
+// One column pair (row r, columns 2 cc, 2 cc + 1) of a combo4 node: every
+// window is 16-byte aligned with an even pitch and even extents, so a pair is
+// either wholly inside a window or wholly outside (zero / not written).
+__device__ __forceinline__ void ride_load(const RideNode& n, int r, int cc, double2 (&v)[4]) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    v[q] = make_double2(0.0, 0.0);
+    if (q < n.nsrc && r < n.srows[q] && 2 * cc < n.scols[q])
+      v[q] = ride_ld(n.src[q] + (long long)r * n.sld[q] + 2 * cc);
+  }
+}
+__device__ __forceinline__ void ride_store(const RideNode& n, int r, int cc, const double2 (&v)[4]) {
+#pragma unroll
+  for (int j = 0; j < 5; ++j) {
+    if (j >= n.ndst || r >= n.drows[j] || 2 * cc >= n.dcols[j]) continue;
+    double2 o = make_double2(0.0, 0.0);
+    int code = n.code[j];
+#pragma unroll
+    for (int q = 0; q < 4; ++q, code >>= 2) {
+      const int cq = code & 3;
+      if (cq == 1) o.x += v[q].x, o.y += v[q].y;
+      else if (cq == 2) o.x -= v[q].x, o.y -= v[q].y;
+    }
+    ride_st(n.dst[j] + (long long)r * n.dld[j] + 2 * cc, o);
+  }
+}
+
+// A spare producer warp: claim chunks until the queue is empty.  `node` is the
+// warp's private shared-memory copy of the node it is working on.
+__device__ __forceinline__ void ride_worker(const TmaBatch64& args, RideNode* node, int lane) {
+  int cur = -1;
+  for (;;) {
+    int c = 0;
+    if (lane == 0) c = atomicAdd(args.ride_sync, 1);
+    c = __shfl_sync(0xffffffffu, c, 0);
+    if (c >= args.ride_chunks) break;
+    int ni = cur < 0 ? 0 : cur;
+    while (ni + 1 < args.ride_nodes && c >= __ldg(&args.ride[ni + 1].chunk_begin)) ++ni;
+    if (ni != cur) {
+      __syncwarp();
+      const uint32_t* src = reinterpret_cast<const uint32_t*>(args.ride + ni);
+      uint32_t* dst = reinterpret_cast<uint32_t*>(node);
+      for (int i = lane; i < (int)(sizeof(RideNode) / 4); i += 32) dst[i] = __ldg(src + i);
+      __syncwarp();
+      cur = ni;
+      if (node->wait_chunks > 0) {
+        if (lane == 0) {
+          const int* done = args.ride_sync + node->phase;   // = ride_sync + 1 + (phase - 1)
+          uint64_t t0;
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+          while (ld_acquire(done) < node->wait_chunks) {
+            __nanosleep(256);
+            uint64_t t1;
+            asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+            if (t1 - t0 > 20000000000ull) __trap();   // broken ordering invariant: fail the launch
+          }
+        }
+        __syncwarp();
+      }
+    }
+    const RideNode& n = *node;
+    const long long total = (long long)n.rows * n.cp;
+    const long long first = (long long)(c - n.chunk_begin) * kRideChunk;
+    const int count = (int)(total - first < kRideChunk ? total - first : kRideChunk);
+    long long idx = first + lane;
+    int r = (int)(idx / n.cp), cc = (int)(idx - (long long)r * n.cp);
+    // two pairs per iteration (8 independent 16-byte loads in flight per lane); cp >= 64
+    for (int i = lane; i < count; i += 64) {
+      int r2 = r, c2 = cc + 32;
+      if (c2 >= n.cp) c2 -= n.cp, ++r2;
+      const bool second = i + 32 < count;
+      double2 v[4], w[4];
+      ride_load(n, r, cc, v);
+      if (second) ride_load(n, r2, c2, w);
+      ride_store(n, r, cc, v);
+      if (second) ride_store(n, r2, c2, w);
+      r = r2, cc = c2 + 32;
+      if (cc >= n.cp) cc -= n.cp, ++r;
+    }
+    // publish the chunk: every lane's stores, then one count
+    __threadfence();
+    __syncwarp();
+    if (lane == 0) atomicAdd(args.ride_sync + 1 + n.phase, 1);
+  }
+}
 __device__ __forceinline__ const DProdT<double, kNarrowDests>& prod_of(const TmaBatch64& a, int i) {
   return a.gp[i];
 }
@@ -779,6 +910,7 @@ __global__ void __launch_bounds__(ws64::THREADS, 1) prod_f64_tma_kernel(const __
   int* tinfo = reinterpret_cast<int*>(tempty + kSlots);
   __shared__ __align__(16) unsigned char pdesc_raw[kSlots * sizeof(PD)];
   __shared__ int tdec[kSlots][3];
+  __shared__ __align__(16) RideNode ride_node[3];   // one per spare producer warp
   const int tid = threadIdx.x;
   const int warp = tid >> 5;
   const int lane = tid & 31;
@@ -798,8 +930,12 @@ __global__ void __launch_bounds__(ws64::THREADS, 1) prod_f64_tma_kernel(const __
 
   if (tid < PRODUCERS) {
     // ===================== producer: one warp, one issuing thread =====================
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(PRODUCER_REGS));
-    if (warp != 0) return;
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;\n" ::"n"(wst::PRODUCER_REGS));
+    if (warp != 0) {
+      // spare producer warps: the riding operand sums of the next leaf group
+      if (args.ride_chunks > 0) ride_worker(args, &ride_node[warp - 1], lane);
+      return;
+    }
     int kstep = 0;
     for (int it = 0;; ++it) {
       int tile = 0;
@@ -874,7 +1010,7 @@ __global__ void __launch_bounds__(ws64::THREADS, 1) prod_f64_tma_kernel(const __
   }
 
   // ===================== consumer warpgroups =====================
-  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(CONSUMER_REGS));
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;\n" ::"n"(wst::CONSUMER_REGS));
   const int ctid = tid - PRODUCERS;
   const int cw = warp - PRODUCERS / 32;
   const int wm = cw >> 2, wn = cw & 3;
@@ -1210,6 +1346,12 @@ bool f64_tma_eligible(const DProdT<double, kNarrowDests>* prods, int count) {
     return e ? std::atoi(e) : 1;
   }();
   if (mode == 0 || f64_encoder() == nullptr) return false;
+  // an odd window width is rounded up to a whole 16-byte unit by the 2-D map, so the
+  // TMA unit delivers the element after the window's last column instead of the zero
+  // of the reference's zero-extension: harmless when that column lies beyond the
+  // product's extent (the epilogue truncates it), wrong when the window is narrower
+  // than the product (odd Strassen quadrants) -- those take the cp.async kernel
+  auto width_ok = [](const DTerm<double>& t, int extent) { return (t.cols & 1) == 0 || t.cols >= extent; };
   for (int i = 0; i < count; ++i) {
     const auto& p = prods[i];
     if (p.ns < 1 || p.ns > 2 || !tma_term_ok(p.s[0], true) || (p.ns == 2 && !tma_term_ok(p.s[1], false)))
@@ -1218,6 +1360,11 @@ bool f64_tma_eligible(const DProdT<double, kNarrowDests>* prods, int count) {
     if (p.kind != kSyrk && (p.nt < 1 || p.nt > 2 || !tma_term_ok(p.t[0], true) ||
                             (p.nt == 2 && !tma_term_ok(p.t[1], false))))
       return false;
+    for (int j = 0; j < p.ns; ++j)
+      if (!width_ok(p.s[j], p.n)) return false;
+    if (p.kind != kSyrk)
+      for (int j = 0; j < p.nt; ++j)
+        if (!width_ok(p.t[j], p.k)) return false;
   }
   return true;
 }
@@ -1235,8 +1382,130 @@ static cudaError_t tma_kernel_launch(const TmaBatch64& a, long long total, cudaS
   return cudaGetLastError();
 }
 
+// ---- riding operand sums: host side ----
+static bool ride_win_ok(const void* p, long long ld, int rows, int cols) {
+  return rows >= 0 && cols >= 0 && (cols & 1) == 0 && (ld & 1) == 0 && ld < 0x7fffffffLL &&
+         (reinterpret_cast<uintptr_t>(p) & 15) == 0;
+}
+bool f64_ride_eligible(const EwArgs<double>& a) {
+  if (a.lower || a.nsrc < 1 || a.nsrc > 4 || a.ndst < 1 || a.ndst > 5 || a.rows < 1 || a.cols < 64 || (a.cols & 1))
+    return false;
+  for (int q = 0; q < a.nsrc; ++q)
+    if (!ride_win_ok(a.src[q].p, a.src[q].ld, a.src[q].rows, a.src[q].cols)) return false;
+  for (int j = 0; j < a.ndst; ++j)
+    if (!ride_win_ok(a.dst[j].p, a.dst[j].ld, a.dst[j].rows, a.dst[j].cols)) return false;
+  return true;
+}
+namespace {
+struct Span {   // bounding address interval of a window (conservative for strided windows)
+  uintptr_t lo, hi;
+};
+template <typename W>
+Span span_of(const W& w) {
+  if (w.rows <= 0 || w.cols <= 0) return {0, 0};
+  const uintptr_t lo = reinterpret_cast<uintptr_t>(w.p);
+  return {lo, lo + ((uintptr_t)(w.rows - 1) * (uintptr_t)w.ld + (uintptr_t)w.cols) * sizeof(double)};
+}
+bool overlap(Span a, Span b) { return a.lo < a.hi && b.lo < b.hi && a.lo < b.hi && b.lo < a.hi; }
+// b conflicts with a (a earlier): b reads what a writes, or b writes what a reads or writes
+bool ride_conflict(const EwArgs<double>& a, const EwArgs<double>& b) {
+  for (int j = 0; j < b.ndst; ++j) {
+    for (int q = 0; q < a.nsrc; ++q)
+      if (overlap(span_of(b.dst[j]), span_of(a.src[q]))) return true;
+    for (int e = 0; e < a.ndst; ++e)
+      if (overlap(span_of(b.dst[j]), span_of(a.dst[e]))) return true;
+  }
+  for (int q = 0; q < b.nsrc; ++q)
+    for (int e = 0; e < a.ndst; ++e)
+      if (overlap(span_of(b.src[q]), span_of(a.dst[e]))) return true;
+  return false;
+}
+}  // namespace
+
+// The riding nodes must be independent of the launch's products: they may not
+// write anything a product reads or writes, nor read anything a product writes
+// (checked on bounding intervals; the planner guarantees it, this is the guard).
+static bool ride_independent(const EwArgs<double>* ride, int n_ride, const DProdT<double, kNarrowDests>* prods,
+                             int count) {
+  for (int i = 0; i < n_ride; ++i) {
+    const EwArgs<double>& a = ride[i];
+    for (int pi = 0; pi < count; ++pi) {
+      const auto& p = prods[pi];
+      for (int j = 0; j < a.ndst; ++j) {
+        const Span d = span_of(a.dst[j]);
+        for (int q = 0; q < p.ns; ++q)
+          if (overlap(d, span_of(p.s[q]))) return false;
+        for (int q = 0; q < (p.kind == kSyrk ? 0 : p.nt); ++q)
+          if (overlap(d, span_of(p.t[q]))) return false;
+        for (int e = 0; e < p.nd; ++e)
+          if (overlap(d, span_of(p.d[e]))) return false;
+      }
+      for (int q = 0; q < a.nsrc; ++q)
+        for (int e = 0; e < p.nd; ++e)
+          if (overlap(span_of(a.src[q]), span_of(p.d[e]))) return false;
+    }
+  }
+  return true;
+}
+
+// RideNodes of a ride (phases by dependency among the nodes, chunk prefix);
+// false when the ride cannot run inside the launch (the caller then runs the
+// nodes as ordinary combo4 launches first).
+static bool build_ride(const EwArgs<double>* ride, int n_ride, std::vector<RideNode>& out, int& chunks,
+                       int& phases) {
+  out.clear();
+  chunks = 0;
+  phases = 0;
+  int phase = 0, phase_first = 0, phase_chunks = 0, prev_phase_chunks = 0;
+  for (int i = 0; i < n_ride; ++i) {
+    const EwArgs<double>& a = ride[i];
+    if (!f64_ride_eligible(a)) return false;
+    bool dep = false;
+    for (int e = phase_first; e < i && !dep; ++e) dep = ride_conflict(ride[e], a);
+    if (dep) {
+      ++phase;
+      phase_first = i;
+      prev_phase_chunks = phase_chunks;
+      phase_chunks = 0;
+      // (a node also conflicting with phases before the previous one is covered:
+      // finishing phase p - 1 implies every earlier phase finished)
+    }
+    if (phase >= kMaxRidePhases) return false;
+    RideNode n;
+    std::memset(&n, 0, sizeof(n));
+    for (int q = 0; q < a.nsrc; ++q) {
+      n.src[q] = a.src[q].p;
+      n.sld[q] = (int)a.src[q].ld;
+      n.srows[q] = a.src[q].rows;
+      n.scols[q] = a.src[q].cols;
+    }
+    for (int j = 0; j < a.ndst; ++j) {
+      n.dst[j] = a.dst[j].p;
+      n.dld[j] = (int)a.dst[j].ld;
+      n.drows[j] = a.dst[j].rows;
+      n.dcols[j] = a.dst[j].cols;
+      n.code[j] = a.dst[j].coef;
+    }
+    n.nsrc = a.nsrc;
+    n.ndst = a.ndst;
+    n.rows = a.rows;
+    n.cp = a.cols / 2;
+    n.chunk_begin = chunks;
+    n.phase = phase;
+    n.wait_chunks = phase > 0 ? prev_phase_chunks : 0;
+    const long long pairs = (long long)n.rows * n.cp;
+    const long long c = (pairs + kRideChunk - 1) / kRideChunk;
+    if (chunks + c > 0x3fffffffLL) return false;
+    chunks += (int)c;
+    phase_chunks += (int)c;
+    out.push_back(n);
+  }
+  phases = phase + 1;
+  return !out.empty();
+}
+
 cudaError_t launch_batch_f64_tma(DProdT<double, kNarrowDests>* prods, int count, double alpha, int* sync,
-                                 long long sync_ints, cudaStream_t s) {
+                                 long long sync_ints, cudaStream_t s, const EwArgs<double>* ride, int n_ride) {
   using namespace ws64;
   long long total = 0;
   for (int i = 0; i < count; ++i) {
@@ -1246,7 +1515,7 @@ cudaError_t launch_batch_f64_tma(DProdT<double, kNarrowDests>* prods, int count,
     p.tile_begin = (int)total;
     total += p.kind == kSyrk ? (long long)p.tn * (p.tn + 1) / 2 : (long long)p.tn * p.tk;
   }
-  if (total <= 0) return cudaSuccess;
+  if (total <= 0) return n_ride > 0 ? cudaErrorNotSupported : cudaSuccess;
   if (total > 0x7fffffffLL) return cudaErrorInvalidConfiguration;
   // destination regions (DDest.sem = batch-local region id, 1-based; 0 = none):
   // per-tile turn counters at sync[1..], as in launch_ws
@@ -1283,6 +1552,15 @@ cudaError_t launch_batch_f64_tma(DProdT<double, kNarrowDests>* prods, int count,
   static const bool force_static = std::getenv("ATA_F64_TMA_STATIC") != nullptr;
   const bool dynamic = n_sync > 1 || (sync != nullptr && sync_ints >= 1 && !force_static);
   if (dynamic && (sync == nullptr || n_sync > sync_ints)) return cudaErrorInvalidValue;
+  // riding operand sums: their chunk queue and per-phase counts follow the turn counters
+  std::vector<RideNode> rnodes;
+  int ride_chunks = 0, ride_phases = 0;
+  if (n_ride > 0) {
+    if (sync == nullptr || !build_ride(ride, n_ride, rnodes, ride_chunks, ride_phases) ||
+        n_sync + 1 + ride_phases > sync_ints || !ride_independent(ride, n_ride, prods, count))
+      return cudaErrorNotSupported;   // the caller runs the nodes as ordinary launches
+  }
+  const size_t rbytes = sizeof(RideNode) * rnodes.size();
   // device blob: tensor maps (64-byte aligned), descriptors, tile -> product
   // table; identified by the descriptors themselves (the maps are a function of
   // them), so a repeated launch skips encoding its maps
@@ -1301,12 +1579,15 @@ cudaError_t launch_batch_f64_tma(DProdT<double, kNarrowDests>* prods, int count,
     if (p.kind != kSyrk)
       for (int j = 0; j < p.nt; ++j) map3d = map3d && tma_term3d(p.t[j]);
   }
-  std::vector<unsigned char> sig(dbytes + 4 * sizeof(int));
+  std::vector<unsigned char> sig(dbytes + 4 * sizeof(int) + rbytes);
   std::memcpy(sig.data(), prods, dbytes);
   const int tail[4] = {0x544d4146, bk, map3d ? 1 : 0, (int)total};   // "TMA" tag: own hash domain
   std::memcpy(sig.data() + dbytes, tail, sizeof(tail));
+  if (rbytes) std::memcpy(sig.data() + dbytes + sizeof(tail), rnodes.data(), rbytes);
+  const size_t tbytes = (sizeof(int) * (size_t)total + 7) & ~size_t(7);
   auto build = [&](std::vector<unsigned char>& blob) -> cudaError_t {
-    blob.assign(mbytes + dbytes + ((sizeof(int) * (size_t)total + 7) & ~size_t(7)), 0);
+    blob.assign(mbytes + dbytes + tbytes + rbytes, 0);
+    if (rbytes) std::memcpy(blob.data() + mbytes + dbytes + tbytes, rnodes.data(), rbytes);
     CUtensorMap* maps = reinterpret_cast<CUtensorMap*>(blob.data());
     auto map_term = [&](CUtensorMap* m, const DTerm<double>& t) {
       return map3d ? f64_map_term(m, t, bk) : f64_map_term2d(m, t, bk);
@@ -1343,8 +1624,15 @@ cudaError_t launch_batch_f64_tma(DProdT<double, kNarrowDests>* prods, int count,
   a.maps = reinterpret_cast<const CUtensorMap*>(dev);
   a.gp = reinterpret_cast<const DProdT<double, kNarrowDests>*>(reinterpret_cast<const unsigned char*>(dev) + mbytes);
   a.tile_prod = reinterpret_cast<const int*>(reinterpret_cast<const unsigned char*>(dev) + mbytes + dbytes);
-  if (dynamic) {
-    cudaError_t e = cudaMemsetAsync(sync, 0, (size_t)n_sync * sizeof(int), s);
+  if (!rnodes.empty()) {
+    a.ride_nodes = (int)rnodes.size();
+    a.ride_chunks = ride_chunks;
+    a.ride = reinterpret_cast<const RideNode*>(reinterpret_cast<const unsigned char*>(dev) + mbytes + dbytes + tbytes);
+    a.ride_sync = sync + n_sync;
+  }
+  if (dynamic || !rnodes.empty()) {
+    const size_t ints = (size_t)n_sync + (rnodes.empty() ? 0 : 1 + (size_t)ride_phases);
+    cudaError_t e = cudaMemsetAsync(sync, 0, ints * sizeof(int), s);
     if (e != cudaSuccess) return e;
   }
   if (ns == 1 && nt == 1) return tma_kernel_launch<WST_BK, 1, 1>(a, total, s);

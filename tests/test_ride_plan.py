@@ -1,0 +1,110 @@
+"""Riding operand sums (ATA_OPF_RIDE, auto_plan._hoist_sums): the reordered
+plans keep their sequential meaning, every flagged COMBO4 sits directly in
+front of a product group and is element-wise independent of it (the executor
+runs it concurrently with that group's launch)."""
+import numpy as np
+import pytest
+from hypothesis import given, settings, strategies as st
+
+from oracle import atamul_oracle as O
+from paper_2110_13042_b200 import _native as nat
+from paper_2110_13042_b200 import auto_plan
+
+import plan_interp
+
+
+def _cells(ref, lower=False):
+    rows, cols, off, ld = int(ref["rows"]), int(ref["cols"]), int(ref["off"]), int(ref["ld"])
+    if rows == 0 or cols == 0:
+        return set()
+    r, c = np.meshgrid(np.arange(rows), np.arange(cols), indexing="ij")
+    keep = (c <= r) if lower else np.ones_like(r, dtype=bool)
+    return {(int(ref["base"]), int(e)) for e in (off + r * ld + c)[keep].ravel()}
+
+
+def _reads_writes(op):
+    t = int(op["type"])
+    reads, writes = set(), set()
+    for j in range(int(op["ns"])):
+        reads |= _cells(op["s"][j])
+    if t in (nat.OP_GEMM, nat.OP_POSTADD7):
+        for j in range(int(op["nt"])):
+            reads |= _cells(op["t"][j])
+    for j in range(int(op["nd"])):
+        writes |= _cells(op["d"][j])
+    return reads, writes
+
+
+def _ride_runs(ops):
+    """[(first, last, group_first, group_last)]: maximal runs of flagged ops and
+    the product group that follows each."""
+    out, i, n = [], 0, len(ops)
+    while i < n:
+        if int(ops[i]["flags"]) & nat.OPF_RIDE:
+            j = i
+            while j < n and int(ops[j]["flags"]) & nat.OPF_RIDE:
+                j += 1
+            k = j
+            while k < n and int(ops[k]["type"]) in (nat.OP_GEMM, nat.OP_SYRK) and \
+                    int(ops[k]["group"]) == int(ops[j]["group"]):
+                k += 1
+            out.append((i, j, j, k))
+            i = j
+        else:
+            i += 1
+    return out
+
+
+FORCED_DFS = dict(leaf_cols=16, min_dim=4, max_depth=3, hbm_gbs=1e9, ws_budget_gb=2e-5)
+
+
+@settings(max_examples=25, deadline=None)
+@given(m=st.integers(40, 260), n=st.integers(40, 200), seed=st.integers(0, 2**16),
+       budget=st.sampled_from([4e-6, 2e-5, 1e-4]))
+def test_hoisted_plan_semantics(m, n, seed, budget):
+    a = np.random.default_rng(seed).uniform(-1, 1, (m, n))
+    params = auto_plan.AutoParams(**{**FORCED_DFS, "ws_budget_gb": budget})
+    p = auto_plan.plan_ata_auto(m, n, n, n, params)
+    c = np.zeros((n, n))
+    c[np.triu_indices(n, 1)] = 7.0
+    plan_interp.run(p.ops, a, c, 1.0, WS=np.zeros(max(1, p.ws_scalars)))
+    assert np.all(c[np.triu_indices(n, 1)] == 7.0)
+    assert O.rel_frobenius_lower(c, O.gram(a)) <= 1e-12
+    # same multiplications and ops as the plan without riding sums
+    q = auto_plan.plan_ata_auto(m, n, n, n, auto_plan.AutoParams(**{**FORCED_DFS, "ws_budget_gb": budget,
+                                                                    "ride_sums": False}))
+    assert q.mults == p.mults and len(q.ops) == len(p.ops)
+    assert not (q.ops["flags"] & nat.OPF_RIDE).any()
+
+
+@pytest.mark.parametrize("m,n", [(192, 160), (257, 131), (300, 96)])
+def test_ride_ops_precede_a_group_and_are_independent_of_it(m, n):
+    p = auto_plan.plan_ata_auto(m, n, n, n, auto_plan.AutoParams(**FORCED_DFS))
+    ops = p.ops
+    runs = _ride_runs(ops)
+    assert runs, "the forced depth-first plan has riding sums"
+    assert int((ops["flags"] & nat.OPF_RIDE).sum()) == sum(j - i for i, j, _, _ in runs)
+    for (i, j, g0, g1) in runs:
+        assert g1 > g0, "a riding run is followed by a product group"
+        assert all(int(ops[q]["type"]) == nat.OP_COMBO4 and int(ops[q]["accumulate"]) == 0 for q in range(i, j))
+        g_reads, g_writes = set(), set()
+        for q in range(g0, g1):
+            r, w = _reads_writes(ops[q])
+            g_reads |= r
+            g_writes |= w
+        for q in range(i, j):
+            r, w = _reads_writes(ops[q])
+            assert not (w & g_reads) and not (w & g_writes) and not (r & g_writes), (q, g0, g1)
+
+
+def test_c4_plan_rides_most_operand_sums():
+    """Config c4: every leaf group except each tree's first carries the next group's sums."""
+    p = auto_plan.plan_ata_auto(65536, 32768, 32768, 32768, auto_plan.AutoParams())
+    ops = p.ops
+    combo = ops["type"] == nat.OP_COMBO4
+    ride = (ops["flags"] & nat.OPF_RIDE) != 0
+    assert not (ride & ~combo).any()
+    assert ride.sum() >= 0.9 * combo.sum()
+    q = auto_plan.plan_ata_auto(65536, 32768, 32768, 32768, auto_plan.AutoParams(ride_sums=False))
+    assert q.mults == p.mults
+    assert p.ws_scalars * 8 <= 50e9      # the alternating regions cost < 10 GB on c4

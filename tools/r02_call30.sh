@@ -1,0 +1,11 @@
+set -x
+python -c "import __graft_entry__ as g; g.build()" || exit 1
+timeout 240 python tools/ride_check.py 2>&1 | tail -14
+[ "${PIPESTATUS[0]}" = 0 ] || { echo "ride_check failed"; exit 1; }
+for r in 0 1; do
+  ATA_RIDE=$r timeout 400 python bench.py --config c4 --steps 3 --warmup 2 --no-e2e --no-cpu --dump-units gpurun_out/ride${r}_units_c4.json > gpurun_out/ride${r}_bench_c4.json 2> gpurun_out/ride${r}_bench_c4.err
+  tail -3 gpurun_out/ride${r}_bench_c4.err
+  python -c "
+import json; d=json.load(open('gpurun_out/ride${r}_bench_c4.json')); r=d['roofline']
+print('c4 ride=$r', round(d['value']), 'ms', round(d['ms_per_step'],2), 'frac', round(r['frac'],4), 'share', round(r['share_of_step'],3))"
+done
