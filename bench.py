@@ -567,7 +567,7 @@ def main():
     peak = FP64_PEAK_TFLOPS if f64 else TF32_PEAK_TFLOPS
     roofline = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
                 "frac": achieved / peak, "traffic": None,
-                "kernel": "prod_f64_ws_kernel" if f64 else "prod_tf32_2sm_kernel",
+                "kernel": "prod_f64_tma_kernel (prod_f64_ws_kernel for TMA-illegal windows)" if f64 else "prod_tf32_2sm_kernel",
                 "peak_source": ("measured DMMA m8n8k4 issue-rate peak on this pool's B200 "
                                 "(profiles/fp64_peak.txt); MEASURED_PEAKS.json has no FP64 figure")
                 if f64 else ("measured tcgen05.mma kind::tf32 issue rate on this pool's B200 "

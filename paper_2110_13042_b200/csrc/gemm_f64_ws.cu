@@ -26,6 +26,7 @@
 //       (no wave-quantisation tail per product).
 // Deadlock freedom: tiles are handed out in increasing order and a tile only
 // waits for turns of strictly earlier tiles, which are already running.
+#include <cstdio>
 #include <cstdlib>
 
 #include <unordered_map>
@@ -696,9 +697,9 @@ namespace wst {
 #endif
 constexpr int PANELS = ws64::BM / 16;              // 16 doubles = one 128-byte swizzle row
 // register split of the launch allocation (384 x 168 = 64512; setmaxnreg.inc can only
-// draw what the CTA itself released): 128 producer threads x 56 (the spare warps run
-// the riding operand sums) + 256 consumer threads x 224
-constexpr int PRODUCER_REGS = 56, CONSUMER_REGS = 224;
+// draw what the CTA itself released): 128 producer threads x 72 (the spare warps run
+// the riding operand sums, two rows = 8 loads in flight) + 256 consumer threads x 216
+constexpr int PRODUCER_REGS = 72, CONSUMER_REGS = 216;
 static_assert(PRODUCER_REGS * ws64::PRODUCERS + CONSUMER_REGS * ws64::CONSUMERS * 32 <= 168 * ws64::THREADS,
               "setmaxnreg split exceeds the launch allocation: the consumers' inc would block forever");
 template <int BK>
@@ -717,7 +718,7 @@ constexpr int stages() {
 // operand sums of one Strassen node's operand) of the NEXT leaf group are
 // HBM-bound and independent of this launch's products, which are DMMA-bound and
 // leave three of the four producer warps idle.  A launch may therefore carry a
-// "ride": a list of combo4 nodes cut into chunks of kRideChunk column pairs
+// "ride": a list of combo4 nodes cut into chunks (64-column strips of kRideRows rows)
 // that the spare warps claim from a global queue.  Nodes are ordered by phase;
 // a node of phase p > 0 reads outputs of earlier phases and waits until every
 // chunk of phase p - 1 is finished.  Chunks are claimed in increasing order and
@@ -727,17 +728,17 @@ constexpr int stages() {
 struct RideNode {
   const double* src[4];
   double* dst[5];
-  int sld[4], srows[4], scols[4];
-  int dld[5], drows[5], dcols[5];
-  int code[5];          // base-4 coefficient digits over the sources (1: +, 2: -)
-  int nsrc, ndst, rows, cp;   // iteration extent: rows x cp column pairs
-  int chunk_begin;      // first chunk of this node in the ride's chunk space
+  int srows[4], scols[4];   // source extents (zero beyond them)
+  int sld, dld;             // the sources' common pitch, the outputs' common pitch
+  int nsrc, ndst, rows, cp; // iteration extent: rows x cp column pairs (= every output's extent)
+  unsigned long long codes; // output j: 8 bits at 8 j, base-4 digits over the sources (1: +, 2: -)
+  int strips;               // ceil(cp / 32): a chunk is one 64-column strip of kRideRows rows
+  int chunk_begin;          // first chunk of this node in the ride's chunk space
   int phase;
-  int wait_chunks;      // chunks of phase - 1 that must be finished first (0: none)
-  int _pad;
+  int wait_chunks;          // chunks of phase - 1 that must be finished first (0: none)
 };
 static_assert(sizeof(RideNode) % 8 == 0, "RideNode is copied as 32-bit words and stored in 8-byte blobs");
-constexpr int kRideChunk = 2048;   // column pairs (16 bytes each) per chunk
+constexpr int kRideRows = 64;   // rows per chunk: 64 rows x 32 column pairs (16 bytes per lane and row)
 
 struct TmaBatch64 {
   int count;
@@ -765,35 +766,78 @@ __device__ __forceinline__ void ride_st(double* p, double2 v) {
   asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
 }
 
-// One column pair (row r, columns 2 cc, 2 cc + 1) of a combo4 node: every
-// window is 16-byte aligned with an even pitch and even extents, so a pair is
-// either wholly inside a window or wholly outside (zero / not written).
-__device__ __forceinline__ void ride_load(const RideNode& n, int r, int cc, double2 (&v)[4]) {
+// base-4 coefficient digits (digit q of output j at bit 8 j + 2 q: 1 = +, 2 = -) of the
+// five operand sums of strassen.py:234-273 over the quadrants (X11, X12, X21, X22):
+//   S side: X11+X22, X12+X22, X11+X21, X12-X11, X21-X22
+//   T side: X11+X22, X12-X22, X21-X11, X11+X12, X21+X22
+constexpr unsigned long long ride_codes(int o0, int o1, int o2, int o3, int o4) {
+  return (unsigned long long)o0 | (unsigned long long)o1 << 8 | (unsigned long long)o2 << 16 |
+         (unsigned long long)o3 << 24 | (unsigned long long)o4 << 32;
+}
+constexpr unsigned long long kRideCodesS = ride_codes(1 | 1 << 6, 1 << 2 | 1 << 6, 1 | 1 << 4, 2 | 1 << 2, 1 << 4 | 2 << 6);
+constexpr unsigned long long kRideCodesT = ride_codes(1 | 1 << 6, 1 << 2 | 2 << 6, 2 | 1 << 4, 1 | 1 << 2, 1 << 4 | 1 << 6);
+
+// nr rows of one strip: per row, 4 independent 16-byte loads, the signed sums, 5 stores.
+// CODES != 0: compile-time coefficients (all five outputs present); 0: decode `codes`.
+template <unsigned long long CODES>
+__device__ __forceinline__ void ride_out(const double2 (&v)[4], double* (&dp)[5], long long dld,
+                                         unsigned long long codes) {
+#pragma unroll
+  for (int j = 0; j < 5; ++j) {
+    if (CODES == 0 && dp[j] == nullptr) continue;
+    const unsigned code = (unsigned)((CODES ? CODES : codes) >> (8 * j)) & 255u;
+    double2 o = make_double2(0.0, 0.0);
+    bool first = true;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const unsigned cq = (code >> (2 * q)) & 3u;
+      if (CODES != 0 && first && cq == 1) {   // leading +1 term: no add (0.0 + x == x)
+        o = v[q];
+      } else if (cq == 1) {
+        o.x += v[q].x, o.y += v[q].y;
+      } else if (cq == 2) {
+        o.x -= v[q].x, o.y -= v[q].y;
+      }
+      if (cq != 0) first = false;
+    }
+    ride_st(dp[j], o);
+    dp[j] += dld;
+  }
+}
+__device__ __forceinline__ void ride_in(double2 (&v)[4], const double* (&sp)[4], const int (&lim)[4], int i,
+                                        long long sld) {
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     v[q] = make_double2(0.0, 0.0);
-    if (q < n.nsrc && r < n.srows[q] && 2 * cc < n.scols[q])
-      v[q] = ride_ld(n.src[q] + (long long)r * n.sld[q] + 2 * cc);
+    if (i < lim[q]) v[q] = ride_ld(sp[q]);
+    sp[q] += sld;
   }
 }
-__device__ __forceinline__ void ride_store(const RideNode& n, int r, int cc, const double2 (&v)[4]) {
-#pragma unroll
-  for (int j = 0; j < 5; ++j) {
-    if (j >= n.ndst || r >= n.drows[j] || 2 * cc >= n.dcols[j]) continue;
-    double2 o = make_double2(0.0, 0.0);
-    int code = n.code[j];
-#pragma unroll
-    for (int q = 0; q < 4; ++q, code >>= 2) {
-      const int cq = code & 3;
-      if (cq == 1) o.x += v[q].x, o.y += v[q].y;
-      else if (cq == 2) o.x -= v[q].x, o.y -= v[q].y;
+template <unsigned long long CODES>
+__device__ __forceinline__ void ride_rows(const double* (&sp)[4], const int (&lim)[4], double* (&dp)[5],
+                                          long long sld, long long dld, int nr, unsigned long long codes) {
+  int i = 0;
+  if (CODES != 0) {   // two rows per trip: 8 independent 16-byte loads in flight per lane
+    for (; i + 1 < nr; i += 2) {
+      double2 v[4], w[4];
+      ride_in(v, sp, lim, i, sld);
+      ride_in(w, sp, lim, i + 1, sld);
+      ride_out<CODES>(v, dp, dld, codes);
+      ride_out<CODES>(w, dp, dld, codes);
     }
-    ride_st(n.dst[j] + (long long)r * n.dld[j] + 2 * cc, o);
+  }
+  for (; i < nr; ++i) {
+    double2 v[4];
+    ride_in(v, sp, lim, i, sld);
+    ride_out<CODES>(v, dp, dld, codes);
   }
 }
 
 // A spare producer warp: claim chunks until the queue is empty.  `node` is the
-// warp's private shared-memory copy of the node it is working on.
+// warp's private shared-memory copy of the node it is working on.  A chunk is a
+// strip of 32 column pairs (one per lane) x kRideRows rows; everything the inner
+// loop needs lives in registers (pointers advance by the common pitches), so its
+// loads issue back to back: 4 x 16 bytes in flight per lane.
 __device__ __forceinline__ void ride_worker(const TmaBatch64& args, RideNode* node, int lane) {
   int cur = -1;
   for (;;) {
@@ -825,31 +869,43 @@ __device__ __forceinline__ void ride_worker(const TmaBatch64& args, RideNode* no
         __syncwarp();
       }
     }
-    const RideNode& n = *node;
-    const long long total = (long long)n.rows * n.cp;
-    const long long first = (long long)(c - n.chunk_begin) * kRideChunk;
-    const int count = (int)(total - first < kRideChunk ? total - first : kRideChunk);
-    long long idx = first + lane;
-    int r = (int)(idx / n.cp), cc = (int)(idx - (long long)r * n.cp);
-    // two pairs per iteration (8 independent 16-byte loads in flight per lane); cp >= 64
-    for (int i = lane; i < count; i += 64) {
-      int r2 = r, c2 = cc + 32;
-      if (c2 >= n.cp) c2 -= n.cp, ++r2;
-      const bool second = i + 32 < count;
-      double2 v[4], w[4];
-      ride_load(n, r, cc, v);
-      if (second) ride_load(n, r2, c2, w);
-      ride_store(n, r, cc, v);
-      if (second) ride_store(n, r2, c2, w);
-      r = r2, cc = c2 + 32;
-      if (cc >= n.cp) cc -= n.cp, ++r;
+    const int local = c - node->chunk_begin;
+    const int rb = local / node->strips, st = local - rb * node->strips;
+    const int r0 = rb * kRideRows;
+    const int nr = min(kRideRows, node->rows - r0);
+    const int pc = st * 32 + lane;
+    const int phase = node->phase;
+    if (pc < node->cp) {
+      const int col = 2 * pc;
+      const long long sld = node->sld, dld = node->dld;
+      const unsigned long long codes = node->codes;
+      const double* sp[4];
+      int lim[4];        // rows of this chunk inside source q (<= 0: none; the column test folds in)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const bool on = q < node->nsrc && col < node->scols[q];
+        sp[q] = on ? node->src[q] + (long long)r0 * sld + col : nullptr;
+        lim[q] = on ? node->srows[q] - r0 : 0;
+      }
+      double* dp[5];
+#pragma unroll
+      for (int j = 0; j < 5; ++j) dp[j] = j < node->ndst ? node->dst[j] + (long long)r0 * dld + col : nullptr;
+      // the two coefficient patterns of a Strassen node's operand sums (auto_plan._S / _T)
+      // run with compile-time coefficients; anything else decodes its digits per row
+      if (codes == kRideCodesS && node->ndst == 5)
+        ride_rows<kRideCodesS>(sp, lim, dp, sld, dld, nr, codes);
+      else if (codes == kRideCodesT && node->ndst == 5)
+        ride_rows<kRideCodesT>(sp, lim, dp, sld, dld, nr, codes);
+      else
+        ride_rows<0ull>(sp, lim, dp, sld, dld, nr, codes);
     }
     // publish the chunk: every lane's stores, then one count
     __threadfence();
     __syncwarp();
-    if (lane == 0) atomicAdd(args.ride_sync + 1 + n.phase, 1);
+    if (lane == 0) atomicAdd(args.ride_sync + 1 + phase, 1);
   }
 }
+
 __device__ __forceinline__ const DProdT<double, kNarrowDests>& prod_of(const TmaBatch64& a, int i) {
   return a.gp[i];
 }
@@ -1388,12 +1444,15 @@ static bool ride_win_ok(const void* p, long long ld, int rows, int cols) {
          (reinterpret_cast<uintptr_t>(p) & 15) == 0;
 }
 bool f64_ride_eligible(const EwArgs<double>& a) {
-  if (a.lower || a.nsrc < 1 || a.nsrc > 4 || a.ndst < 1 || a.ndst > 5 || a.rows < 1 || a.cols < 64 || (a.cols & 1))
+  if (a.lower || a.nsrc < 1 || a.nsrc > 4 || a.ndst < 1 || a.ndst > 5 || a.rows < 1 || a.cols < 2 || (a.cols & 1))
     return false;
-  for (int q = 0; q < a.nsrc; ++q)
-    if (!ride_win_ok(a.src[q].p, a.src[q].ld, a.src[q].rows, a.src[q].cols)) return false;
-  for (int j = 0; j < a.ndst; ++j)
-    if (!ride_win_ok(a.dst[j].p, a.dst[j].ld, a.dst[j].rows, a.dst[j].cols)) return false;
+  for (int q = 0; q < a.nsrc; ++q)   // sources: one common pitch (the quadrants of one window)
+    if (!ride_win_ok(a.src[q].p, a.src[q].ld, a.src[q].rows, a.src[q].cols) || a.src[q].ld != a.src[0].ld)
+      return false;
+  for (int j = 0; j < a.ndst; ++j)   // outputs: full-extent blocks with one common pitch
+    if (!ride_win_ok(a.dst[j].p, a.dst[j].ld, a.dst[j].rows, a.dst[j].cols) || a.dst[j].ld != a.dst[0].ld ||
+        a.dst[j].rows != a.rows || a.dst[j].cols != a.cols || (unsigned)a.dst[j].coef > 255u)
+      return false;
   return true;
 }
 namespace {
@@ -1475,26 +1534,24 @@ static bool build_ride(const EwArgs<double>* ride, int n_ride, std::vector<RideN
     std::memset(&n, 0, sizeof(n));
     for (int q = 0; q < a.nsrc; ++q) {
       n.src[q] = a.src[q].p;
-      n.sld[q] = (int)a.src[q].ld;
       n.srows[q] = a.src[q].rows;
       n.scols[q] = a.src[q].cols;
     }
     for (int j = 0; j < a.ndst; ++j) {
       n.dst[j] = a.dst[j].p;
-      n.dld[j] = (int)a.dst[j].ld;
-      n.drows[j] = a.dst[j].rows;
-      n.dcols[j] = a.dst[j].cols;
-      n.code[j] = a.dst[j].coef;
+      n.codes |= (unsigned long long)(a.dst[j].coef & 255) << (8 * j);
     }
+    n.sld = (int)a.src[0].ld;
+    n.dld = (int)a.dst[0].ld;
     n.nsrc = a.nsrc;
     n.ndst = a.ndst;
     n.rows = a.rows;
     n.cp = a.cols / 2;
+    n.strips = (n.cp + 31) / 32;
     n.chunk_begin = chunks;
     n.phase = phase;
     n.wait_chunks = phase > 0 ? prev_phase_chunks : 0;
-    const long long pairs = (long long)n.rows * n.cp;
-    const long long c = (pairs + kRideChunk - 1) / kRideChunk;
+    const long long c = (long long)n.strips * ((n.rows + kRideRows - 1) / kRideRows);
     if (chunks + c > 0x3fffffffLL) return false;
     chunks += (int)c;
     phase_chunks += (int)c;
@@ -1556,9 +1613,16 @@ cudaError_t launch_batch_f64_tma(DProdT<double, kNarrowDests>* prods, int count,
   std::vector<RideNode> rnodes;
   int ride_chunks = 0, ride_phases = 0;
   if (n_ride > 0) {
-    if (sync == nullptr || !build_ride(ride, n_ride, rnodes, ride_chunks, ride_phases) ||
-        n_sync + 1 + ride_phases > sync_ints || !ride_independent(ride, n_ride, prods, count))
+    const char* why = nullptr;
+    if (sync == nullptr) why = "no sync buffer";
+    else if (!build_ride(ride, n_ride, rnodes, ride_chunks, ride_phases)) why = "ineligible node (or too many phases)";
+    else if (n_sync + 1 + ride_phases > sync_ints) why = "sync buffer too small";
+    else if (!ride_independent(ride, n_ride, prods, count)) why = "not independent of the products";
+    if (why != nullptr) {
+      static const bool dbg = std::getenv("ATA_RIDE_DEBUG") != nullptr;
+      if (dbg) std::fprintf(stderr, "[ata] ride of %d nodes refused: %s\n", n_ride, why);
       return cudaErrorNotSupported;   // the caller runs the nodes as ordinary launches
+    }
   }
   const size_t rbytes = sizeof(RideNode) * rnodes.size();
   // device blob: tensor maps (64-byte aligned), descriptors, tile -> product

@@ -46,11 +46,12 @@ def test_riding_sums_match_blas(m, n, budget, rides):
     assert O.rel_frobenius_lower(got, want) <= 1e-12
     if rides:
         assert carried > 0, "no product launch carried operand sums"
-    # bitwise equal to the plan without riding sums (same ops, same order of arithmetic)
+    # the plan without riding sums: same ops (scratch addresses differ, and with them the
+    # alignment-dependent choice between the TMA and cp.async leaf kernels)
     import dataclasses
     plain, none = _ata(a, dataclasses.replace(params, ride_sums=False))
     assert none == 0
-    assert np.array_equal(np.tril(got), np.tril(plain))
+    assert O.rel_frobenius_lower(got, np.tril(plain)) <= 1e-14
 
 
 def test_riding_is_deterministic_and_alpha_linear():
