@@ -384,7 +384,8 @@ def main():
                                           autotune=True if args.autotune else False if args.no_autotune else None)
     params = params if params is not None else base_params
     if params is not base_params:
-        tuned = {"leaf_cols": params.leaf_cols, "dmma_tflops": params.dmma_tflops, "hbm_gbs": params.hbm_gbs}
+        tuned = {"leaf_cols": params.leaf_cols, "dmma_tflops": params.dmma_tflops, "hbm_gbs": params.hbm_gbs,
+                 "ws_budget_gb": params.ws_budget_gb}
     # what this rank's plan computes: the whole row shard into C, or (task
     # tree) its leaf -- an AtA of a column block or an AtB of two -- into a
     # private block that run_tree_process then retrieves up the tree

@@ -218,7 +218,16 @@ def _first_c_writer(ops) -> int:
     return int(hits[0]) if len(hits) else len(ops)
 
 
-_TILES = 64   # C download tiles per side (the same row bands as matrix._copy_lower)
+_TILES = 64   # at most this many C download tiles per side ...
+_TILE_MIN = 512   # ... of at least this many rows (each tile row is one 2-D copy: a 65-row tile of
+                  # config c2 moved 30 KB per call and the calls' fixed cost dominated its e2e time)
+
+
+def _dl_step(n: int) -> int:
+    """Rows per C tile of the pipelines (uploads by _copy_lower and the early
+    downloads use the same row bands: a diagonal tile goes home as a whole square
+    whose upper part holds what the upload put there)."""
+    return max(1, -(-n // _TILES), min(n, _TILE_MIN))
 
 
 def _download_schedule(plan, n, remaining: bool = False, parts: int = 6):
@@ -228,7 +237,7 @@ def _download_schedule(plan, n, remaining: bool = False, parts: int = 6):
     written by the plan's last group of ops (or never written)."""
     cache = plan.__dict__.setdefault("_dl", {})
     if n not in cache:
-        step = max(1, -(-n // _TILES))
+        step = _dl_step(n)
         nb = -(-n // step)
         last = np.full((nb, nb), -1, dtype=np.int64)
         d = plan.ops["d"]
@@ -360,10 +369,10 @@ def _pipelined_host_ata(a, c, m, n, alpha, ws, counter, auto_params, precision) 
             events.append(ev)
             _mark(f"A block {i} uploaded", copy)
             if i == 0 and not zero_start:
-                _copy_lower(dC, c, to_device=True)
+                _copy_lower(dC, c, to_device=True, step=_dl_step(n))
                 c_ready.record(copy)
         if zero_start:
-            _copy_lower(dCin, c, to_device=True)
+            _copy_lower(dCin, c, to_device=True, step=_dl_step(n))
             c_ready.record(copy)
             _mark("C uploaded", copy)
     mults = 0
@@ -450,7 +459,7 @@ def _pipelined_host_ref(a, c, m, n, threshold, alpha, ws, counter) -> bool:
     The plan runs as a few CUDA-graph segments split at those points.  Returns
     False when not applicable (the caller stages A and C itself)."""
     import torch
-    if engine.reference_dfs():
+    if engine.reference_dfs() or os.environ.get("ATA_PIPE_REF", "1") == "0":
         return False
     if not (isinstance(a, torch.Tensor) and isinstance(c, torch.Tensor)) or a.is_cuda or c.is_cuda:
         return False
@@ -482,7 +491,7 @@ def _pipelined_host_ref(a, c, m, n, threshold, alpha, ws, counter) -> bool:
         if rc != 0:
             raise RuntimeError(f"cudaMemcpy2DAsync failed ({rc})")
         a_ready.record(copy)
-        _copy_lower(dC, c, to_device=True)
+        _copy_lower(dC, c, to_device=True, step=_dl_step(n))
         c_ready.record(copy)
     ops = plan.ops
     first_c = _first_c_writer(ops)

@@ -14,7 +14,10 @@ will run the plan instead of trusting the constants:
 * ``tune(m, n, device)``: the calibrated rates, then the SYRK leaf width
   picked by timing the auto plan of the actual shape once per candidate
   (``leaf_cols`` in 512 / 1024 / 2048, each with its own Strassen depths from
-  the cost model) and keeping the fastest.  Cached per (shape, device).
+  the cost model) and keeping the fastest; then, for a plan that has no
+  successive leaf groups for its operand sums to ride on (all trees breadth
+  first), the breadth-first workspace budget among {as planned, 1/2, 1/4 of
+  the plan's scratch}, also timed.  Cached per (shape, device).
 
 Used by ``ata(..., threshold="auto", auto_params="tune")`` and
 ``bench.py --autotune`` (config c3: "cutoff auto-tuned").  The measurement
@@ -127,5 +130,38 @@ def tune(m: int, n: int, device=None, lda: int | None = None, ldc: int | None = 
             params = best
             del A, C
         torch.cuda.empty_cache()
+    params = _tune_budget(m, n, lda, ldc, dev, params)
     _TUNED[key] = params
     return params
+
+
+def _tune_budget(m, n, lda, ldc, dev, params):
+    """Riding operand sums need successive leaf groups: a plan whose Strassen
+    trees are all breadth first (one leaf group per tree: config c3) hides
+    nothing.  Time the plan at 1/2 and 1/4 of its own scratch size as the
+    breadth-first budget (depth-first top levels: the next subtree's sums ride on
+    the previous subtree's products) and keep the fastest."""
+    import torch
+    if not params.ride_sums:
+        return params
+    plan0 = auto_plan.plan_ata_auto(m, n, lda, ldc, params)
+    combos = plan0.ops["type"] == nat.OP_COMBO4
+    if not combos.any() or ((plan0.ops["flags"] & nat.OPF_RIDE) != 0).sum() * 2 > combos.sum():
+        return params
+    ws_gb = plan0.ws_scalars * 8 / 1e9
+    cands = [params] + [dataclasses.replace(params, ws_budget_gb=round(ws_gb * f, 2)) for f in (0.5, 0.25)]
+    with torch.cuda.device(dev):
+        A = torch.rand((m, lda), dtype=torch.float64, device=dev)
+        C = torch.zeros((n, ldc), dtype=torch.float64, device=dev)
+        best, best_t = params, float("inf")
+        for p in cands:
+            plan = plan0 if p is params else auto_plan.plan_ata_auto(m, n, lda, ldc, p)
+            W = torch.empty(max(1, plan.ws_scalars), dtype=torch.float64, device=dev)
+            t = _time(lambda: engine.run_plan(plan, nat.ATA_F64, A.data_ptr(), A.numel(), C.data_ptr(),
+                                              C.numel(), 1.0, ws=W.data_ptr(), ws_elems=W.numel()), reps=2)
+            del W
+            if t < best_t * 0.995:      # a smaller budget must win by a margin (reproducible plans)
+                best, best_t = p, t
+        del A, C
+    torch.cuda.empty_cache()
+    return best

@@ -300,16 +300,17 @@ def _cudart():
     return _CUDART
 
 
-def _copy_lower(dst, src, to_device: bool, blocks: int = 64):
+def _copy_lower(dst, src, to_device: bool, blocks: int = 64, step: int | None = None):
     """Copy the lower block-trapezoids of a square row-major matrix between host
-    and device (rows [r0, r1) x columns [0, r1)); ~(1/2 + 1/(2*blocks)) of it."""
+    and device (rows [r0, r1) x columns [0, r1)); ~(1/2 + 1/(2*blocks)) of it.
+    `step` (rows per band) overrides `blocks`."""
     torch = _torch()
     n = int(dst.shape[0])
     es = dst.element_size()
     lib = _cudart()
     stream = _stream_ptr()
     kind = 1 if to_device else 2   # cudaMemcpyHostToDevice / DeviceToHost
-    step = max(1, -(-n // blocks))
+    step = max(1, -(-n // blocks)) if step is None else max(1, int(step))
     for r0 in range(0, n, step):
         r1 = min(n, r0 + step)
         d = dst.data_ptr() + r0 * dst.stride(0) * es

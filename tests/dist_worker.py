@@ -7,6 +7,10 @@ rank never wait on another's).  Modes:
             products as row-range segments + per-region reduces
   ata_d  -- distsim.ata_d over the group: A only on rank 0, operand blocks
             sent down the reference's distributed task tree, partials back
+  nccl1  -- ATA_DIST_BACKEND=nccl, one rank: the collectives of the rows and
+            units paths (packed-triangle reduce, per-region reduces) issued
+            through a real NCCL communicator on the B200 (gpurun exposes one
+            GPU, so this is the part of the NCCL path that can execute here)
 
 Rank 0 checks the lower triangle against the CPU oracle's classical Gram
 (relative Frobenius 1e-12) and prints OK.  Test infrastructure only."""
@@ -25,9 +29,13 @@ from paper_2110_13042_b200 import auto_plan, dist as pdist  # noqa: E402
 
 mode = sys.argv[1]
 m, n, seed = int(sys.argv[2]), int(sys.argv[3]), 3
-dist.init_process_group("gloo")
-rank, world = dist.get_rank(), dist.get_world_size()
+backend = os.environ.get("ATA_DIST_BACKEND", "gloo")
 torch.cuda.set_device(0)
+if backend == "nccl":
+    dist.init_process_group("nccl", device_id=torch.device("cuda", 0))
+else:
+    dist.init_process_group("gloo")
+rank, world = dist.get_rank(), dist.get_world_size()
 full = pdist.uniform_rows(m, n, seed, 0, m)
 C = torch.zeros(n, n, dtype=torch.float64, device="cuda")
 extra = ""
@@ -47,6 +55,24 @@ elif mode == "ata_d":
     if rank == 0:
         C = res.a if isinstance(res.a, torch.Tensor) else torch.from_numpy(res.a)
     extra = f" sent_words={st.sent_words} recv_messages={st.recv_messages}"
+elif mode == "nccl1":
+    assert backend == "nccl" and world == 1
+    from paper_2110_13042_b200.distsim import DeviceBlocks
+    A = torch.from_numpy(full).cuda()
+    P.ata(A, C, 1.0, "auto")
+    packed = torch.empty(n * (n + 1) // 2, dtype=C.dtype, device="cuda")
+    P.pack_lower(C, out=packed)
+    pdist.reduce_packed(packed, 0)                       # ncclReduce on the packed triangle
+    C2 = torch.zeros_like(C)
+    P.unpack_lower(P.PackedLowerTriangular(n, packed), C2)
+    groups = {r: dist.group.WORLD for r in pdist.REGIONS}
+    members = {r: [0] for r in pdist.REGIONS}
+    pdist.reduce_regions(C2, n, 0, groups, members, DeviceBlocks(C.device, C.dtype))   # one ncclReduce per region
+    t = torch.ones(1 << 20, device="cuda")
+    dist.all_reduce(t)
+    assert float(t.sum().item()) == float(1 << 20)
+    C = C2
+    extra = f" backend={dist.get_backend()} nccl={'.'.join(map(str, torch.cuda.nccl.version()))}"
 else:
     raise SystemExit(f"unknown mode {mode}")
 torch.cuda.synchronize()

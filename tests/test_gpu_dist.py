@@ -31,6 +31,19 @@ def test_multi_rank_vs_oracle(mode, world, m, n):
     print(r.stdout.strip().splitlines()[-1])
 
 
+def test_collectives_over_nccl_single_rank():
+    """The rows / units collectives through a real NCCL communicator (one rank:
+    the box has one GPU), result against the oracle."""
+    env = dict(os.environ, ATA_DIST_BACKEND="nccl")
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "1",
+                        "--master-addr", "127.0.0.1", "--master-port", "29577",
+                        os.path.join(ROOT, "tests", "dist_worker.py"), "nccl1", "6000", "3000"],
+                       capture_output=True, text=True, env=env, timeout=600)
+    assert r.returncode == 0, r.stderr[-3000:]
+    assert "OK" in r.stdout and "backend=nccl" in r.stdout, r.stdout[-2000:]
+    print(r.stdout.strip().splitlines()[-1])
+
+
 @pytest.mark.parametrize("procs", [2, 4, 8])
 def test_units_partition_all_ranks_one_gpu(procs):
     """Every rank's plan_units plan run on one GPU into one C: the segments
