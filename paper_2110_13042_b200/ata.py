@@ -459,7 +459,7 @@ def _pipelined_host_ref(a, c, m, n, threshold, alpha, ws, counter) -> bool:
     The plan runs as a few CUDA-graph segments split at those points.  Returns
     False when not applicable (the caller stages A and C itself)."""
     import torch
-    if engine.reference_dfs() or os.environ.get("ATA_PIPE_REF", "1") == "0":
+    if engine.reference_dfs() or os.environ.get("ATA_PIPE_REF", "0") != "1":
         return False
     if not (isinstance(a, torch.Tensor) and isinstance(c, torch.Tensor)) or a.is_cuda or c.is_cuda:
         return False
