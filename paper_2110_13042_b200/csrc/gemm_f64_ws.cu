@@ -757,12 +757,20 @@ struct TmaBatch64 {
   int* ride_sync;                               // [0] chunk queue, [1 + p] finished chunks of phase p
 };
 
+// A/B probes (tools/ride_ab.py): RIDE_AB_NOLOAD / NOSTORE / NOADD drop one ingredient of
+// the riding sums (wrong results, timing only)
 __device__ __forceinline__ double2 ride_ld(const double* p) {
   double2 v;
+#ifdef RIDE_AB_NOLOAD
+  return make_double2((double)(reinterpret_cast<uintptr_t>(p) & 255), 1.0);
+#endif
   asm volatile("ld.global.cs.v2.f64 {%0, %1}, [%2];" : "=d"(v.x), "=d"(v.y) : "l"(p));
   return v;
 }
 __device__ __forceinline__ void ride_st(double* p, double2 v) {
+#ifdef RIDE_AB_NOSTORE
+  if (v.x != 1.2345e300) return;
+#endif
   asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
 }
 
@@ -793,11 +801,14 @@ __device__ __forceinline__ void ride_out(const double2 (&v)[4], double* (&dp)[5]
       const unsigned cq = (code >> (2 * q)) & 3u;
       if (CODES != 0 && first && cq == 1) {   // leading +1 term: no add (0.0 + x == x)
         o = v[q];
-      } else if (cq == 1) {
+      }
+#ifndef RIDE_AB_NOADD
+      else if (cq == 1) {
         o.x += v[q].x, o.y += v[q].y;
       } else if (cq == 2) {
         o.x -= v[q].x, o.y -= v[q].y;
       }
+#endif
       if (cq != 0) first = false;
     }
     ride_st(dp[j], o);
