@@ -327,7 +327,12 @@ def _pipelined_host_ata(a, c, m, n, alpha, ws, counter, auto_params, precision) 
     round_tf32 = precision == "tf32" and c.dtype == torch.float32
     params = auto_params or auto_plan.AutoParams()
     blocks = []
-    for (r0, rows) in _row_blocks(m, n, es, round_tf32 or es == 4):
+    rb = _row_blocks(m, n, es, round_tf32 or es == 4)
+    if not (PIPELINE_ZERO_C and len(rb) >= 3 and rb[0][1] * 2 < rb[1][1]) and params.diag_first:
+        # C is uploaded behind block 0 and awaited by its first C writer: keep the
+        # diagonal SYRK leaves (C writers) out of the front of the plan
+        params = dataclasses.replace(params, diag_first=False)
+    for (r0, rows) in rb:
         # each block's plan takes the Strassen tree of the whole A (cost model at m
         # rows): the blocks together execute the single plan's multiplications
         bp = dataclasses.replace(params, cost_row_scale=params.cost_row_scale * m / rows)

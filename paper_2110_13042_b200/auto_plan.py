@@ -87,6 +87,11 @@ class AutoParams:
                                    # group's product launch (ATA_OPF_RIDE, executed by the leaf kernel's
                                    # spare warps while the DMMAs run): scratch of successive leaf groups
                                    # alternates between two regions and _hoist_sums reorders / flags the ops
+    diag_first: bool = True        # riding sums + a depth-first top tree: the diagonal SYRK leaves (they
+                                   # read only A) run as the FIRST product group, so the top tree's first
+                                   # operand sums ride on them instead of running exposed.  The host
+                                   # pipeline turns it off when C is uploaded behind block 0 (the SYRKs
+                                   # write C)
     tail_split: bool = True        # FP64: K-split a group's trailing products (partial last wave)
     min_tail_rows: int = 1024      # ... only when every chunk keeps this many rows
 
@@ -494,6 +499,9 @@ class _AutoPlanner:
                     diag_prods = []
                     self.ws_top = self.ws_floor
                 else:
+                    if diag_prods and self._riding() and self.p.diag_first and not self.pb.rows:
+                        self.emit_products(diag_prods)     # nothing before it: the first launch
+                        diag_prods = []
                     for (a, b, c) in blocks:
                         self.node(a, b, a.rows, a.cols, b.cols, c, 1.0, True, self.p.max_depth)
             level = nxt

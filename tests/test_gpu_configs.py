@@ -77,7 +77,7 @@ def _run(name, host_path=True):
     got, params = _device_result(name, a)
     err = O.rel_frobenius_lower_blocked(got, ref)
     _record(name, "device (bench value)", err,
-            {"plan_params": {k: getattr(params, k) for k in ("leaf_cols", "dmma_tflops", "hbm_gbs")}
+            {"plan_params": {k: getattr(params, k) for k in ("leaf_cols", "dmma_tflops", "hbm_gbs", "ws_budget_gb", "ride_sums", "diag_first")}
              if params is not None else None})
     assert err <= TOL[name], err
     del got
