@@ -71,6 +71,8 @@ def parse():
                    help="auto plan: breadth-first workspace budget in GB (smaller: depth-first Strassen "
                         "subtrees, whose operand sums ride on the previous subtree's product launch)")
     p.add_argument("--no-ride", action="store_true", help="A/B: plan without riding operand sums")
+    p.add_argument("--ride-gbs", type=float, default=None,
+                   help="A/B: additions (GB/s of a launch's own duration) a product launch may carry")
     p.add_argument("--no-diag-first", action="store_true",
                    help="A/B: diagonal SYRK leaves in the last leaf group instead of the first launch")
     p.add_argument("--fuse-leaf-sums", action="store_true",
@@ -376,6 +378,7 @@ def main():
                                                         ("ws_budget_gb", args.ws_budget),
                                                         ("ride_sums", False if args.no_ride else None),
                                                         ("diag_first", False if args.no_diag_first else None),
+                                                        ("ride_gbs", args.ride_gbs),
                                                         ("fuse_leaf_sums", args.fuse_leaf_sums or None))
                                                      if v is not None})
     mloc = r1 - r0

@@ -87,6 +87,9 @@ class AutoParams:
                                    # group's product launch (ATA_OPF_RIDE, executed by the leaf kernel's
                                    # spare warps while the DMMAs run): scratch of successive leaf groups
                                    # alternates between two regions and _hoist_sums reorders / flags the ops
+    ride_gbs: float = 800.0        # additions a product launch hides per second of its own duration
+                                   # (measured, tools/ride_ab.py: free to ~700 GB/s, break-even with
+                                   # separate passes near 1.1 TB/s; c4: 1381 ms at 800, 1389 unlimited); _hoist_sums moves no more
     diag_first: bool = True        # riding sums + a depth-first top tree: the diagonal SYRK leaves (they
                                    # read only A) run as the FIRST product group, so the top tree's first
                                    # operand sums ride on them instead of running exposed.  The host
@@ -533,7 +536,12 @@ def _hit(a, b) -> bool:
                  (b[None, :, 1] < a[:, None, 2])).any())
 
 
-def _hoist_sums(ops):
+def _op_bytes(op, esize: int = 8) -> int:
+    refs = list(op["s"][:int(op["ns"])]) + list(op["d"][:int(op["nd"])])
+    return esize * sum(int(r["rows"]) * int(r["cols"]) for r in refs)
+
+
+def _hoist_sums(ops, ride_gbs: float = 800.0, tflops: float = 35.0):
     """Reorder a plan for riding operand sums (AutoParams.ride_sums).
 
     Between the end of a product group G and the start of the next one lie G's
@@ -543,7 +551,9 @@ def _hoist_sums(ops):
     directly in front of G and flagged ATA_OPF_RIDE: the executor then runs it
     inside G's launch, on the FP64 leaf kernel's spare warps, instead of as an HBM
     pass of its own between the two product launches.  The sequential meaning of
-    the op list is unchanged (only independent ops are reordered)."""
+    the op list is unchanged (only independent ops are reordered).  A group carries
+    at most ride_gbs x its own duration (flops / tflops) of additions: beyond
+    that the ride outlasts the products and separate passes are faster."""
     n = len(ops)
     types, groups = ops["type"], ops["group"]
     prod = (types == nat.OP_GEMM) | (types == nat.OP_SYRK)
@@ -567,11 +577,15 @@ def _hoist_sums(ops):
         reads = np.concatenate([r for r, _ in rw])
         writes = np.concatenate([w for _, w in rw])
         moved, stay = [], []
+        flops = sum(2.0 * int(o["m"]) * int(o["n"]) * int(o["k"]) if int(o["type"]) == nat.OP_GEMM
+                    else 1.0 * int(o["m"]) * int(o["n"]) * (int(o["n"]) + 1) for o in ops[g0:g1])
+        room = ride_gbs * 1e9 * flops / (tflops * 1e12)      # bytes this group can hide
         for q in range(g1, nxt):
             r, w = _op_spans(ops, q)
             free = (int(types[q]) == nat.OP_COMBO4 and int(ops[q]["accumulate"]) == 0 and
                     not _hit(w, reads) and not _hit(w, writes) and not _hit(r, writes))
-            if free:
+            if free and _op_bytes(ops[q]) <= room:
+                room -= _op_bytes(ops[q])
                 moved.append(q)
             else:
                 stay.append(q)
@@ -589,7 +603,7 @@ def _finish(ap) -> Plan:
     plan = ap.pb.finish()
     plan.ws_scalars = max(plan.ws_scalars, ap.ws_peak)
     if ap.p.ride_sums and ap.esize == 8:
-        plan.ops = _hoist_sums(plan.ops)
+        plan.ops = _hoist_sums(plan.ops, ap.p.ride_gbs, ap.p.dmma_tflops)
     return plan
 
 

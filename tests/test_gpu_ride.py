@@ -11,7 +11,8 @@ from oracle import atamul_oracle as O
 pytestmark = pytest.mark.gpu
 SENT = 1.2345e67
 
-DEEP = dict(leaf_cols=256, min_dim=128, max_depth=3, hbm_gbs=1e9)
+# (ride_gbs: no capacity limit, so these small plans exercise the riding path)
+DEEP = dict(leaf_cols=256, min_dim=128, max_depth=3, hbm_gbs=1e9, ride_gbs=1e12)
 
 
 def _ata(a, params, alpha=1.0):

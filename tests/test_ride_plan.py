@@ -55,7 +55,8 @@ def _ride_runs(ops):
     return out
 
 
-FORCED_DFS = dict(leaf_cols=16, min_dim=4, max_depth=3, hbm_gbs=1e9, ws_budget_gb=2e-5)
+# (ride_gbs: no capacity limit -- these toy products are far too short to hide anything)
+FORCED_DFS = dict(leaf_cols=16, min_dim=4, max_depth=3, hbm_gbs=1e9, ws_budget_gb=2e-5, ride_gbs=1e12)
 
 
 @settings(max_examples=25, deadline=None)
@@ -104,7 +105,22 @@ def test_c4_plan_rides_most_operand_sums():
     combo = ops["type"] == nat.OP_COMBO4
     ride = (ops["flags"] & nat.OPF_RIDE) != 0
     assert not (ride & ~combo).any()
-    assert ride.sum() >= 0.9 * combo.sum()
+    assert ride.sum() >= 0.85 * combo.sum()      # (the rest: each later tree's first group, and what exceeds ride_gbs)
     q = auto_plan.plan_ata_auto(65536, 32768, 32768, 32768, auto_plan.AutoParams(ride_sums=False))
     assert q.mults == p.mults
     assert p.ws_scalars * 8 <= 50e9      # the alternating regions cost < 10 GB on c4
+
+
+def test_ride_capacity_limits_what_a_group_carries():
+    """A product group carries at most ride_gbs x its own duration of additions."""
+    base = dict(leaf_cols=256, min_dim=128, max_depth=3, hbm_gbs=1e9, ws_budget_gb=0.02)
+    free = auto_plan.plan_ata_auto(4096, 2048, 2048, 2048, auto_plan.AutoParams(**base, ride_gbs=1e12))
+    tight = auto_plan.plan_ata_auto(4096, 2048, 2048, 2048, auto_plan.AutoParams(**base, ride_gbs=800.0))
+    none = auto_plan.plan_ata_auto(4096, 2048, 2048, 2048, auto_plan.AutoParams(**base, ride_gbs=0.0))
+    count = lambda p: int(((p.ops["flags"] & nat.OPF_RIDE) != 0).sum())
+    assert count(free) > count(tight) >= count(none) == 0
+    for (i, j, g0, g1) in _ride_runs(tight.ops):
+        flops = sum(2.0 * int(o["m"]) * int(o["n"]) * int(o["k"]) if int(o["type"]) == nat.OP_GEMM
+                    else 1.0 * int(o["m"]) * int(o["n"]) * (int(o["n"]) + 1) for o in tight.ops[g0:g1])
+        moved = sum(auto_plan._op_bytes(o) for o in tight.ops[i:j])
+        assert moved <= 800e9 * flops / (auto_plan.AutoParams().dmma_tflops * 1e12) + 1

@@ -1,0 +1,8 @@
+set -x
+for v in 700 800 600 700 800; do
+  timeout 500 python bench.py --config c4 --steps 5 --warmup 3 --no-e2e --no-cpu --ride-gbs $v > gpurun_out/ab_c4_g.json 2> gpurun_out/ab_c4.err
+  tail -2 gpurun_out/ab_c4.err
+  python -c "
+import json; d=json.load(open('gpurun_out/ab_c4_g.json')); r=d['roofline']
+print('c4 [$v]', round(d['value']), 'ms', round(d['ms_per_step'],2), 'frac', round(r['frac'],4), r['secondary']['share_of_step'])"
+done

@@ -11,9 +11,9 @@ from paper_2110_13042_b200.auto_plan import AutoParams
 
 rng = np.random.default_rng(11)
 lib = nat.load()
-for (m, n, kw) in [(4096, 2048, dict(leaf_cols=256, min_dim=128, ws_budget_gb=0.02, max_depth=3, hbm_gbs=1e9)),
-                   (3000, 1536, dict(leaf_cols=256, min_dim=128, ws_budget_gb=0.01, max_depth=3, hbm_gbs=1e9)),
-                   (2050, 1100, dict(leaf_cols=256, min_dim=128, ws_budget_gb=0.005, max_depth=3, hbm_gbs=1e9)),
+for (m, n, kw) in [(4096, 2048, dict(leaf_cols=256, min_dim=128, ws_budget_gb=0.02, max_depth=3, hbm_gbs=1e9, ride_gbs=1e12)),
+                   (3000, 1536, dict(leaf_cols=256, min_dim=128, ws_budget_gb=0.01, max_depth=3, hbm_gbs=1e9, ride_gbs=1e12)),
+                   (2050, 1100, dict(leaf_cols=256, min_dim=128, ws_budget_gb=0.005, max_depth=3, hbm_gbs=1e9, ride_gbs=1e12)),
                    (8192, 4096, dict(ws_budget_gb=0.2))]:
     A = torch.from_numpy(rng.uniform(-1, 1, (m, n))).cuda()
     want = O.gram_blas(A.cpu().numpy())
