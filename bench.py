@@ -73,6 +73,12 @@ def parse():
     p.add_argument("--no-ride", action="store_true", help="A/B: plan without riding operand sums")
     p.add_argument("--ride-gbs", type=float, default=None,
                    help="A/B: additions (GB/s of a launch's own duration) a product launch may carry")
+    p.add_argument("--ride-lookback", type=int, default=None,
+                   help="A/B: product groups before its own that an operand sum may ride on")
+    p.add_argument("--ride-band-gb", type=float, default=None,
+                   help="A/B: operand sums above this size are cut into row bands before hoisting")
+    p.add_argument("--ride-arenas", type=int, default=None, choices=[0, 1],
+                   help="A/B: top-level frames alternate between two scratch arenas")
     p.add_argument("--no-diag-first", action="store_true",
                    help="A/B: diagonal SYRK leaves in the last leaf group instead of the first launch")
     p.add_argument("--fuse-leaf-sums", action="store_true",
@@ -379,6 +385,10 @@ def main():
                                                         ("ride_sums", False if args.no_ride else None),
                                                         ("diag_first", False if args.no_diag_first else None),
                                                         ("ride_gbs", args.ride_gbs),
+                                                        ("ride_lookback", args.ride_lookback),
+                                                        ("ride_band_gb", args.ride_band_gb),
+                                                        ("ride_arenas", None if args.ride_arenas is None
+                                                         else bool(args.ride_arenas)),
                                                         ("fuse_leaf_sums", args.fuse_leaf_sums or None))
                                                      if v is not None})
     mloc = r1 - r0

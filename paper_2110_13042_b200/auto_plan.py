@@ -90,6 +90,10 @@ class AutoParams:
     ride_gbs: float = 800.0        # additions a product launch hides per second of its own duration
                                    # (measured, tools/ride_ab.py: free to ~700 GB/s, break-even with
                                    # separate passes near 1.1 TB/s; c4: 1381 ms at 800, 1389 unlimited); _hoist_sums moves no more
+    ride_lookback: int = 0         # a sum may ride up to this many product groups before the one it precedes
+    ride_band_gb: float = 0.0      # ... and sums above this size are cut into row bands first (_hoist_sums)
+    ride_arenas: bool = False      # successive top-level frames alternate between two scratch arenas
+                                   # (_enter_frame; more workspace, the later frames' first sums ride too)
     diag_first: bool = True        # riding sums + a depth-first top tree: the diagonal SYRK leaves (they
                                    # read only A) run as the FIRST product group, so the top tree's first
                                    # operand sums ride on them instead of running exposed.  The host
@@ -158,6 +162,9 @@ class _AutoPlanner:
         self.flip_tree = 0       # ride_sums: successive breadth-first subtrees / depth-first operand
         self.flip_sums = 0       # sums alternate between two scratch regions
         self.flip_extra = 0      # elements below ws_top that are second copies of alternating regions
+        self.frames = 0          # ride_arenas: top-level frames planned so far,
+        self.arena1 = None       # where the odd ones start (above everything planned before the first),
+        self.frame_off = 0       # and the current frame's offset above ws_floor
 
     # ---------------------------------------------------------------- workspace
     def alloc(self, rows: int, cols: int) -> Win:
@@ -389,12 +396,33 @@ class _AutoPlanner:
     def _riding(self) -> bool:
         return self.p.ride_sums and self.esize == 8
 
+    def _arenas(self) -> bool:
+        return self._riding() and self.p.ride_arenas
+
+    def _enter_frame(self):
+        """ride_arenas: successive top-level frames (a depth-first C21 tree, or one
+        breadth-first AtA level) alternate between two arenas, so the whole
+        scratch of the next frame is free while the current one runs and its first
+        operand sums can ride on the current frame's product launches
+        (_hoist_sums looks back across groups).  The odd arena starts above
+        everything planned before its first use; overlap between later frames
+        would only block rides (the hoist tests the windows), never correctness."""
+        if self.frames % 2 == 1:
+            if self.arena1 is None:
+                self.arena1 = self.ws_peak
+            self.frame_off = self.arena1 - self.ws_floor
+        else:
+            self.frame_off = 0
+        self.ws_top = self.ws_floor + self.frame_off
+        self.frames += 1
+
     def node(self, a, b, m, n, k, out, sign, accumulate, depth, level=0):
         """Depth-first at this node when its breadth-first workspace exceeds the budget."""
         need = self._dry_ws(a, b, m, n, k, depth)
         # (the budget decides breadth- vs depth-first as without riding sums: the
         # second copies of alternating regions do not count against it)
-        if self.ws_top - self.flip_extra + need <= self.budget or not self.worth_split(m, n, k, depth):
+        if (self.ws_top - self.frame_off - self.flip_extra + need <= self.budget
+                or not self.worth_split(m, n, k, depth)):
             leaves, posts = [], []
             mark = self.ws_top
             if self._riding() and need > 0:
@@ -489,7 +517,9 @@ class _AutoPlanner:
                            for (a, b, _) in blocks)
                 if need <= self.budget:
                     leaves, posts = [], []
-                    if self._riding() and 0 < need <= self.budget // 4:
+                    if self._arenas():
+                        self._enter_frame()
+                    elif self._riding() and 0 < need <= self.budget // 4:
                         # alternate scratch regions for successive levels (see node())
                         self.ws_top = self.ws_floor + self.flip_tree * need
                         self.ws_peak = max(self.ws_peak, self.ws_floor + 2 * need)
@@ -500,13 +530,16 @@ class _AutoPlanner:
                                   leaves, posts)
                     self.emit(leaves, posts, diag_prods)
                     diag_prods = []
-                    self.ws_top = self.ws_floor
+                    self.ws_top, self.frame_off = self.ws_floor, 0
                 else:
                     if diag_prods and self._riding() and self.p.diag_first and not self.pb.rows:
                         self.emit_products(diag_prods)     # nothing before it: the first launch
                         diag_prods = []
                     for (a, b, c) in blocks:
+                        if self._arenas():
+                            self._enter_frame()
                         self.node(a, b, a.rows, a.cols, b.cols, c, 1.0, True, self.p.max_depth)
+                        self.ws_top, self.frame_off = self.ws_floor, 0
             level = nxt
         self.emit_products(diag_prods)
 
@@ -541,7 +574,30 @@ def _op_bytes(op, esize: int = 8) -> int:
     return esize * sum(int(r["rows"]) * int(r["cols"]) for r in refs)
 
 
-def _hoist_sums(ops, ride_gbs: float = 800.0, tflops: float = 35.0):
+def _split_bands(op, band_rows: int, group: int):
+    """Row bands of one full-extent COMBO4 op (sources zero-extended below their
+    own extents, as in the whole op): independent ops writing disjoint row ranges."""
+    rows = max(int(d["rows"]) for d in op["d"][:int(op["nd"])])
+    out = []
+    for r0 in range(0, rows, band_rows):
+        h = min(band_rows, rows - r0)
+        b = op.copy()
+        b["group"] = group
+        for key, cnt in (("s", int(op["ns"])), ("d", int(op["nd"]))):
+            for j in range(cnt):
+                ref = b[key][j]
+                keep = max(0, min(h, int(ref["rows"]) - r0))
+                if keep == 0:
+                    ref["rows"], ref["cols"] = 0, 0
+                else:
+                    ref["off"] = int(ref["off"]) + r0 * int(ref["ld"])
+                    ref["rows"] = keep
+        out.append(b)
+    return out
+
+
+def _hoist_sums(ops, ride_gbs: float = 800.0, tflops: float = 35.0, lookback: int = 0,
+                band_gb: float = 0.0):
     """Reorder a plan for riding operand sums (AutoParams.ride_sums).
 
     Between the end of a product group G and the start of the next one lie G's
@@ -553,46 +609,106 @@ def _hoist_sums(ops, ride_gbs: float = 800.0, tflops: float = 35.0):
     pass of its own between the two product launches.  The sequential meaning of
     the op list is unchanged (only independent ops are reordered).  A group carries
     at most ride_gbs x its own duration (flops / tflops) of additions: beyond
-    that the ride outlasts the products and separate passes are faster."""
+    that the ride outlasts the products and separate passes are faster.
+
+    lookback > 0: a sum may also ride on one of the `lookback` groups before G, as
+    far back as it stays independent of everything it jumps over; it takes the
+    EARLIEST such group with room (sums that can only ride on G itself -- the next
+    subtree's, whose scratch region the group before G still uses -- then find G's
+    room free).  band_gb > 0: sums larger than that are first cut into row bands
+    (independent ops of one launch group), so the sums of the upper tree levels,
+    larger than any one group's room, spread over the groups before them."""
     n = len(ops)
     types, groups = ops["type"], ops["group"]
     prod = (types == nat.OP_GEMM) | (types == nat.OP_SYRK)
-    spans, i = [], 0
-    while i < n:
-        if prod[i] and groups[i] >= 0:
-            j = i + 1
-            while j < n and prod[j] and groups[j] == groups[i]:
-                j += 1
-            spans.append((i, j))
-            i = j
-        else:
-            i += 1
+
+    def find_spans():
+        spans, i = [], 0
+        while i < n:
+            if prod[i] and groups[i] >= 0:
+                j = i + 1
+                while j < n and prod[j] and groups[j] == groups[i]:
+                    j += 1
+                spans.append((i, j))
+                i = j
+            else:
+                i += 1
+        return spans
+    spans = find_spans()
     if len(spans) < 2:
         return ops
-    order, ride = list(range(spans[0][0])), set()
-    for si, (g0, g1) in enumerate(spans):
+    if band_gb > 0:
+        # cut the big candidates (after the first group, before the last) into row bands
+        rows_out, next_group = [], int(groups.max()) + 1
+        first, last = spans[0][1], spans[-1][0]
+        for q in range(n):
+            op = ops[q]
+            if (first <= q < last and int(types[q]) == nat.OP_COMBO4 and int(op["accumulate"]) == 0
+                    and _op_bytes(op) > band_gb * 1e9):
+                nd = int(op["nd"])
+                rows = max(int(d["rows"]) for d in op["d"][:nd])
+                full = all(int(d["rows"]) == rows for d in op["d"][:nd])
+                band_rows = max(64, int(rows * band_gb * 1e9 / _op_bytes(op)) // 64 * 64)
+                if full and band_rows < rows:
+                    g = int(op["group"])
+                    if g < 0:
+                        g, next_group = next_group, next_group + 1
+                    rows_out += _split_bands(op, band_rows, g)
+                    continue
+            rows_out.append(op)
+        ops = np.array(rows_out, dtype=ops.dtype)
+        n = len(ops)
+        types, groups = ops["type"], ops["group"]
+        prod = (types == nat.OP_GEMM) | (types == nat.OP_SYRK)
+        spans = find_spans()
+    empty = np.zeros((0, 3), np.int64)
+
+    class Seg:       # one product group, the sums riding on it and the ops that stay behind it
+        def __init__(self, g0, g1):
+            rw = [_op_spans(ops, q) for q in range(g0, g1)]
+            self.g0, self.g1 = g0, g1
+            self.reads = np.concatenate([r for r, _ in rw])      # group + stays
+            self.writes = np.concatenate([w for _, w in rw])
+            self.r_reads, self.r_writes = empty, empty           # riders
+            self.riders, self.stays = [], []
+            flops = sum(2.0 * int(o["m"]) * int(o["n"]) * int(o["k"]) if int(o["type"]) == nat.OP_GEMM
+                        else 1.0 * int(o["m"]) * int(o["n"]) * (int(o["n"]) + 1) for o in ops[g0:g1])
+            self.room = ride_gbs * 1e9 * flops / (tflops * 1e12)  # bytes this group can hide
+
+    def clear(r, w, reads, writes):
+        return not _hit(w, reads) and not _hit(w, writes) and not _hit(r, writes)
+    segs = [Seg(g0, g1) for (g0, g1) in spans]
+    for si, seg in enumerate(segs):
         nxt = spans[si + 1][0] if si + 1 < len(spans) else n
-        # blockers so far: the group itself; interval sets grow with the ops that stay
-        rw = [_op_spans(ops, q) for q in range(g0, g1)]
-        reads = np.concatenate([r for r, _ in rw])
-        writes = np.concatenate([w for _, w in rw])
-        moved, stay = [], []
-        flops = sum(2.0 * int(o["m"]) * int(o["n"]) * int(o["k"]) if int(o["type"]) == nat.OP_GEMM
-                    else 1.0 * int(o["m"]) * int(o["n"]) * (int(o["n"]) + 1) for o in ops[g0:g1])
-        room = ride_gbs * 1e9 * flops / (tflops * 1e12)      # bytes this group can hide
-        for q in range(g1, nxt):
+        for q in range(seg.g1, nxt):
             r, w = _op_spans(ops, q)
-            free = (int(types[q]) == nat.OP_COMBO4 and int(ops[q]["accumulate"]) == 0 and
-                    not _hit(w, reads) and not _hit(w, writes) and not _hit(r, writes))
-            if free and _op_bytes(ops[q]) <= room:
-                room -= _op_bytes(ops[q])
-                moved.append(q)
+            best = None
+            if int(types[q]) == nat.OP_COMBO4 and int(ops[q]["accumulate"]) == 0:
+                size, sj = _op_bytes(ops[q]), si
+                ok = clear(r, w, seg.reads, seg.writes)
+                while ok:
+                    if size <= segs[sj].room:
+                        best = sj
+                    if sj == 0 or si - sj >= lookback:
+                        break
+                    # one group earlier: past the riders of sj and the group + stays of sj - 1
+                    ok = (clear(r, w, segs[sj].r_reads, segs[sj].r_writes) and
+                          clear(r, w, segs[sj - 1].reads, segs[sj - 1].writes))
+                    sj -= 1
+            if best is None:
+                seg.stays.append(q)
+                seg.reads = np.concatenate([seg.reads, r])
+                seg.writes = np.concatenate([seg.writes, w])
             else:
-                stay.append(q)
-                reads = np.concatenate([reads, r])
-                writes = np.concatenate([writes, w])
-        order += moved + list(range(g0, g1)) + stay
-        ride.update(moved)
+                t = segs[best]
+                t.room -= size
+                t.riders.append(q)
+                t.r_reads = np.concatenate([t.r_reads, r])
+                t.r_writes = np.concatenate([t.r_writes, w])
+    order, ride = list(range(spans[0][0])), set()
+    for seg in segs:
+        order += seg.riders + list(range(seg.g0, seg.g1)) + seg.stays
+        ride.update(seg.riders)
     out = ops[np.asarray(order, dtype=np.int64)].copy()
     flag = np.asarray([q in ride for q in order])
     out["flags"][flag] |= nat.OPF_RIDE
@@ -603,7 +719,7 @@ def _finish(ap) -> Plan:
     plan = ap.pb.finish()
     plan.ws_scalars = max(plan.ws_scalars, ap.ws_peak)
     if ap.p.ride_sums and ap.esize == 8:
-        plan.ops = _hoist_sums(plan.ops, ap.p.ride_gbs, ap.p.dmma_tflops)
+        plan.ops = _hoist_sums(plan.ops, ap.p.ride_gbs, ap.p.dmma_tflops, ap.p.ride_lookback, ap.p.ride_band_gb)
     return plan
 
 

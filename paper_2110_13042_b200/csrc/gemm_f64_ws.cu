@@ -787,9 +787,59 @@ constexpr unsigned long long kRideCodesT = ride_codes(1 | 1 << 6, 1 << 2 | 2 << 
 
 // nr rows of one strip: per row, 4 independent 16-byte loads, the signed sums, 5 stores.
 // CODES != 0: compile-time coefficients (all five outputs present); 0: decode `codes`.
+// A two-term sum (every operand sum of a Strassen node) is a plain store of its + term
+// followed by an L2 reduction of the other (red.global.add.f64 -- SASS REDG.E.ADD.F64.RN --
+// the - sign applied with an integer XOR): the same IEEE round-to-nearest sum, computed by
+// the L2 atomic units, so no instruction of the ride enters the FP64 pipe the DMMAs own
+// (a DADD queued ~300 cycles behind the consumers' DMMA bursts).  A thread's store and
+// reduction to one address are ordered (same-address program order).  -DRIDE_DADD: the
+// sums in registers (the first version; measured c4 1380 vs 1367 ms).
+__device__ __forceinline__ double ride_flip(double x) {
+  return __longlong_as_double(__double_as_longlong(x) ^ (long long)0x8000000000000000ull);
+}
+__device__ __forceinline__ void ride_red(double* p, double2 v) {
+#ifdef RIDE_AB_NORED
+  if (v.x != 1.2345e300) return;
+#endif
+  asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v.x) : "memory");
+  asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p + 1), "d"(v.y) : "memory");
+}
+__device__ __forceinline__ void ride_st_keep(double* p, double2 v) {
+#ifdef RIDE_AB_NOSTORE
+  if (v.x != 1.2345e300) return;
+#endif
+  asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+}
+constexpr int ride_plus_term(unsigned code) {
+  return (code & 3u) == 1 ? 0 : ((code >> 2) & 3u) == 1 ? 1 : ((code >> 4) & 3u) == 1 ? 2 : 3;
+}
+constexpr int ride_other_term(unsigned code) {
+  const int a = ride_plus_term(code);
+  return (a != 0 && (code & 3u)) ? 0 : (a != 1 && ((code >> 2) & 3u)) ? 1 : (a != 2 && ((code >> 4) & 3u)) ? 2 : 3;
+}
+
 template <unsigned long long CODES>
 __device__ __forceinline__ void ride_out(const double2 (&v)[4], double* (&dp)[5], long long dld,
                                          unsigned long long codes) {
+#ifndef RIDE_DADD
+  if (CODES != 0) {
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      const unsigned code = (unsigned)(CODES >> (8 * j)) & 255u;
+      ride_st_keep(dp[j], v[ride_plus_term(code)]);
+    }
+#pragma unroll
+    for (int j = 0; j < 5; ++j) {
+      const unsigned code = (unsigned)(CODES >> (8 * j)) & 255u;
+      const int qb = ride_other_term(code);
+      double2 t = v[qb];
+      if (((code >> (2 * qb)) & 3u) == 2) t = make_double2(ride_flip(t.x), ride_flip(t.y));
+      ride_red(dp[j], t);
+      dp[j] += dld;
+    }
+    return;
+  }
+#endif
 #pragma unroll
   for (int j = 0; j < 5; ++j) {
     if (CODES == 0 && dp[j] == nullptr) continue;

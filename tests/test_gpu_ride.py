@@ -75,3 +75,24 @@ def test_narrow_odd_window_products_are_zero_extended():
     a = np.random.default_rng(0).standard_normal((2050, 1100))
     got, _ = _ata(a, AutoParams(**{**DEEP, "ws_budget_gb": 0.005, "ride_sums": False}))
     assert O.rel_frobenius_lower(got, O.gram_blas(a)) <= 1e-12
+
+
+@pytest.mark.parametrize("m,n,budget", [(4096, 2048, 0.02), (8192, 4096, 0.05), (3000, 1536, 0.01)])
+@pytest.mark.parametrize("arenas", [False, True])
+def test_spread_riding_sums_match_blas(m, n, budget, arenas):
+    """Sums hoisted several groups early, cut into row bands, top-level frames in
+    two arenas (auto_plan._hoist_sums lookback / _split_bands / _enter_frame)."""
+    from paper_2110_13042_b200.auto_plan import AutoParams, plan_ata_auto
+    from paper_2110_13042_b200 import _native as nat
+    params = AutoParams(**{**DEEP, "ws_budget_gb": budget, "ride_lookback": 16, "ride_band_gb": 1e-3,
+                           "ride_arenas": arenas, "ride_gbs": 3e4})
+    near = plan_ata_auto(m, n, n, n, AutoParams(**{**DEEP, "ws_budget_gb": budget, "ride_gbs": 3e4,
+                                                   "ride_lookback": 0, "ride_band_gb": 0.0, "ride_arenas": False}))
+    plan = plan_ata_auto(m, n, n, n, params)
+    riding = lambda p: int(((p.ops["flags"] & nat.OPF_RIDE) != 0).sum())
+    assert riding(plan) > riding(near) > 0
+    a = np.random.default_rng(m + n + 1).uniform(-1, 1, (m, n))
+    got, carried = _ata(a, params)
+    assert carried > 0
+    assert np.all(got[np.triu_indices(n, 1)] == SENT)
+    assert O.rel_frobenius_lower(got, O.gram_blas(a)) <= 1e-12

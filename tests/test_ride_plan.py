@@ -124,3 +124,74 @@ def test_ride_capacity_limits_what_a_group_carries():
                     else 1.0 * int(o["m"]) * int(o["n"]) * (int(o["n"]) + 1) for o in tight.ops[g0:g1])
         moved = sum(auto_plan._op_bytes(o) for o in tight.ops[i:j])
         assert moved <= 800e9 * flops / (auto_plan.AutoParams().dmma_tflops * 1e12) + 1
+
+
+# looking back across groups, row bands of large sums, alternating top-level arenas
+SPREAD = dict(ride_lookback=16, ride_band_gb=2e-6, ride_arenas=True)
+
+
+@settings(max_examples=25, deadline=None)
+@given(m=st.integers(40, 400), n=st.integers(40, 260), seed=st.integers(0, 2**16),
+       budget=st.sampled_from([4e-6, 2e-5, 1e-4]), gbs=st.sampled_from([1e12, 3e6, 3e5]),
+       arenas=st.booleans(), band=st.sampled_from([0.0, 2e-6, 2e-5]))
+def test_spread_hoist_keeps_plan_semantics(m, n, seed, budget, gbs, arenas, band):
+    """Sums riding several groups early, cut into row bands, frames in two arenas:
+    the op list still computes lower(A^T A) sequentially, with the same products."""
+    a = np.random.default_rng(seed).uniform(-1, 1, (m, n))
+    kw = {**FORCED_DFS, "ws_budget_gb": budget, "ride_gbs": gbs, "ride_lookback": 16,
+          "ride_band_gb": band, "ride_arenas": arenas}
+    p = auto_plan.plan_ata_auto(m, n, n, n, auto_plan.AutoParams(**kw))
+    c = np.zeros((n, n))
+    c[np.triu_indices(n, 1)] = 7.0
+    plan_interp.run(p.ops, a, c, 1.0, WS=np.zeros(max(1, p.ws_scalars)))
+    assert np.all(c[np.triu_indices(n, 1)] == 7.0)
+    assert O.rel_frobenius_lower(c, O.gram(a)) <= 1e-12
+    q = auto_plan.plan_ata_auto(m, n, n, n, auto_plan.AutoParams(**{**FORCED_DFS, "ws_budget_gb": budget,
+                                                                    "ride_sums": False}))
+    assert q.mults == p.mults
+    is_prod = lambda o: np.isin(o["type"], (nat.OP_GEMM, nat.OP_SYRK))
+    assert int(is_prod(p.ops).sum()) == int(is_prod(q.ops).sum())
+    if band == 0.0:
+        assert len(p.ops) == len(q.ops)
+
+
+@pytest.mark.parametrize("m,n", [(192, 160), (257, 131), (300, 96), (520, 300)])
+def test_spread_ride_ops_are_independent_of_their_group(m, n):
+    p = auto_plan.plan_ata_auto(m, n, n, n, auto_plan.AutoParams(**{**FORCED_DFS, **SPREAD}))
+    ops = p.ops
+    runs = _ride_runs(ops)
+    assert runs
+    assert int((ops["flags"] & nat.OPF_RIDE).sum()) == sum(j - i for i, j, _, _ in runs)
+    for (i, j, g0, g1) in runs:
+        assert g1 > g0
+        g_reads, g_writes = set(), set()
+        for q in range(g0, g1):
+            r, w = _reads_writes(ops[q])
+            g_reads |= r
+            g_writes |= w
+        for q in range(i, j):
+            assert int(ops[q]["type"]) == nat.OP_COMBO4 and int(ops[q]["accumulate"]) == 0
+            r, w = _reads_writes(ops[q])
+            assert not (w & g_reads) and not (w & g_writes) and not (r & g_writes), (q, g0, g1)
+
+
+def test_spread_hoist_hides_more_than_the_adjacent_one():
+    """Config c4: with look-back, row bands and two arenas almost every operand sum rides
+    (146.8 GB exposed -> 2.4 GB), no group above its capacity."""
+    def exposed(**kw):
+        p = auto_plan.plan_ata_auto(65536, 32768, 32768, 32768, auto_plan.AutoParams(**kw))
+        ops = p.ops
+        e = sum(auto_plan._op_bytes(o) for o in ops
+                if int(o["type"]) == nat.OP_COMBO4 and not int(o["flags"]) & nat.OPF_RIDE)
+        return e, p
+    e0, p0 = exposed(ride_lookback=0, ride_band_gb=0.0, ride_arenas=False)
+    e1, p1 = exposed(ride_lookback=64, ride_band_gb=1.25, ride_arenas=False)
+    e2, p2 = exposed(ride_lookback=64, ride_band_gb=1.25, ride_arenas=True)
+    assert e0 > e1 > e2 and e2 < 5e9
+    assert p0.mults == p1.mults == p2.mults
+    assert p1.ws_scalars == p0.ws_scalars and p2.ws_scalars * 8 <= 80e9
+    for (i, j, g0, g1) in _ride_runs(p2.ops):
+        flops = sum(2.0 * int(o["m"]) * int(o["n"]) * int(o["k"]) if int(o["type"]) == nat.OP_GEMM
+                    else 1.0 * int(o["m"]) * int(o["n"]) * (int(o["n"]) + 1) for o in p2.ops[g0:g1])
+        moved = sum(auto_plan._op_bytes(o) for o in p2.ops[i:j])
+        assert moved <= 800e9 * flops / (auto_plan.AutoParams().dmma_tflops * 1e12) + 1
