@@ -77,7 +77,9 @@ def ata(A, C, alpha=1.0, threshold=DEFAULT_THRESHOLD, ws: StrassenWorkspace | No
             raise ValueError(f"auto_params must be AutoParams, None or 'tune', not {auto_params!r}")
         auto_params = _tuned_params(a, c, m, n)
     if threshold == AUTO:
-        auto_params = fit_workspace_budget(auto_params or auto_plan.AutoParams())
+        es = 4 if str(getattr(c, "dtype", "")).endswith("float32") else 8
+        auto_params = fit_workspace_budget(auto_params or auto_plan.AutoParams(),
+                                           resident_bytes=(m * n + 2 * n * n) * es)
     if threshold == AUTO and _pipelined_host_ata(a, c, m, n, alpha, ws, counter, auto_params, precision):
         return
     if threshold != AUTO and _pipelined_host_ref(a, c, m, n, threshold, alpha, ws, counter):
@@ -137,24 +139,30 @@ def even_pitch(op, slot: int = 0):
     return op
 
 
-def fit_workspace_budget(params, device=None, headroom: float = 0.8):
+def fit_workspace_budget(params, device=None, headroom: float = 0.8, resident_bytes: int = 0):
     """AutoParams whose breadth-first workspace budget (default 40 GB) fits the
     HBM this process can still get: free device memory plus what torch's
     caching allocator holds unused, times `headroom`.  Unchanged (same plans,
     same cache keys) whenever the default budget fits -- e.g. c4 on a 180 GB
     B200 -- and a smaller budget (depth-first Strassen subtrees, less scratch)
-    when the device is shared or nearly full."""
+    when the device is shared or nearly full.  The second scratch arena of
+    riding plans (AutoParams.ride_arenas, up to twice the workspace) is kept
+    only when the operands (`resident_bytes`) plus that workspace fit the
+    device's TOTAL memory -- a figure that does not move between calls, so
+    repeated calls plan alike while their buffers are alive."""
     import dataclasses
     import torch
     if not torch.cuda.is_available():
         return params
     dev = torch.device("cuda", torch.cuda.current_device()) if device is None else device
-    free, _ = torch.cuda.mem_get_info(dev)
+    free, total = torch.cuda.mem_get_info(dev)
     avail = free + torch.cuda.memory_reserved(dev) - torch.cuda.memory_allocated(dev)
     cap_gb = avail * headroom / 1e9
-    if cap_gb >= params.ws_budget_gb:
-        return params
-    return dataclasses.replace(params, ws_budget_gb=max(0.5, round(cap_gb, 1)))
+    if cap_gb < params.ws_budget_gb:
+        return dataclasses.replace(params, ws_budget_gb=max(0.5, round(cap_gb, 1)), ride_arenas=False)
+    if params.ride_arenas and resident_bytes + 2.2e9 * params.ws_budget_gb > headroom * total:
+        return dataclasses.replace(params, ride_arenas=False)
+    return params
 
 
 def _tuned_params(a, c, m, n):

@@ -87,13 +87,17 @@ class AutoParams:
                                    # group's product launch (ATA_OPF_RIDE, executed by the leaf kernel's
                                    # spare warps while the DMMAs run): scratch of successive leaf groups
                                    # alternates between two regions and _hoist_sums reorders / flags the ops
-    ride_gbs: float = 800.0        # additions a product launch hides per second of its own duration
+    ride_gbs: float = 650.0        # additions a product launch hides per second of its own duration
                                    # (measured, tools/ride_ab.py: free to ~700 GB/s, break-even with
-                                   # separate passes near 1.1 TB/s; c4: 1381 ms at 800, 1389 unlimited); _hoist_sums moves no more
-    ride_lookback: int = 0         # a sum may ride up to this many product groups before the one it precedes
-    ride_band_gb: float = 0.0      # ... and sums above this size are cut into row bands first (_hoist_sums)
-    ride_arenas: bool = False      # successive top-level frames alternate between two scratch arenas
-                                   # (_enter_frame; more workspace, the later frames' first sums ride too)
+                                   # separate passes near 1.1 TB/s; c4 with the spread hoist below: 1347 ms
+                                   # at 650, 1351 at 800, 1364 at 1000); _hoist_sums moves no more
+    ride_lookback: int = 64        # a sum may ride up to this many product groups before the one it precedes
+    ride_band_gb: float = 1.25     # ... and sums above this size are cut into row bands first (_hoist_sums);
+                                   # c4: exposed operand sums 146.8 -> 94.2 GB, 1367 -> 1360 ms
+    ride_arenas: bool = True       # successive top-level frames alternate between two scratch arenas
+                                   # (_enter_frame): the later frames' first sums ride too (c4: exposed
+                                   # 94.2 -> 2.4 GB, 1360 -> 1351 ms; workspace 45.6 -> 76.4 GB;
+                                   # ata.fit_workspace_budget turns it off when HBM is short)
     diag_first: bool = True        # riding sums + a depth-first top tree: the diagonal SYRK leaves (they
                                    # read only A) run as the FIRST product group, so the top tree's first
                                    # operand sums ride on them instead of running exposed.  The host

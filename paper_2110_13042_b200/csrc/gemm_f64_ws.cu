@@ -793,22 +793,44 @@ constexpr unsigned long long kRideCodesT = ride_codes(1 | 1 << 6, 1 << 2 | 2 << 
 // the L2 atomic units, so no instruction of the ride enters the FP64 pipe the DMMAs own
 // (a DADD queued ~300 cycles behind the consumers' DMMA bursts).  A thread's store and
 // reduction to one address are ordered (same-address program order).  -DRIDE_DADD: the
-// sums in registers (the first version; measured c4 1380 vs 1367 ms).
+// sums in registers (the first version; measured c4 1380 vs 1367 ms); -DRIDE_RED_MASK=bits:
+// only those outputs go through L2 reductions, the others are added in registers.
 __device__ __forceinline__ double ride_flip(double x) {
   return __longlong_as_double(__double_as_longlong(x) ^ (long long)0x8000000000000000ull);
+}
+// (RIDE_POLICY: stores and reductions carry an L2 evict_first policy, so the sums stream
+// through L2 without displacing the operand panels the products re-read; RIDE_ST_CS: the
+// store alone is a streaming store)
+__device__ __forceinline__ unsigned long long ride_policy() {
+  unsigned long long pol;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
+  return pol;
 }
 __device__ __forceinline__ void ride_red(double* p, double2 v) {
 #ifdef RIDE_AB_NORED
   if (v.x != 1.2345e300) return;
 #endif
+#ifdef RIDE_POLICY
+  const unsigned long long pol = ride_policy();
+  asm volatile("red.global.add.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p), "d"(v.x), "l"(pol) : "memory");
+  asm volatile("red.global.add.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(p + 1), "d"(v.y), "l"(pol) : "memory");
+#else
   asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p), "d"(v.x) : "memory");
   asm volatile("red.global.add.f64 [%0], %1;" ::"l"(p + 1), "d"(v.y) : "memory");
+#endif
 }
 __device__ __forceinline__ void ride_st_keep(double* p, double2 v) {
 #ifdef RIDE_AB_NOSTORE
   if (v.x != 1.2345e300) return;
 #endif
+#if defined(RIDE_POLICY)
+  const unsigned long long pol = ride_policy();
+  asm volatile("st.global.L2::cache_hint.v2.f64 [%0], {%1, %2}, %3;" ::"l"(p), "d"(v.x), "d"(v.y), "l"(pol) : "memory");
+#elif defined(RIDE_ST_CS)
+  asm volatile("st.global.cs.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+#else
   asm volatile("st.global.v2.f64 [%0], {%1, %2};" ::"l"(p), "d"(v.x), "d"(v.y) : "memory");
+#endif
 }
 constexpr int ride_plus_term(unsigned code) {
   return (code & 3u) == 1 ? 0 : ((code >> 2) & 3u) == 1 ? 1 : ((code >> 4) & 3u) == 1 ? 2 : 3;
@@ -821,15 +843,22 @@ constexpr int ride_other_term(unsigned code) {
 template <unsigned long long CODES>
 __device__ __forceinline__ void ride_out(const double2 (&v)[4], double* (&dp)[5], long long dld,
                                          unsigned long long codes) {
-#ifndef RIDE_DADD
+#ifndef RIDE_RED_MASK
+#ifdef RIDE_DADD
+#define RIDE_RED_MASK 0
+#else
+#define RIDE_RED_MASK 31   // bit j: output j of a compile-time pattern is a store + L2 reduction
+#endif
+#endif
   if (CODES != 0) {
 #pragma unroll
     for (int j = 0; j < 5; ++j) {
       const unsigned code = (unsigned)(CODES >> (8 * j)) & 255u;
-      ride_st_keep(dp[j], v[ride_plus_term(code)]);
+      if (RIDE_RED_MASK >> j & 1) ride_st_keep(dp[j], v[ride_plus_term(code)]);
     }
 #pragma unroll
     for (int j = 0; j < 5; ++j) {
+      if (!(RIDE_RED_MASK >> j & 1)) continue;
       const unsigned code = (unsigned)(CODES >> (8 * j)) & 255u;
       const int qb = ride_other_term(code);
       double2 t = v[qb];
@@ -837,12 +866,11 @@ __device__ __forceinline__ void ride_out(const double2 (&v)[4], double* (&dp)[5]
       ride_red(dp[j], t);
       dp[j] += dld;
     }
-    return;
   }
-#endif
 #pragma unroll
   for (int j = 0; j < 5; ++j) {
     if (CODES == 0 && dp[j] == nullptr) continue;
+    if (CODES != 0 && (RIDE_RED_MASK >> j & 1)) continue;
     const unsigned code = (unsigned)((CODES ? CODES : codes) >> (8 * j)) & 255u;
     double2 o = make_double2(0.0, 0.0);
     bool first = true;
@@ -878,6 +906,20 @@ template <unsigned long long CODES>
 __device__ __forceinline__ void ride_rows(const double* (&sp)[4], const int (&lim)[4], double* (&dp)[5],
                                           long long sld, long long dld, int nr, unsigned long long codes) {
   int i = 0;
+#ifdef RIDE_PIPE
+  if (CODES != 0 && nr >= 2) {   // rows alternate between two register sets: the next row's loads
+    double2 v[4], w[4];          // are issued before the current row's stores
+    ride_in(v, sp, lim, 0, sld);
+    for (; i + 1 < nr; i += 2) {
+      ride_in(w, sp, lim, i + 1, sld);
+      ride_out<CODES>(v, dp, dld, codes);
+      if (i + 2 < nr) ride_in(v, sp, lim, i + 2, sld);
+      ride_out<CODES>(w, dp, dld, codes);
+    }
+    if (i < nr) ride_out<CODES>(v, dp, dld, codes);
+    return;
+  }
+#endif
   if (CODES != 0) {   // two rows per trip: 8 independent 16-byte loads in flight per lane
     for (; i + 1 < nr; i += 2) {
       double2 v[4], w[4];
