@@ -349,7 +349,9 @@ def _pipelined_host_ata(a, c, m, n, alpha, ws, counter, auto_params, precision) 
             key, lambda rows=rows, bp=bp: auto_plan.plan_ata_auto(rows, n, n, n, bp, round_tf32=round_tf32))))
     need = max(p.ws_scalars for (_, _, p) in blocks)
     if ws is None:
-        ws = workspace_for_ata(m, n, AUTO, dtype=c.dtype)
+        # the cached arena of this shape (shared with the device-operand path: one
+        # workspace per shape, grown to the larger of the two plans' needs)
+        ws = _default_workspace(m, n, AUTO, c.dtype)
     wbuf = ws.ensure(dev, extra=need, dtype=c.dtype) if need > 0 else None
     wptr = int(wbuf.data_ptr()) if wbuf is not None else 0
     wel = int(wbuf.numel()) if wbuf is not None else 0

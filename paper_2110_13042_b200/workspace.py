@@ -186,6 +186,7 @@ class StrassenWorkspace:
                 and self.buffer.numel() >= max(need, 1)):
             return self.buffer
         self.extra = max(self.extra, extra)
+        self.buffer = None      # release the smaller arena before allocating its replacement
         self.buffer = _new_buffer(max(need, 1), tdt, device)
         self.device = device
         return self.buffer
