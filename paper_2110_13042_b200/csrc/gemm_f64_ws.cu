@@ -796,7 +796,13 @@ constexpr unsigned long long kRideCodesT = ride_codes(1 | 1 << 6, 1 << 2 | 2 << 
 // sums in registers (the first version; measured c4 1380 vs 1367 ms); -DRIDE_RED_MASK=bits:
 // only those outputs go through L2 reductions, the others are added in registers.
 __device__ __forceinline__ double ride_flip(double x) {
-  return __longlong_as_double(__double_as_longlong(x) ^ (long long)0x8000000000000000ull);
+  // (asm: written as C++ the XOR is folded into an fneg, which ptxas emits as a DADD)
+  unsigned lo, hi;
+  double y;
+  asm volatile("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "d"(x));
+  asm volatile("xor.b32 %0, %0, 0x80000000;" : "+r"(hi));
+  asm volatile("mov.b64 %0, {%1, %2};" : "=d"(y) : "r"(lo), "r"(hi));
+  return y;
 }
 // (RIDE_POLICY: stores and reductions carry an L2 evict_first policy, so the sums stream
 // through L2 without displacing the operand panels the products re-read; RIDE_ST_CS: the
@@ -893,27 +899,33 @@ __device__ __forceinline__ void ride_out(const double2 (&v)[4], double* (&dp)[5]
     dp[j] += dld;
   }
 }
+// FULL: every source covers all rows of the chunk (no per-row limit tests)
+template <bool FULL>
 __device__ __forceinline__ void ride_in(double2 (&v)[4], const double* (&sp)[4], const int (&lim)[4], int i,
                                         long long sld) {
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
-    v[q] = make_double2(0.0, 0.0);
-    if (i < lim[q]) v[q] = ride_ld(sp[q]);
+    if (FULL) {
+      v[q] = ride_ld(sp[q]);
+    } else {
+      v[q] = make_double2(0.0, 0.0);
+      if (i < lim[q]) v[q] = ride_ld(sp[q]);
+    }
     sp[q] += sld;
   }
 }
-template <unsigned long long CODES>
+template <unsigned long long CODES, bool FULL>
 __device__ __forceinline__ void ride_rows(const double* (&sp)[4], const int (&lim)[4], double* (&dp)[5],
                                           long long sld, long long dld, int nr, unsigned long long codes) {
   int i = 0;
 #ifdef RIDE_PIPE
   if (CODES != 0 && nr >= 2) {   // rows alternate between two register sets: the next row's loads
     double2 v[4], w[4];          // are issued before the current row's stores
-    ride_in(v, sp, lim, 0, sld);
+    ride_in<FULL>(v, sp, lim, 0, sld);
     for (; i + 1 < nr; i += 2) {
-      ride_in(w, sp, lim, i + 1, sld);
+      ride_in<FULL>(w, sp, lim, i + 1, sld);
       ride_out<CODES>(v, dp, dld, codes);
-      if (i + 2 < nr) ride_in(v, sp, lim, i + 2, sld);
+      if (i + 2 < nr) ride_in<FULL>(v, sp, lim, i + 2, sld);
       ride_out<CODES>(w, dp, dld, codes);
     }
     if (i < nr) ride_out<CODES>(v, dp, dld, codes);
@@ -923,15 +935,15 @@ __device__ __forceinline__ void ride_rows(const double* (&sp)[4], const int (&li
   if (CODES != 0) {   // two rows per trip: 8 independent 16-byte loads in flight per lane
     for (; i + 1 < nr; i += 2) {
       double2 v[4], w[4];
-      ride_in(v, sp, lim, i, sld);
-      ride_in(w, sp, lim, i + 1, sld);
+      ride_in<FULL>(v, sp, lim, i, sld);
+      ride_in<FULL>(w, sp, lim, i + 1, sld);
       ride_out<CODES>(v, dp, dld, codes);
       ride_out<CODES>(w, dp, dld, codes);
     }
   }
   for (; i < nr; ++i) {
     double2 v[4];
-    ride_in(v, sp, lim, i, sld);
+    ride_in<FULL>(v, sp, lim, i, sld);
     ride_out<CODES>(v, dp, dld, codes);
   }
 }
@@ -995,12 +1007,16 @@ __device__ __forceinline__ void ride_worker(const TmaBatch64& args, RideNode* no
       for (int j = 0; j < 5; ++j) dp[j] = j < node->ndst ? node->dst[j] + (long long)r0 * dld + col : nullptr;
       // the two coefficient patterns of a Strassen node's operand sums (auto_plan._S / _T)
       // run with compile-time coefficients; anything else decodes its digits per row
-      if (codes == kRideCodesS && node->ndst == 5)
-        ride_rows<kRideCodesS>(sp, lim, dp, sld, dld, nr, codes);
-      else if (codes == kRideCodesT && node->ndst == 5)
-        ride_rows<kRideCodesT>(sp, lim, dp, sld, dld, nr, codes);
-      else
-        ride_rows<0ull>(sp, lim, dp, sld, dld, nr, codes);
+      const bool full = lim[0] >= nr && lim[1] >= nr && lim[2] >= nr && lim[3] >= nr;
+      if (codes == kRideCodesS && node->ndst == 5) {
+        if (full) ride_rows<kRideCodesS, true>(sp, lim, dp, sld, dld, nr, codes);
+        else ride_rows<kRideCodesS, false>(sp, lim, dp, sld, dld, nr, codes);
+      } else if (codes == kRideCodesT && node->ndst == 5) {
+        if (full) ride_rows<kRideCodesT, true>(sp, lim, dp, sld, dld, nr, codes);
+        else ride_rows<kRideCodesT, false>(sp, lim, dp, sld, dld, nr, codes);
+      } else {
+        ride_rows<0ull, false>(sp, lim, dp, sld, dld, nr, codes);
+      }
     }
     // publish the chunk: every lane's stores, then one count
     __threadfence();
