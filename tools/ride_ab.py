@@ -63,6 +63,8 @@ def main():
              (58, 48, 4096, 1024), (0, 64, 2048, 512), (58, 64, 2048, 512)]
     if len(sys.argv) > 1 and sys.argv[1] == "bound":
         cases = [(58, 48, 4096, 1024), (58, 64, 4096, 1024)]
+    if len(sys.argv) > 1 and sys.argv[1] == "bound2":
+        cases = [(58, 64, 4096, 1024), (58, 96, 4096, 1024), (58, 128, 4096, 1024), (58, 192, 4096, 1024)]
     for (nprod, nodes, rows, cols) in cases:
         plan, moved = plan_for(nprod, m, nodes, rows, cols, lda)
         ws = torch.empty(max(1, plan.ws_scalars), dtype=torch.float64, device="cuda")
