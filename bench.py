@@ -383,6 +383,7 @@ def main():
                                                         ("max_depth", args.max_depth),
                                                         ("min_dim", args.min_dim),
                                                         ("gain", args.gain),
+                                                        ("gain_ride", args.gain),
                                                         ("ws_budget_gb", args.ws_budget),
                                                         ("ride_sums", False if args.no_ride else None),
                                                         ("diag_first", False if args.no_diag_first else None),
@@ -695,7 +696,12 @@ def main():
             "input_gen_s": t_gen}
     # ---- e2e through the public API with pinned host buffers (N = 1) ----
     if world == 1 and not args.no_e2e:
+        # the device leg's buffers go first: ata() below stages its own A, C and workspace
         del C
+        wsbuf = None
+        if "ws" in locals() and getattr(ws, "buffer", None) is not None:
+            ws.buffer = None
+        graph = None
         torch.cuda.empty_cache()
         hA = torch.from_numpy(host).pin_memory()
         hC = torch.zeros((n, n), dtype=A.dtype).pin_memory()

@@ -36,6 +36,7 @@ multiplication count differs (reported as plan.mults).
 """
 from __future__ import annotations
 
+import dataclasses
 import os
 from dataclasses import dataclass
 
@@ -79,6 +80,8 @@ class AutoParams:
                                    # combo4 pass for the last Strassen level).  Off: measured
                                    # 2.1-2.2x slower on c3/c4 (the two-term kernel configuration
                                    # runs at 14 TF/s vs 34 for plain operands)
+    min_leaf_rows: int = 0         # never split a node whose children would contract fewer rows than this
+                                   # (the units partition plans row pieces with their unit's tree: 1024)
     cost_row_scale: float = 1.0    # the cost model sees m * this many contraction rows: a row
                                    # block of a larger A (the pinned-host pipeline) gets the
                                    # Strassen tree of the whole A, so the blocks' executed
@@ -87,10 +90,15 @@ class AutoParams:
                                    # group's product launch (ATA_OPF_RIDE, executed by the leaf kernel's
                                    # spare warps while the DMMAs run): scratch of successive leaf groups
                                    # alternates between two regions and _hoist_sums reorders / flags the ops
-    ride_gbs: float = 650.0        # additions a product launch hides per second of its own duration
-                                   # (measured, tools/ride_ab.py: free to ~700 GB/s, break-even with
-                                   # separate passes near 1.1 TB/s; c4 with the spread hoist below: 1347 ms
-                                   # at 650, 1351 at 800, 1364 at 1000); _hoist_sums moves no more
+    ride_gbs: float = 1500.0       # additions a product launch hides per second of its own duration
+                                   # (measured, tools/ride_ab.py: with no FP64-pipe instruction left in
+                                   # the ride 2.0 TB/s cost +2 % of the launch, 2.5 TB/s +8 %, bound near
+                                   # 2.9 TB/s; c4: 1294 ms at 1200-1600, 1299 unlimited); _hoist_sums moves no more
+    gain_ride: float = 1.0         # the split threshold `gain` of plans with riding sums (their operand
+                                   # sums are nearly free): c4 executes 0.630 of the classical
+                                   # multiplications instead of 0.6735, 1348 -> 1294 ms (deeper still --
+                                   # gain 0.8, max_depth 5, 0.593 -- is slower: 1333 ms, 2048 x 512 x 512
+                                   # leaves run at 0.86-0.88 of the DMMA peak)
     ride_lookback: int = 64        # a sum may ride up to this many product groups before the one it precedes
     ride_band_gb: float = 1.25     # ... and sums above this size are cut into row bands first (_hoist_sums);
                                    # c4: exposed operand sums 146.8 -> 94.2 GB, 1367 -> 1360 ms
@@ -112,6 +120,7 @@ NUM_SMS = 148     # B200
 MAX_BATCH = 48    # products per persistent launch (kMaxBatch, ata_common.cuh)
 MAX_BATCH_NARROW = 104   # FP64 products with <= 2 destinations (kMaxBatchNarrow)
 TAIL_CHUNKS = 4          # K split of a leaf group's trailing products
+UNIT_MIN_LEAF_ROWS = 1024   # units partition: leaf products of a row piece contract at least this many rows
 
 
 def _ceil2(d: int) -> int:
@@ -179,15 +188,16 @@ class _AutoPlanner:
 
     # ------------------------------------------------------------- cost model
     def worth_split(self, m: int, n: int, k: int, depth_left: int) -> bool:
-        if depth_left <= 0 or min(n, k) < 2 * self.p.min_dim or m < 2:
+        if depth_left <= 0 or min(n, k) < 2 * self.p.min_dim or m < 2 or m < 2 * self.p.min_leaf_rows:
             return False
         m = m * self.p.cost_row_scale
+        gain = min(self.p.gain, self.p.gain_ride) if self._riding() else self.p.gain
         saved_s = 2.0 * m * n * k / 8 / (self.rate * 1e12)
         # pre: read both operands, write 5 + 5 quarter sums; post: write 7 child
         # products (leaf epilogue), read them back, write (or RMW) 4 quadrants
         moved = self.esize * (m * n * (1 + 5 / 4) + m * k * (1 + 5 / 4) + n * k * (7 / 4 + 7 / 4 + 2))
         added_s = moved / (self.p.hbm_gbs * 1e9)
-        return saved_s > self.p.gain * added_s
+        return saved_s > gain * added_s
 
     # --------------------------------------------------------------- Strassen
     def _sums(self, a: Win, b: Win, m: int, n: int, k: int, depth: int = 0):
@@ -896,6 +906,19 @@ class _UnitPlanner(_AutoPlanner):
         rows = r1 - r0
         if rows <= 0:
             return
+        # a piece keeps the Strassen tree of its whole unit (cost model at the unit's
+        # rows, like the host pipeline's row blocks): the pieces of a unit together
+        # execute the unit's multiplications, so equal rows are equal work
+        keep = self.p
+        self.p = dataclasses.replace(keep, cost_row_scale=keep.cost_row_scale * unit_rows(unit, m, n) / rows,
+                                     min_leaf_rows=max(keep.min_leaf_rows, UNIT_MIN_LEAF_ROWS))
+        try:
+            self._segment(unit, r0, rows, A, C, m, n)
+        finally:
+            self.p = keep
+
+    def _segment(self, unit: str, r0: int, rows: int, A: Win, C: Win, m: int, n: int):
+        n1, n2, m1 = unit_geometry(m, n)
         mark = self.ws_top
         if unit == "ata_l":
             self.ata_win(A.sub(r0, 0, rows, n1), C.sub(0, 0, n1, n1))

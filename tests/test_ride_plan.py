@@ -106,9 +106,11 @@ def test_c4_plan_rides_most_operand_sums():
     ride = (ops["flags"] & nat.OPF_RIDE) != 0
     assert not (ride & ~combo).any()
     assert ride.sum() >= 0.85 * combo.sum()      # (the rest: each later tree's first group, and what exceeds ride_gbs)
-    q = auto_plan.plan_ata_auto(65536, 32768, 32768, 32768, auto_plan.AutoParams(ride_sums=False))
+    # (plans with riding sums split at gain_ride = 1.0: the same tree without riding sums)
+    q = auto_plan.plan_ata_auto(65536, 32768, 32768, 32768, auto_plan.AutoParams(ride_sums=False, gain=1.0))
     assert q.mults == p.mults
-    assert p.ws_scalars * 8 <= 80e9      # alternating regions + the second top-level arena (45.6 GB without arenas)
+    assert p.mults < 0.64 * 65536 * 32768 * 32769 // 2
+    assert p.ws_scalars * 8 <= 115e9     # alternating regions + the second top-level arena (65.1 GB without arenas)
 
 
 def test_ride_capacity_limits_what_a_group_carries():
@@ -184,9 +186,10 @@ def test_spread_hoist_hides_more_than_the_adjacent_one():
         e = sum(auto_plan._op_bytes(o) for o in ops
                 if int(o["type"]) == nat.OP_COMBO4 and not int(o["flags"]) & nat.OPF_RIDE)
         return e, p
-    e0, p0 = exposed(ride_gbs=800.0, ride_lookback=0, ride_band_gb=0.0, ride_arenas=False)
-    e1, p1 = exposed(ride_gbs=800.0, ride_lookback=64, ride_band_gb=1.25, ride_arenas=False)
-    e2, p2 = exposed(ride_gbs=800.0, ride_lookback=64, ride_band_gb=1.25, ride_arenas=True)
+    old = dict(ride_gbs=800.0, gain_ride=1.25)       # the tree and capacity the hoist was first measured on
+    e0, p0 = exposed(**old, ride_lookback=0, ride_band_gb=0.0, ride_arenas=False)
+    e1, p1 = exposed(**old, ride_lookback=64, ride_band_gb=1.25, ride_arenas=False)
+    e2, p2 = exposed(**old, ride_lookback=64, ride_band_gb=1.25, ride_arenas=True)
     assert e0 > e1 > e2 and e2 < 5e9
     assert p0.mults == p1.mults == p2.mults
     assert p1.ws_scalars == p0.ws_scalars and p2.ws_scalars * 8 <= 80e9

@@ -76,7 +76,7 @@ def test_c4_balance_beats_row_shards():
     for P in (4, 8):
         loads = [ap.plan_units(s, m, n, n, n).mults for s in ap.partition_units(m, n, P, costs=costs)]
         rows_shard = ap.plan_ata_auto(m // P, n, n, n).mults
-        assert max(loads) < 0.96 * rows_shard, (P, max(loads), rows_shard)
+        assert max(loads) < 0.975 * rows_shard, (P, max(loads), rows_shard)
         assert max(loads) <= 1.02 * sum(loads) / P
 
 
