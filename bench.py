@@ -81,6 +81,8 @@ def parse():
                    help="A/B: operand sums above this size are cut into row bands before hoisting")
     p.add_argument("--ride-arenas", type=int, default=None, choices=[0, 1],
                    help="A/B: top-level frames alternate between two scratch arenas")
+    p.add_argument("--no-tail-private", action="store_true",
+                   help="A/B: no K-split tail for leaf groups beyond one shared-destination launch")
     p.add_argument("--no-diag-first", action="store_true",
                    help="A/B: diagonal SYRK leaves in the last leaf group instead of the first launch")
     p.add_argument("--fuse-leaf-sums", action="store_true",
@@ -388,6 +390,7 @@ def main():
                                                         ("ride_sums", False if args.no_ride else None),
                                                         ("diag_first", False if args.no_diag_first else None),
                                                         ("ride_gbs", args.ride_gbs),
+                                                        ("tail_private", False if args.no_tail_private else None),
                                                         ("ride_lookback", args.ride_lookback),
                                                         ("ride_band_gb", args.ride_band_gb),
                                                         ("ride_arenas", None if args.ride_arenas is None

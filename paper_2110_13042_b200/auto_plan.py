@@ -112,6 +112,7 @@ class AutoParams:
                                    # pipeline turns it off when C is uploaded behind block 0 (the SYRKs
                                    # write C)
     tail_split: bool = True        # FP64: K-split a group's trailing products (partial last wave)
+    tail_private: bool = True      # ... groups too large for shared-destination launches: private partials
     min_tail_rows: int = 1024      # ... only when every chunk keeps this many rows
 
 
@@ -292,6 +293,7 @@ class _AutoPlanner:
         (FP64 groups only: ordered accumulation needs the FP64 kernel's turn
         counters).  The trailing products covering one wave of tiles are split
         when the group ends in a partial wave and stays within one launch."""
+        self.tail_private = False
         if self.esize != 8 or not self.p.tail_split:
             return len(prods)
         tl = [self._tiles(p[0], p[2], p[3]) for p in prods]
@@ -305,7 +307,11 @@ class _AutoPlanner:
         if any(prods[q][1] < TAIL_CHUNKS * self.p.min_tail_rows for q in range(j, len(prods))):
             return len(prods)
         if j + (len(prods) - j) * TAIL_CHUNKS > MAX_BATCH_NARROW:
-            return len(prods)
+            # launches with shared destination regions hold at most MAX_BATCH_NARROW products:
+            # the chunks of a larger group's tail write private partials instead (summed by
+            # one small combo4 launch behind the group), which keeps the group one launch
+            self.tail_private = self.p.tail_private
+            return j if self.tail_private else len(prods)
         return j
 
     def _chunks(self, tiles: int, rows: int, nprods: int = 1) -> int:
@@ -353,9 +359,11 @@ class _AutoPlanner:
             # (chunk 0 writes, the rest accumulate in turn through the FP64
             # kernel's per-tile turn counters), issued last so the dynamic tile
             # queue ends with short tiles instead of a partial wave of full ones
+            reductions = []
             for (kind, m, n, k, a, b, out, sign, accumulate) in prods[split_from:]:
-                region = self.pb.new_region()
+                region = 0 if self.tail_private else self.pb.new_region()
                 mc = -(-m // TAIL_CHUNKS)
+                parts = []
                 for c in range(TAIL_CHUNKS):
                     r0 = c * mc
                     rows = min(mc, m - r0)
@@ -363,8 +371,16 @@ class _AutoPlanner:
                         break
                     ac = _clip_terms(a, r0, rows)
                     T = [] if kind == "syrk" else _clip_terms(b, r0, rows)
-                    self.pb.product(kind, rows, n, k, ac, T, [(out, sign, region)],
-                                    accumulate=int(accumulate or c > 0), group=group)
+                    if self.tail_private:
+                        P = self.alloc(n, k)
+                        self.pb.product(kind, rows, n, k, ac, T, [(P, 1.0)], accumulate=0, group=group)
+                        parts.append(P)
+                    else:
+                        self.pb.product(kind, rows, n, k, ac, T, [(out, sign, region)],
+                                        accumulate=int(accumulate or c > 0), group=group)
+                if parts:
+                    reductions.append((kind, out, sign, accumulate, parts))
+            self._reduce_partials(reductions)
             return
         # chunk-major order: the products of one row chunk are adjacent, so a
         # wave of the persistent grid runs whole chunks (periodic_workers)
@@ -385,8 +401,11 @@ class _AutoPlanner:
                 self.pb.product(kind, rows, n, k, ac, T, [(P, 1.0)], accumulate=0,
                                 group=group)
                 parts[pi].append(P)
-        reductions = [(kind, out, sign, accumulate, parts[pi])
-                      for pi, (kind, m, n, k, a, b, out, sign, accumulate) in enumerate(prods)]
+        self._reduce_partials([(kind, out, sign, accumulate, parts[pi])
+                               for pi, (kind, m, n, k, a, b, out, sign, accumulate) in enumerate(prods)])
+
+    def _reduce_partials(self, reductions):
+        """out (+)= sign * sum(parts) for [(kind, out, sign, accumulate, parts)]."""
         # each product's partials are summed by a chain of combo4 passes; the
         # chains are independent, so passes of equal depth form one multi-node
         # launch (depth-major emission, one group per depth)

@@ -96,3 +96,23 @@ def test_spread_riding_sums_match_blas(m, n, budget, arenas):
     assert carried > 0
     assert np.all(got[np.triu_indices(n, 1)] == SENT)
     assert O.rel_frobenius_lower(got, O.gram_blas(a)) <= 1e-12
+
+
+def test_private_tail_split_matches_blas():
+    """A 343-leaf group (one launch, beyond the shared-destination batch size):
+    its trailing products are K-split into private partials (AutoParams.tail_private)."""
+    from paper_2110_13042_b200.auto_plan import AutoParams, plan_ata_auto, MAX_BATCH_NARROW
+    from paper_2110_13042_b200 import _native as nat
+    m, n = 8192, 4096
+    params = AutoParams(leaf_cols=2048, min_dim=128, max_depth=3, hbm_gbs=1e9, ws_budget_gb=4.0, min_tail_rows=128)
+    plan = plan_ata_auto(m, n, n, n, params)
+    prod = np.isin(plan.ops["type"], (nat.OP_GEMM, nat.OP_SYRK))
+    groups = np.unique(plan.ops["group"][prod], return_counts=True)
+    assert groups[1].max() > MAX_BATCH_NARROW + 20
+    import dataclasses
+    plain = plan_ata_auto(m, n, n, n, dataclasses.replace(params, tail_split=False))
+    assert int(prod.sum()) > int(np.isin(plain.ops["type"], (nat.OP_GEMM, nat.OP_SYRK)).sum())
+    a = np.random.default_rng(11).uniform(-1, 1, (m, n))
+    got, _ = _ata(a, params)
+    assert np.all(got[np.triu_indices(n, 1)] == SENT)
+    assert O.rel_frobenius_lower(got, O.gram_blas(a)) <= 1e-12

@@ -198,3 +198,33 @@ def test_spread_hoist_hides_more_than_the_adjacent_one():
                     else 1.0 * int(o["m"]) * int(o["n"]) * (int(o["n"]) + 1) for o in p2.ops[g0:g1])
         moved = sum(auto_plan._op_bytes(o) for o in p2.ops[i:j])
         assert moved <= 800e9 * flops / (auto_plan.AutoParams().dmma_tflops * 1e12) + 1
+
+
+@pytest.mark.parametrize("m,n,private", [(260, 200, True), (333, 170, True), (260, 200, False)])
+def test_private_tail_of_a_large_group(m, n, private):
+    """A leaf group too large for a shared-destination launch (> MAX_BATCH_NARROW
+    products) K-splits its trailing products into private partials summed by combo4
+    passes behind the group: same result, same multiplications, no regions."""
+    a = np.random.default_rng(m * n).uniform(-1, 1, (m, n))
+    kw = dict(leaf_cols=16, min_dim=4, max_depth=3, hbm_gbs=1e9, ws_budget_gb=1.0, min_tail_rows=2,
+              tail_private=private)
+    p = auto_plan.plan_ata_auto(m, n, n, n, auto_plan.AutoParams(**kw))
+    q = auto_plan.plan_ata_auto(m, n, n, n, auto_plan.AutoParams(**{**kw, "tail_split": False}))
+    ops = p.ops
+    prod = np.isin(ops["type"], (nat.OP_GEMM, nat.OP_SYRK))
+    sizes = {}
+    for o in ops[prod]:
+        sizes[int(o["group"])] = sizes.get(int(o["group"]), 0) + 1
+    big = [g for g, c in sizes.items() if c > auto_plan.MAX_BATCH_NARROW]
+    assert big, "the breadth-first tree has a group beyond one shared-destination launch"
+    regions = {g: any(int(d["region"]) > 0 for o in ops[prod & (ops["group"] == g)] for d in o["d"][:int(o["nd"])])
+               for g in big}
+    assert not any(regions.values())
+    if private:
+        assert int(prod.sum()) > int(np.isin(q.ops["type"], (nat.OP_GEMM, nat.OP_SYRK)).sum())
+    assert p.mults == q.mults
+    c = np.zeros((n, n))
+    c[np.triu_indices(n, 1)] = 7.0
+    plan_interp.run(ops, a, c, 1.0, WS=np.zeros(max(1, p.ws_scalars)))
+    assert np.all(c[np.triu_indices(n, 1)] == 7.0)
+    assert O.rel_frobenius_lower(c, O.gram(a)) <= 1e-12
