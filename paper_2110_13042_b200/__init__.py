@@ -18,7 +18,7 @@ and the formats/callers either side of the path: ATAM ``read_matrix`` /
 ``write_matrix``, the task trees (``build_tree_*``, ``render_tree``) and the
 ``atamul`` command line (``python -m paper_2110_13042_b200.cli``).
 """
-from .ata import AUTO, ata, ata_full, ata_mult_count, workspace_for_ata
+from .ata import AUTO, ata, ata_full, ata_mult_count, release_cached_buffers, workspace_for_ata
 from .distsim import CommStats, ata_d, verify_comm_bounds
 from .errors import (AtamulError, InvalidMeasurementError, NativeError, ProtocolError,
                      ShapeMismatchError, TooManyWorkersError, UnknownProcessError,
@@ -46,7 +46,7 @@ __all__ = [
     "ata", "ata_full", "ata_mult_count", "check_tolerance", "count_allocations",
     "effective_gflops", "fast_strassen", "gen_matrix", "mirror_lower_to_upper",
     "naive_gemm_atb", "naive_syrk_lower", "pack_lower", "split4", "strassen_mult_count",
-    "unpack_lower", "workspace_for", "workspace_for_ata",
+    "unpack_lower", "workspace_for", "workspace_for_ata", "release_cached_buffers",
     # callers / formats either side of the path
     "ComputationType", "Region", "Task", "TaskTree", "build_tree_distributed",
     "build_tree_shared", "leaf_task", "levels_distributed", "levels_shared", "path_to_root",

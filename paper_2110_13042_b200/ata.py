@@ -178,6 +178,22 @@ def _tuned_params(a, c, m, n):
     return autotune.tune(m, n, dev)
 
 
+def release_cached_buffers() -> None:
+    """Drop the device buffers ata() keeps between calls (the two most recent
+    per-shape workspace arenas, the host pipeline's staged C, even-pitch operand
+    copies) and return torch's unused cached blocks to the device -- e.g. after a
+    c4-sized call (110 GB of workspace) when other work needs the HBM."""
+    _WS_CACHE.clear()
+    _PIPE_CIN.clear()
+    _PITCH_CACHE.clear()
+    try:
+        import torch
+        if torch.cuda.is_available():
+            torch.cuda.empty_cache()
+    except ImportError:      # pragma: no cover
+        pass
+
+
 def _default_workspace(m, n, threshold, dtype):
     """ws=None: one arena per (shape, threshold, dtype), kept for the next call
     (the two most recent) -- repeated calls allocate nothing and keep their

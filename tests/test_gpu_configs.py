@@ -71,6 +71,16 @@ def _host_result(name, a):
 
 
 def _run(name, host_path=True):
+    import paper_2110_13042_b200 as P
+    try:
+        _run_config(name, host_path)
+    finally:
+        # the per-shape workspace arenas (c4: 110 GB) must not outlive the test: later
+        # tests start subprocesses that share this GPU
+        P.release_cached_buffers()
+
+
+def _run_config(name, host_path=True):
     from paper_2110_13042_b200.measure import config_matrix
     a = config_matrix(name)
     ref = O.gram_lower_blas(a)

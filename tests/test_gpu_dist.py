@@ -71,6 +71,8 @@ def test_bench_two_ranks_shared_gpu(dist, prefix, port):
     shards and the reference's task tree; the driver's JSON line names the
     partition."""
     import json
+    import paper_2110_13042_b200 as P
+    P.release_cached_buffers()       # the ranks are subprocesses sharing this GPU's memory
     env = dict(os.environ, ATA_DIST_BACKEND="gloo")
     r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
                         "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.join(ROOT, "bench.py"),
