@@ -493,8 +493,15 @@ class _AutoPlanner:
     def _dry_ws(self, a, b, m, n, k, depth) -> int:
         probe = _AutoPlanner(self.p)
         probe.rate, probe.esize = self.rate, self.esize
-        probe.tree(a, b, m, n, k, Win(nat.BASE_C, 0, max(k, 1), n, k), 1.0, True, depth, [], [])
-        return probe.ws_peak
+        leaves = []
+        probe.tree(a, b, m, n, k, Win(nat.BASE_C, 0, max(k, 1), n, k), 1.0, True, depth, leaves, [])
+        extra = 0
+        if self.esize == 8 and self.p.tail_split and self.p.tail_private and len(leaves) > 1:
+            # room for the private partials of a large group's K-split tail (emit_products:
+            # the trailing products covering one wave of tiles, TAIL_CHUNKS partials each)
+            nk = max(lf[1] * lf[2] for lf in leaves)
+            extra = TAIL_CHUNKS * (NUM_SMS * TILE * TILE + 2 * nk)
+        return probe.ws_peak + extra
 
     def ata(self, m: int, n: int, lda: int, ldc: int, round_tf32: bool = False):
         A = Win(nat.BASE_A, 0, lda, m, n)
