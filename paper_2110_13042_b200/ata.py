@@ -226,12 +226,11 @@ def _mark(label, stream):
         ev = torch.cuda.Event(enable_timing=True)
         ev.record(stream)
         PIPE_TRACE.append((label, ev))
-PIPELINE_GEOMETRIC_MIN_RATIO = 4.0    # PIPELINE_GEOMETRIC_BLOCKS geometric blocks from here
-PIPELINE_GEOMETRIC_MIN_RATIO2 = 2.0   # two geometric blocks from here
-PIPELINE_GEOMETRIC_BLOCKS = 3     # measured (tools/e2e_ab.py): c4 e2e 1718 -> 1683 ms at 3 blocks,
-                                  # 4-5 blocks no gain (each block repeats the plan's C-sized work)
+PIPELINE_GEOMETRIC_MIN_RATIO = 1.5    # geometric blocks from this compute / upload ratio (c3: 1.9, c4: 3.8)
+PIPELINE_GEOMETRIC_BLOCKS = 3     # (4 blocks: no gain, each block repeats the plan's C-sized work)
+PIPELINE_GEOMETRIC_GROWTH = 2.5   # rows of block i+1 / rows of block i (_row_blocks)
 PIPELINE_PCIE_GBS = 50.0          # measured pinned H2D on the box (e2e h2d bytes / time)
-PIPELINE_FP64_TFLOPS = 40.0       # effective AtA rate of the fp64 auto plans (bench c3/c4)
+PIPELINE_FP64_TFLOPS = 54.0       # effective AtA rate of the fp64 auto plans (bench c4)
 PIPELINE_TF32_TFLOPS = 460.0
 
 
@@ -586,21 +585,22 @@ def _add_plan(n: int):
 
 
 def _row_blocks(m: int, n: int, es: int, tensor_rate: bool):
-    """Row blocks of the host pipeline.  Each block after the first must cross
-    PCIe while the GPU computes the previous one, and every block repeats the
-    C-sized work of a plan (post-additions, C updates), so: when the per-row
-    compute time exceeds the per-row upload time by `ratio` (fp64: ~n / 6400),
-    use PIPELINE_GEOMETRIC_BLOCKS blocks growing by g = min(4, 0.75 ratio) -- a
-    small first block (short exposed upload), few blocks in total -- when
-    ratio >= 4 (c4), two such blocks when 2 <= ratio < 4 (c3's 2.6: 137.2 -> 135.0 ms
-    against two equal blocks in tools/e2e_c3_probe.py; neutral inside bench.py's c3
-    e2e, 136.0-137.2 ms either way).  Otherwise (TF32: PCIe bound)
-    up to 8 equal blocks of ~PIPELINE_BLOCK_BYTES."""
+    """Row blocks of the host pipeline.  Each block after the first crosses PCIe
+    while the GPU computes the previous ones, and every block repeats the C-sized
+    work of a plan (post-additions, C updates), so compute-bound plans -- per-row
+    compute time over per-row upload time `ratio` >= 1.5 (fp64: ~n / 8600) -- use
+    PIPELINE_GEOMETRIC_BLOCKS blocks growing by PIPELINE_GEOMETRIC_GROWTH: a small
+    first block (short exposed upload; less than half the second, so C can start
+    at zero on the device), few blocks in total.  Measured with the round's final
+    device plans (tools/e2e_blocks.py, profiles/r02n_e2e_blocks.log): c4 1436 ms
+    at growth 3.84 -> 1368-1370 ms at 2.3-2.7, 1399-1440 with four blocks,
+    1402-1616 with two; c3 130 ms with two blocks -> 114-115 ms with three at
+    growth 2.5-3.  Otherwise (TF32: PCIe bound) up to 8 equal blocks of
+    ~PIPELINE_BLOCK_BYTES."""
     rate = (PIPELINE_TF32_TFLOPS if tensor_rate else PIPELINE_FP64_TFLOPS) * 1e12
     ratio = n * PIPELINE_PCIE_GBS * 1e9 / (rate * es)
-    if PIPELINE_GEOMETRIC and ratio >= PIPELINE_GEOMETRIC_MIN_RATIO2:
-        g = min(4.0, 0.75 * ratio)
-        R = PIPELINE_GEOMETRIC_BLOCKS if ratio >= PIPELINE_GEOMETRIC_MIN_RATIO else 2
+    if PIPELINE_GEOMETRIC and ratio >= PIPELINE_GEOMETRIC_MIN_RATIO:
+        g, R = PIPELINE_GEOMETRIC_GROWTH, PIPELINE_GEOMETRIC_BLOCKS
         w = [g ** i for i in range(R)]
         cuts = [0]
         for i in range(R - 1):
