@@ -29,6 +29,9 @@
 #include <cudaTypedefs.h>
 
 #include <cstdlib>
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 
 #include "ata_common.cuh"
@@ -766,11 +769,39 @@ cudaError_t launch_tf32_2sm(const DProd<float>* prods, int count, double alpha, 
       cfg.blockDim = dim3(THREADS, 1, 1);
       cfg.dynamicSmemBytes = smem;
       cfg.stream = s;
-      cudaLaunchAttribute attrs[1];
+      cudaLaunchAttribute attrs[2];
       attrs[0].id = cudaLaunchAttributeCooperative;
       attrs[0].val.cooperative = 1;
       cfg.attrs = attrs;
       cfg.numAttrs = 1;
+      // ATA_TF32_RING_PIN=1 (A/B): an L2 access-policy window over the two rings marks
+      // their lines persisting (slots are re-read by every tile of the wave) and the
+      // launch's other traffic streaming
+      static const bool pin = std::getenv("ATA_TF32_RING_PIN") != nullptr;
+      if (pin) {
+        int dev = 0, max_persist = 0, max_window = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
+        cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+        const size_t ring_bytes = (size_t)2 * a.rg.nslot * PR * a.rg.ncols * sizeof(float);
+        if (max_persist > 0 && max_window > 0) {
+          cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, (size_t)max_persist);
+          const size_t win = std::min(ring_bytes, (size_t)max_window);
+          attrs[1].id = cudaLaunchAttributeAccessPolicyWindow;
+          attrs[1].val.accessPolicyWindow.base_ptr = a.rg.ring[0];
+          attrs[1].val.accessPolicyWindow.num_bytes = win;
+          attrs[1].val.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)max_persist / (double)win);
+          attrs[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+          attrs[1].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+          cfg.numAttrs = 2;
+          static bool said = false;
+          if (!said) {
+            said = true;
+            std::fprintf(stderr, "[ata] TF32 ring pinned: ring %zu B, window %zu B, persisting L2 %d B\n", ring_bytes,
+                         win, max_persist);
+          }
+        }
+      }
       e = cudaLaunchKernelEx(&cfg, prod_tf32_2sm_kernel, a);
     } else {
       prod_tf32_2sm_kernel<<<clusters * 2, THREADS, smem, s>>>(a);
